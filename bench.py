@@ -1,0 +1,285 @@
+"""Benchmark: particle-steps/s (N*T/s) of the full particle-learning cycle.
+
+Workload (BASELINE.json configs[2]): the paper's trend+noise model, particle
+learning of sigma2 and tau2 with Priors() (IG(5,4), IG(5,0.4), x0~N(0,10)),
+N = 2^24 particles, T = 1000 synthetic observations simulated from aux
+stream 2^62+1 (bench.py:36 of the reference), seed 0, cut-point resampler,
+fp64, track_quantiles=False -- exactly the reference bench's par_cutpoint
+cell (bench.py:28-34,130-143), so parameter mean/sd/5 quantiles are computed
+every step.  One bench "step" = one complete filter run (init + T time
+steps).  State arrays (2 x 512 MiB records + 128 MiB log-weights ...) are
+far larger than the 126 MB L2, so no explicit flush is needed.
+
+  value  = N*T*K / (device time of K resident runs, CUDA events), max over ranks
+  e2e    = same metric through the public API run_particle_learning() with a
+           host y and host outputs (host->device and device->host inside)
+  --impl reference  times the reference's CPU algorithm (oracle port, numpy +
+           scipy, all host threads as Backend lanes) on a bounded sample.
+
+Multi-GPU (--gpus N under torchrun): every rank runs its own N-particle
+filter (replicas; weak scaling); the barrier + max-over-ranks timing stays.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ALG_BYTES_STEP_KERNEL = 84  # lookup 12 + gather 32 + write 32 + log-weight 8
+ALG_BYTES_CYCLE = 112       # whole PL cycle per particle-step
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._loop, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > i + 2 and r[i + 2].lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def cpu_reference_run(n, t_len, lanes):
+    """The reference's par_cutpoint cell restated (oracle port), timed."""
+    from oracle import restate as R
+
+    _, y = R.simulate(1.0, 0.1, 0.0, t_len, 0)
+    pool = R.Lanes(lanes)
+    try:
+        R.run_loop(y[:1], min(n, 1024), 0, track_quantiles=False, lanes=pool)  # warm-up
+        t0 = time.perf_counter()
+        R.run_loop(y, n, 0, track_quantiles=False, lanes=pool)
+        dt = time.perf_counter() - t0
+    finally:
+        pool.close()
+    return n * t_len / dt, dt
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return
+    lanes = os.cpu_count() or 1
+    n, t_len = args.ref_n, args.ref_t
+    vals = []
+    for _ in range(args.warmup):
+        cpu_reference_run(n, max(2, t_len // 4), lanes)
+    for _ in range(args.steps):
+        v, _ = cpu_reference_run(n, t_len, lanes)
+        vals.append(v)
+    vals.sort()
+    value = vals[len(vals) // 2]
+    line = {
+        "impl": "reference",
+        "metric": "particle-steps/sec (N*T/s), full particle-learning cycle",
+        "value": value, "unit": "particle-steps/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": n * t_len / value * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"PL trend+noise, Priors(), cutpoint, N={args.n}, T={args.t} "
+                               f"(CPU sample N={n}, T={t_len})", "N": args.n, "T": args.t},
+        "cpu_baseline": {"value": value, "unit": "particle-steps/s", "cores": lanes,
+                         "kind": "port",
+                         "sample": f"oracle/restate.py run_loop N={n} T={t_len}, {lanes} lanes"},
+        "e2e": {"value": value, "unit": "particle-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def load_traffic():
+    """ncu dram bytes per step-kernel launch, from the committed profile summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "step_kernel_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=1 << 24)
+    ap.add_argument("--t", type=int, default=1000)
+    ap.add_argument("--ref-n", type=int, default=1 << 16)
+    ap.add_argument("--ref-t", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference_arm(args, world, rank)
+        return
+
+    import numpy as np
+
+    import paper_1212_1639_b200 as P
+    from paper_1212_1639_b200 import _lib
+
+    lib = _lib.require_device()
+    n, t_len = args.n, args.t
+    _, y = P.simulate(P.TrendNoiseModel(), t_len, P.RngStream(0, P.rng.AUX_STREAM_BASE + 1))
+    backend = P.Backend("cuda", device=local)
+    # first call: engine creation + gamma tables (excluded, like the
+    # reference bench's numba warm-up, bench.py:153-161)
+    P.run_particle_learning(P.Priors(), y, n, seed=0, backend=backend, track_quantiles=False)
+    eng = next(iter(backend._engines.values()))
+    cfg = eng.cfg
+    for _ in range(args.warmup):
+        eng.run_resident(t_len)
+    # ---- value: K resident runs, device events
+    barrier(world)
+    k0 = lib.pf_launch_count()
+    step_ms = []
+    with ClockSampler(local) as clk:
+        tot_ms = 0.0
+        for _ in range(args.steps):
+            eng.run_resident(t_len)
+            tm = eng.last_timing()
+            tot_ms += tm["total_ms"]
+            step_ms.append(tm["step_kernel_ms"])
+    launches = lib.pf_launch_count() - k0
+    barrier(world)
+    tot_ms = max_over_ranks(tot_ms, world)
+    value = world * n * t_len * args.steps / (tot_ms / 1e3)
+    # ---- e2e: public API, host y in / host summaries out
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        out = P.run_particle_learning(P.Priors(), y, n, seed=0, backend=backend,
+                                      track_quantiles=False)
+        _ = out.param_posterior["sigma2"].mean[-1]
+    e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+    e2e = world * n * t_len * args.steps / e2e_s
+    d2h = 8 * t_len * (1 + 2 * 7)  # filtered mean + 2 params x (mean, sd, 5 quantiles)
+    h2d = 8 * t_len + _lib.C.sizeof(_lib.PfConfig)
+    backend.close()
+    del cfg
+
+    peak, peak_kind = _peaks()
+    kern_ms = float(np.mean(step_ms))
+    achieved = ALG_BYTES_STEP_KERNEL * n / (kern_ms / 1e3) / 1e9
+    traffic = load_traffic()
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        lanes = os.cpu_count() or 1
+        v, dt = cpu_reference_run(args.ref_n, args.ref_t, lanes)
+        cpu = {"value": v, "unit": "particle-steps/s", "cores": lanes, "kind": "port",
+               "sample": f"oracle/restate.py run_loop N={args.ref_n} T={args.ref_t} "
+                         f"({dt:.1f} s, {lanes} lanes)"}
+    if rank == 0:
+        line = {
+            "metric": "particle-steps/sec (N*T/s), full particle-learning cycle",
+            "value": value, "unit": "particle-steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"PL trend+noise, Priors(), cutpoint, N=2^{n.bit_length() - 1}, "
+                                   f"T={t_len}, seed 0, track_quantiles=False",
+                       "N": n, "T": t_len, "parallelism": f"replicas x{world}",
+                       "l2": "working set >> L2 (no flush needed)"},
+            "e2e": {"value": e2e, "unit": "particle-steps/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "roofline": {"bound": "hbm", "kernel": "step_kernel", "achieved": achieved,
+                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": achieved / peak,
+                         "traffic": None if traffic is None else traffic.get("bytes_per_launch"),
+                         "alg_bytes_per_particle": ALG_BYTES_STEP_KERNEL,
+                         "step_kernel_ms": kern_ms,
+                         "cycle_frac": ALG_BYTES_CYCLE * n * t_len / (tot_ms / args.steps / 1e3) / 1e9 / peak},
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

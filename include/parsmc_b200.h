@@ -1,0 +1,185 @@
+/*
+ * parsmc_b200.h -- C ABI of the B200-native particle filtering / particle
+ * learning engine (libparsmc_b200.so).
+ *
+ * Plain pointers and sizes only; no torch or CUDA types cross this boundary.
+ * Every entry point returns a status code (PF_OK on success); the message and
+ * failing time step of the last error on the calling thread are available
+ * from pf_last_error_message() / pf_last_error_step().  Codes map 1:1 onto
+ * the reference's exception classes (parsmc errors.py:4-35):
+ *
+ *   PF_ERR_ALL_WEIGHTS_ZERO   AllWeightsZeroError(step=t)  filtering.py:294-296,
+ *                                                          prefix_sum.py:97-100
+ *   PF_ERR_NON_FINITE_WEIGHT  NonFiniteWeightError         core.py:26-27
+ *   PF_ERR_NOT_POWER_OF_TWO   NotPowerOfTwoError           core.py:16-18
+ *   PF_ERR_VALUE              ValueError                   filtering.py:205-208
+ *
+ * Reference paths below are relative to the reference's pkg/src/parsmc/.
+ * Indices crossing the boundary are 1-based int64, as in the reference
+ * (resampling.py:15-16).
+ */
+#ifndef PARSMC_B200_H
+#define PARSMC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  PF_OK = 0,
+  PF_ERR_ALL_WEIGHTS_ZERO = 1,
+  PF_ERR_NON_FINITE_WEIGHT = 2,
+  PF_ERR_NOT_POWER_OF_TWO = 3,
+  PF_ERR_VALUE = 4,
+  PF_ERR_CUDA = 5,
+  PF_ERR_OUT_OF_MEMORY = 6,
+  PF_ERR_NOT_IMPLEMENTED = 7
+};
+
+enum { PF_DTYPE_F64 = 0, PF_DTYPE_F32 = 1 };
+
+/* ------------------------------------------------------------ library --- */
+const char* pf_version(void);
+const char* pf_last_error_message(void);
+int64_t pf_last_error_step(void);
+/* Number of visible CUDA devices (0 on a host without a GPU; never fails). */
+int pf_device_count(void);
+/* Kernels launched by this process so far (the bench's gpu_launches). */
+int64_t pf_launch_count(void);
+
+/* ------------------------------------------------------ engine (L3) --- */
+/* Replaces filtering._run_loop (filtering.py:200-374) behind
+ * run_particle_learning (filtering.py:178-197) and run_particle_filter
+ * (filtering.py:165-175).  One engine = one device-resident particle system
+ * of n slots; runs are repeatable and bit-identical for a fixed seed. */
+typedef struct pf_config {
+  int64_t n;               /* particle count, a power of two (cut-point) */
+  uint64_t seed;           /* Philox key word 0; slot j uses stream j */
+  int32_t learn;           /* 1: run_particle_learning, 0: run_particle_filter */
+  int32_t learn_sigma2;    /* sigma2 ~ IG(shape, scale) learned (models.py:82-88) */
+  int32_t learn_tau2;
+  int32_t precision;       /* PF_DTYPE_F64 ("double") / PF_DTYPE_F32 ("single") */
+  double x0_mean, x0_var;
+  double sqrt_x0_var;      /* math.sqrt(x0_var), host-computed (filtering.py:235) */
+  double sigma2_shape, sigma2_scale;
+  double tau2_shape, tau2_scale;
+  double sigma2_fixed;     /* used when the parameter is not learned */
+  double tau2_fixed;
+  double sqrt_tau2_fixed;  /* np.sqrt(tau2) (filtering.py:274) */
+  double log_term_fixed;   /* -0.5*(LOG_TWO_PI + np.log(sigma2)) (filtering.py:293) */
+  int32_t track_quantiles; /* weighted 5/50/95% state quantiles per step */
+  int32_t keep_indices;    /* resampled_indices [T, n] (1-based) */
+  int32_t keep_final;      /* final_particles */
+  int32_t store_particles; /* particle_history, one snapshot per step */
+  int32_t phase_timing;    /* per-phase CUDA-event timings (PhaseTimings) */
+  int32_t gamma_method;    /* 0: per-step table (default), 1: accurate per draw */
+  int32_t device;          /* CUDA device ordinal */
+  int32_t reserved;
+} pf_config;
+
+/* Oracle mode: host arrays [T+1][n] (row 0 = initialisation) that replace the
+ * ndtri / gammaincinv outputs (and optionally the normalised weights) with
+ * the reference's own draws.  NULL members are computed on the device. */
+typedef struct pf_feed {
+  const double* z;        /* ndtri(u)        rng.py:223-224 */
+  const double* g_sigma;  /* gammaincinv     rng.py:226-229, filtering.py:280 */
+  const double* g_tau;    /*                 filtering.py:286 */
+  const double* w;        /* exp(lw - max)   filtering.py:297 (rows 1..T) */
+} pf_feed;
+
+/* Caller-allocated host outputs; NULL members are not produced. */
+typedef struct pf_outputs {
+  double* filtered_mean;        /* [T] */
+  double* filtered_quantiles;   /* [T][3]  probs (0.05, 0.5, 0.95) */
+  double* sigma2_mean;          /* [T] */
+  double* sigma2_sd;            /* [T] */
+  double* sigma2_quantiles;     /* [T][5]  probs (0.005, 0.05, 0.5, 0.95, 0.995) */
+  double* tau2_mean;
+  double* tau2_sd;
+  double* tau2_quantiles;
+  int64_t* indices;             /* [T][n] 1-based ancestors */
+  /* final particles (post-resample system at step T; init system if T == 0) */
+  double* final_states;         /* [n] (float32 values when precision single) */
+  double* final_sigma2;         /* [n] */
+  double* final_tau2;
+  double* final_a_sigma;
+  double* final_b_sigma;
+  double* final_a_tau;
+  double* final_b_tau;
+  /* store_particles: [T][n] snapshots of the same seven arrays */
+  double* hist_states;
+  double* hist_sigma2;
+  double* hist_tau2;
+  double* hist_a_sigma;
+  double* hist_b_sigma;
+  double* hist_a_tau;
+  double* hist_b_tau;
+  /* PhaseTimings (filtering.py:44-74): initialize, cdf, resample,
+   * resample_sort_only, propagate, store, other (nanoseconds) */
+  int64_t phase_ns[7];
+  int64_t failed_step;          /* step of AllWeightsZeroError, else 0 */
+} pf_outputs;
+
+typedef struct pf_engine pf_engine;
+
+int pf_engine_create(const pf_config* cfg, pf_engine** out);
+/* Replace the model / seed / output flags of an engine; n, precision and
+ * device must not change (the device buffers are sized by them). */
+int pf_engine_reconfigure(pf_engine* e, const pf_config* cfg);
+int pf_engine_run(pf_engine* e, const double* y, int64_t t_len,
+                  const pf_feed* feed, pf_outputs* out);
+/* Device-resident repeat of the last run's workload: y is already on the
+ * device; no host outputs are copied.  Used by bench.py for the kernel-only
+ * throughput (value); pf_engine_run is the end-to-end path (e2e). */
+int pf_engine_run_resident(pf_engine* e, int64_t t_len);
+/* Device time (ms, CUDA events) of the last run / resident run, and the
+ * average duration and launch count of the step kernel inside it. */
+int pf_engine_last_timing(pf_engine* e, double* total_ms, double* step_kernel_ms,
+                          int64_t* step_kernel_launches, int64_t* kernels_launched);
+int pf_engine_destroy(pf_engine* e);
+
+/* ------------------------------------------------- kernel level (L2) --- */
+/* All kernel-level entries take HOST pointers and run synchronously on the
+ * current device; they exist for parity tests and for the reference's
+ * kernel-level API surface. */
+
+/* philox_block_lanes (rng.py:103-110): words_out is [4][n]. */
+int pf_philox_block(uint64_t seed, const uint64_t* stream_ids, int64_t n,
+                    uint64_t block, uint64_t* words_out);
+/* philox4x64_block (rng.py:49-63) with arbitrary counters: counters is
+ * [4][n] (c0..c3), keys [2][n] (k0, k1), words_out [4][n]. */
+int pf_philox4x64(const uint64_t* counters, const uint64_t* keys, int64_t n, uint64_t* words_out);
+/* uniforms_at (rng.py:122-140). */
+int pf_uniforms_at(uint64_t seed, const uint64_t* stream_ids,
+                   const uint64_t* counters, int64_t n, double* u_out);
+/* scipy.special.ndtri as used at rng.py:223-224. */
+int pf_ndtri(const double* u, int64_t n, double* out);
+/* scipy.special.gammaincinv(a, u) as used at rng.py:226-229.  method 0 uses
+ * the per-step table (hot path), 1 the accurate Halley solver. */
+int pf_gammaincinv(double a, const double* u, int64_t n, int32_t method, double* out);
+/* parallel_cdf (prefix_sum.py:109-127): w -> q, dtype PF_DTYPE_F64/F32.
+ * total_out (optional) receives the adder-tree root. */
+int pf_tree_cdf(const void* w, int64_t n, int32_t dtype, void* q_out, double* total_out);
+/* forward_adder + backward_adder (prefix_sum.py:46-91): levels_out holds the
+ * 2n-1 tree nodes level by level (level 0 first), prefix_out the inclusive
+ * prefix sums. */
+int pf_adder_tree(const void* w, int64_t n, int32_t dtype, void* levels_out, void* prefix_out);
+/* cut_points_parallel (resampling.py:110-134): 1-based cut table. */
+int pf_cut_table(const void* q, int64_t n, int32_t dtype, int64_t* cuts_out);
+/* cutpoint_indices (resampling.py:146-158) over m uniforms. */
+int pf_cutpoint_lookup(const void* q, const int64_t* cuts, int64_t n, int32_t dtype,
+                       const double* u, int64_t m, int64_t* idx_out);
+/* resample_cutpoint (resampling.py:161-177): uniforms of streams 0..n-1 at
+ * `counter`, cut table, lookup. */
+int pf_resample_cutpoint(const void* q, int64_t n, int32_t dtype, uint64_t seed,
+                         uint64_t counter, int64_t* idx_out);
+/* weighted_quantiles (filtering.py:135-140); weights dtype PF_DTYPE_F64/F32. */
+int pf_weighted_quantiles(const double* values, const void* weights, int32_t wdtype,
+                          int64_t n, const double* probs, int32_t nprobs, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARSMC_B200_H */

@@ -1,0 +1,93 @@
+"""Execution backend: the seam through which callers select the device.
+
+The reference's ``Backend(mode, lanes, min_chunk)`` (backend.py:15-82) owns a
+thread pool of CPU worker lanes.  Here the same object owns the *device
+engines*: one resident particle system per (model, n, seed, flags)
+configuration, reused across calls until ``close()``.  Every mode runs on the
+GPU -- ``"sequential"`` / ``"parallel"`` are accepted so existing callers are
+drop-in, and because the reference's results never depend on the lane count
+(backend.py:1-8) mapping them onto the device preserves its semantics.
+``lanes`` and ``min_chunk`` keep their meaning for ``split``.
+"""
+
+from __future__ import annotations
+
+from . import _lib
+
+MODES = ("cuda", "sequential", "parallel")
+
+
+class Backend:
+    """Device engine owner.
+
+    Parameters
+    ----------
+    mode : {"cuda", "sequential", "parallel"}
+        All modes execute on the CUDA device.
+    lanes : int
+        Kept for API compatibility (``split``); has no effect on results.
+    min_chunk : int
+        Kept for API compatibility (``split``).
+    device : int
+        CUDA device ordinal.
+    """
+
+    def __init__(self, mode="cuda", lanes=1, min_chunk=4096, device=0):
+        if mode not in MODES:
+            raise ValueError(f"unknown backend mode: {mode!r}")
+        if lanes < 1:
+            raise ValueError("lanes must be >= 1")
+        self.mode = mode
+        self.lanes = lanes if mode == "parallel" else 1
+        self.min_chunk = min_chunk
+        self.device = int(device)
+        self._engines = {}
+
+    def split(self, n):
+        """Contiguous lane ranges covering [0, n) (backend.py:39-50)."""
+        k = min(self.lanes, max(1, n // self.min_chunk))
+        base, extra = divmod(n, k)
+        out, lo = [], 0
+        for i in range(k):
+            hi = lo + base + (1 if i < extra else 0)
+            if hi > lo:
+                out.append((lo, hi))
+            lo = hi
+        return out
+
+    def engine(self, key, factory):
+        """The cached engine for ``key`` (created by ``factory()`` once)."""
+        eng = self._engines.get(key)
+        if eng is None:
+            eng = factory()
+            self._engines[key] = eng
+        return eng
+
+    def close(self):
+        for eng in self._engines.values():
+            eng.close()
+        self._engines.clear()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __repr__(self):
+        return f"Backend(mode={self.mode!r}, lanes={self.lanes}, device={self.device})"
+
+
+def device_available():
+    """True when the C-ABI library loads and sees a CUDA device."""
+    try:
+        return _lib.device_count() > 0
+    except Exception:
+        return False

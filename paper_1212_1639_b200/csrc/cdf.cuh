@@ -1,0 +1,413 @@
+// Resampling CDF by the paper's two-pass adder tree, bit-identical to the
+// reference (prefix_sum.py:46-106), plus the cut-point table and lookup
+// (resampling.py:110-158).
+//
+// The reference builds the tree level by level over all N weights:
+//   forward   levels[d][i] = levels[d-1][2i] + levels[d-1][2i+1]   (:64)
+//   backward  right child = parent, left child = parent - w[right]  (:86-87)
+//   finalize  q = s/total, running max, clip [0,1], q[N-1] = 1      (:94-106)
+// Any power-of-two aligned tile is a subtree of that tree, so the device
+// splits it into
+//   K2 cdf_reduce  : per 2048-element tile, the exact subtree sum (thread
+//                    pairwise tree -> warp xor-butterfly -> 8-warp tree),
+//                    and per chunk of R tiles the subtree over tile sums;
+//   K3 cdf_top     : one CTA, the tree over chunk sums -> root, then the
+//                    top-down backward pass to every chunk node, and the
+//                    exclusive running max of chunk node values (a leaf
+//                    never exceeds its subtree node, so a chunk's max q is
+//                    its node value / total);
+//   K4 cdf_expand  : per tile, rebuild the subtree, run the backward pass
+//                    from the tile node, divide, running max, clip, pin,
+//                    and scatter the cut-point table L_j = ceil(N q_j).
+// Addition is commutative in IEEE arithmetic, so the butterfly computes
+// node(2i)+node(2i+1) exactly as the reference does.
+#pragma once
+#include <math.h>
+
+#include "common.cuh"
+
+namespace pf {
+
+constexpr int CDF_THREADS = 256;
+constexpr int CDF_V = 8;                         // consecutive elements per thread
+constexpr int CDF_TILE = CDF_THREADS * CDF_V;    // 2048
+constexpr int CDF_MAX_CHUNKS = 4096;             // top tree lives in one CTA
+constexpr int CDF_SMALL_MAX = 1024;              // n <= this: single-CTA path
+
+// Weight source: mode 0 -> w = exp(src - M) (the reference's
+// np.exp(log_w - shift), filtering.py:297); mode 1 -> w = src.
+struct WSrc {
+  const double* src;
+  const double* M;  // device scalar (mode 0)
+  int mode;
+};
+
+template <typename T>
+PF_D T weight_of(double v, double M, int mode) {
+  return mode == 0 ? (T)exp(v - M) : (T)v;
+}
+
+template <typename T>
+PF_D void load_tile_weights(const WSrc& s, int64_t base, double M, T (&v)[CDF_V]) {
+  const double2* p = reinterpret_cast<const double2*>(s.src + base);
+#pragma unroll
+  for (int k = 0; k < CDF_V / 2; ++k) {
+    double2 d = p[k];
+    v[2 * k] = weight_of<T>(d.x, M, s.mode);
+    v[2 * k + 1] = weight_of<T>(d.y, M, s.mode);
+  }
+}
+
+// Tile plan for n >= CDF_TILE: G0 tiles of 2048, chunks of R tiles.
+struct CdfPlan {
+  int64_t n;
+  int64_t tiles;
+  int64_t chunks;
+  int R;
+  bool small;
+};
+
+inline CdfPlan cdf_plan(int64_t n) {
+  CdfPlan p;
+  p.n = n;
+  p.small = n < CDF_TILE;
+  if (p.small) {
+    p.tiles = p.chunks = 1;
+    p.R = 1;
+    return p;
+  }
+  p.tiles = n / CDF_TILE;
+  p.R = 1;
+  while (p.tiles / p.R > CDF_MAX_CHUNKS) p.R *= 2;
+  p.chunks = p.tiles / p.R;
+  return p;
+}
+
+// Exact tree over 8 values held by thread: returns the three levels.
+template <typename T>
+PF_D void thread_tree8(const T (&v)[8], T (&l1)[4], T (&l2)[2], T& l3) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) l1[i] = v[2 * i] + v[2 * i + 1];
+  l2[0] = l1[0] + l1[1];
+  l2[1] = l1[2] + l1[3];
+  l3 = l2[0] + l2[1];
+}
+
+// ------------------------------------------------------------------ K2 ---
+template <typename T>
+__global__ void __launch_bounds__(CDF_THREADS)
+cdf_reduce_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ chunk_tot,
+                  const int64_t* __restrict__ fail) {
+  if (fail && *fail) return;
+  __shared__ T wt[CDF_THREADS / 32];
+  __shared__ T tt[64];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double M = src.mode == 0 ? *src.M : 0.0;
+  const int64_t chunk = blockIdx.x;
+  for (int r = 0; r < R; ++r) {
+    const int64_t tile = chunk * R + r;
+    T v[CDF_V], l1[4], l2[2], g;
+    load_tile_weights<T>(src, tile * CDF_TILE + threadIdx.x * CDF_V, M, v);
+    thread_tree8<T>(v, l1, l2, g);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) g = g + __shfl_xor_sync(0xffffffffu, g, o);
+    if (lane == 0) wt[warp] = g;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      T a0 = wt[0] + wt[1], a1 = wt[2] + wt[3], a2 = wt[4] + wt[5], a3 = wt[6] + wt[7];
+      T tot = (a0 + a1) + (a2 + a3);
+      tt[r] = tot;
+      tile_tot[tile] = tot;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    for (int len = R; len > 1; len >>= 1)
+      for (int i = 0; i < len / 2; ++i) tt[i] = tt[2 * i] + tt[2 * i + 1];
+    chunk_tot[chunk] = tt[0];
+  }
+}
+
+// ------------------------------------------------------------------ K3 ---
+// One CTA of 1024 threads; dynamic smem = (2G + 2G) * sizeof(T).
+template <typename T>
+__global__ void __launch_bounds__(1024)
+cdf_top_kernel(const T* __restrict__ chunk_tot, int64_t G, T* __restrict__ node,
+               T* __restrict__ carry, T* __restrict__ total_out, int64_t* fail, int64_t step) {
+  if (fail && *fail) return;
+  extern __shared__ unsigned char smem_raw[];
+  T* fw = reinterpret_cast<T*>(smem_raw);  // forward levels, 2G-1 nodes
+  T* b0 = fw + 2 * G;                       // backward ping
+  T* b1 = b0 + G;                           // backward pong
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int64_t i = tid; i < G; i += nt) fw[i] = chunk_tot[i];
+  __syncthreads();
+  int64_t off = 0, len = G;
+  while (len > 1) {
+    for (int64_t i = tid; i < len / 2; i += nt) fw[off + len + i] = fw[off + 2 * i] + fw[off + 2 * i + 1];
+    __syncthreads();
+    off += len;
+    len >>= 1;
+  }
+  const T total = fw[off];
+  // backward: level offsets from the top down
+  T* par = b0;
+  T* chi = b1;
+  if (tid == 0) par[0] = total;
+  __syncthreads();
+  int64_t plen = 1;
+  int64_t loff = off;  // offset of the parent level in fw
+  while (plen < G) {
+    const int64_t clen = plen * 2;
+    const int64_t coff = loff - clen;
+    for (int64_t i = tid; i < clen; i += nt) {
+      const T p = par[i >> 1];
+      chi[i] = (i & 1) ? p : (T)(p - fw[coff + i + 1]);
+    }
+    __syncthreads();
+    T* tmp = par;
+    par = chi;
+    chi = tmp;
+    plen = clen;
+    loff = coff;
+  }
+  // par[0..G) = chunk node values.  Exclusive running max -> carry
+  // (max is exact, so any scan order gives the reference's
+  // np.maximum.accumulate bits).
+  for (int64_t i = tid; i < G; i += nt) node[i] = par[i];
+  {
+    __shared__ T wm[32];
+    const int64_t per = (G + nt - 1) / nt;
+    const int64_t lo = tid * per;
+    const int64_t hi = lo + per < G ? lo + per : G;
+    T loc = (T)(-INFINITY);
+    for (int64_t i = lo; i < hi; ++i) loc = fmax(loc, par[i]);
+    const int lane = tid & 31, warp = tid >> 5;
+    T incl = loc;
+    for (int o = 1; o < 32; o <<= 1) {
+      const T other = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl = fmax(incl, other);
+    }
+    if (lane == 31) wm[warp] = incl;
+    __syncthreads();
+    T pre = (T)(-INFINITY);
+    for (int w = 0; w < warp; ++w) pre = fmax(pre, wm[w]);
+    T ex = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane > 0) pre = fmax(pre, ex);
+    for (int64_t i = lo; i < hi; ++i) {
+      carry[i] = pre;
+      pre = fmax(pre, par[i]);
+    }
+  }
+  if (tid == 0) {
+    *total_out = total;
+    if (!(total > (T)0) || !isfinite((double)total)) {
+      if (fail) atomicCAS((unsigned long long*)fail, 0ull, (unsigned long long)(-step));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K4 ---
+template <typename T>
+PF_D T clip01(T x) { return fmin(fmax(x, (T)0), (T)1); }
+
+template <typename T>
+__global__ void __launch_bounds__(CDF_THREADS)
+cdf_expand_kernel(WSrc src, int64_t n, int R, const T* __restrict__ tile_tot,
+                  const T* __restrict__ node, const T* __restrict__ carry,
+                  const T* __restrict__ total_p, T* __restrict__ q_out,
+                  int32_t* __restrict__ cut_out, const int64_t* __restrict__ fail) {
+  if (fail && *fail) return;
+  __shared__ T wt[CDF_THREADS / 32];
+  __shared__ T wmax[CDF_THREADS / 32];
+  __shared__ T tnode[64], tcarry[64];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double M = src.mode == 0 ? *src.M : 0.0;
+  const T total = *total_p;
+  const T nf = (T)n;
+  const int64_t chunk = blockIdx.x;
+  if (threadIdx.x == 0) {
+    // subtree over this chunk's R tile sums: forward, then backward from the
+    // chunk node; per-tile carries of the running max.
+    T fwl[128];  // R <= 32 (n <= 2^28)
+    for (int r = 0; r < R; ++r) fwl[r] = tile_tot[chunk * R + r];
+    int offs[8], k = 0, off = 0, len = R;
+    offs[k++] = 0;
+    while (len > 1) {
+      for (int i = 0; i < len / 2; ++i) fwl[off + len + i] = fwl[off + 2 * i] + fwl[off + 2 * i + 1];
+      off += len;
+      len >>= 1;
+      offs[k++] = off;
+    }
+    T bw[64], nb[64];
+    bw[0] = node[chunk];
+    int plen = 1;
+    for (int lvl = k - 2; lvl >= 0; --lvl) {
+      const int co = offs[lvl];
+      for (int i = 0; i < plen * 2; ++i) nb[i] = (i & 1) ? bw[i >> 1] : (T)(bw[i >> 1] - fwl[co + i + 1]);
+      plen *= 2;
+      for (int i = 0; i < plen; ++i) bw[i] = nb[i];
+    }
+    T m = carry[chunk];
+    for (int r = 0; r < R; ++r) {
+      tnode[r] = bw[r];
+      tcarry[r] = m;
+      m = fmax(m, bw[r]);
+    }
+  }
+  __syncthreads();
+  for (int r = 0; r < R; ++r) {
+    const int64_t tile = chunk * R + r;
+    const int64_t base = tile * CDF_TILE + threadIdx.x * CDF_V;
+    T v[CDF_V], l1[4], l2[2], l3;
+    load_tile_weights<T>(src, base, M, v);
+    thread_tree8<T>(v, l1, l2, l3);
+    T p[5];
+    T g = l3;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      p[k] = __shfl_xor_sync(0xffffffffu, g, 1 << k);
+      g = g + p[k];
+    }
+    if (lane == 0) wt[warp] = g;
+    __syncthreads();
+    // backward: tile node -> warp node (3 levels over 8 warp sums)
+    T val = tnode[r];
+    {
+      const T a0 = wt[0] + wt[1], a1 = wt[2] + wt[3], a2 = wt[4] + wt[5], a3 = wt[6] + wt[7];
+      const T b0 = a0 + a1, b1 = a2 + a3;
+      const T A[4] = {a0, a1, a2, a3};
+      if (!((warp >> 2) & 1)) val = val - b1;
+      const int h = warp >> 1;  // pair index 0..3
+      if (!(h & 1)) val = val - A[h + 1];
+      if (!(warp & 1)) val = val - wt[warp + 1];
+      (void)b0;
+    }
+    // warp node -> lane node
+#pragma unroll
+    for (int k = 4; k >= 0; --k)
+      if (!((lane >> k) & 1)) val = val - p[k];
+    // lane node -> 8 leaves
+    T s[CDF_V];
+    {
+      const T n2l = val - l2[1], n2r = val;
+      const T n1[4] = {n2l - l1[1], n2l, n2r - l1[3], n2r};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        s[2 * i] = n1[i] - v[2 * i + 1];
+        s[2 * i + 1] = n1[i];
+      }
+    }
+    // q = s / total, thread-local running max
+    T run[CDF_V];
+    T m = (T)(-INFINITY);
+#pragma unroll
+    for (int i = 0; i < CDF_V; ++i) {
+      const T qi = s[i] / total;
+      m = fmax(m, qi);
+      run[i] = m;
+    }
+    // exclusive prefix max across lanes and warps, seeded by the tile carry
+    T incl = m;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T other = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl = fmax(incl, other);
+    }
+    T excl = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) excl = (T)(-INFINITY);
+    __syncthreads();  // wt reads done before wmax reuse ordering
+    if (lane == 31) wmax[warp] = incl;
+    __syncthreads();
+    T pre = tcarry[r];
+    for (int w = 0; w < warp; ++w) pre = fmax(pre, wmax[w]);
+    pre = fmax(pre, excl);
+    // finalize and scatter the cut table
+    T qv[CDF_V];
+    int64_t Lprev = (int64_t)ceil(clip01(pre) * nf);
+#pragma unroll
+    for (int i = 0; i < CDF_V; ++i) {
+      T qi = clip01(fmax(pre, run[i]));
+      if (base + i == n - 1) qi = (T)1;
+      qv[i] = qi;
+      const int64_t L = (int64_t)ceil(qi * nf);
+      for (int64_t kk = Lprev; kk < L; ++kk) cut_out[kk] = (int32_t)(base + i);
+      Lprev = L > Lprev ? L : Lprev;
+    }
+#pragma unroll
+    for (int i = 0; i < CDF_V; ++i) q_out[base + i] = qv[i];
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------- small n path ---
+// n <= CDF_SMALL_MAX: one CTA, levels in shared memory (the reference's
+// level loops verbatim), finalize and cut table by one thread.
+template <typename T>
+__global__ void __launch_bounds__(256)
+cdf_small_kernel(WSrc src, int64_t n, T* __restrict__ q_out, int32_t* __restrict__ cut_out,
+                 T* __restrict__ total_out, int64_t* fail, int64_t step) {
+  if (fail && *fail) return;
+  __shared__ T fw[2 * CDF_SMALL_MAX];
+  __shared__ T bw[2 * CDF_SMALL_MAX];
+  const double M = src.mode == 0 ? *src.M : 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) fw[i] = weight_of<T>(src.src[i], M, src.mode);
+  __syncthreads();
+  int64_t off = 0, len = n;
+  while (len > 1) {
+    for (int64_t i = threadIdx.x; i < len / 2; i += blockDim.x)
+      fw[off + len + i] = fw[off + 2 * i] + fw[off + 2 * i + 1];
+    __syncthreads();
+    off += len;
+    len >>= 1;
+  }
+  const T total = fw[off];
+  // backward level by level into bw (same offsets as fw)
+  if (threadIdx.x == 0) bw[off] = total;
+  __syncthreads();
+  int64_t plen = 1, poff = off;
+  while (plen < n) {
+    const int64_t clen = plen * 2, coff = poff - clen;
+    for (int64_t i = threadIdx.x; i < clen; i += blockDim.x) {
+      const T p = bw[poff + (i >> 1)];
+      bw[coff + i] = (i & 1) ? p : (T)(p - fw[coff + i + 1]);
+    }
+    __syncthreads();
+    plen = clen;
+    poff = coff;
+  }
+  if (threadIdx.x == 0) {
+    *total_out = total;
+    if (!(total > (T)0) || !isfinite((double)total)) {
+      if (fail) atomicCAS((unsigned long long*)fail, 0ull, (unsigned long long)(-step));
+      return;
+    }
+    T m = (T)(-INFINITY);
+    int64_t Lprev = 0;
+    const T nf = (T)n;
+    for (int64_t i = 0; i < n; ++i) {
+      m = fmax(m, bw[i] / total);
+      T qi = clip01(m);
+      if (i == n - 1) qi = (T)1;
+      q_out[i] = qi;
+      const int64_t L = (int64_t)ceil(qi * nf);
+      for (int64_t k = Lprev; k < L; ++k) cut_out[k] = (int32_t)i;
+      Lprev = L > Lprev ? L : Lprev;
+    }
+  }
+}
+
+// -------------------------------------------------------------- lookup ---
+// cutpoint_indices (resampling.py:146-158): k = I[ceil(N u) - 1], then
+// advance while u > q(k).  Returns the 0-based ancestor.  Equals
+// searchsorted(q, u, 'left').
+template <typename T>
+PF_D int64_t cutpoint_lookup(const T* __restrict__ q, const int32_t* __restrict__ cut, int64_t n,
+                             double u) {
+  const int64_t s = (int64_t)ceil(u * (double)n);
+  int64_t k = cut[s - 1];
+  while (u > (double)q[k]) ++k;
+  return k;
+}
+
+}  // namespace pf

@@ -1,0 +1,1302 @@
+// Host engine and C ABI of libparsmc_b200.so (see include/parsmc_b200.h).
+//
+// One pf_engine owns a device-resident particle system of n slots and runs
+// the reference's full cycle (filtering.py:200-374) with no host round
+// trips inside the time loop: per step it launches
+//     K1 step_kernel      (resample t-1 + propagate + weights + summaries)
+//     K5 weighted quantiles of x / sigma2 / tau2 (filtering.py:135-155)
+//     K2 cdf_reduce, K3 cdf_top, K4 cdf_expand   (prefix_sum.py, resampling.py)
+// and checks the device status word once, after the loop.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/parsmc_b200.h"
+#include "step.cuh"
+
+using namespace pf;
+
+namespace {
+
+thread_local std::string g_msg;
+thread_local int64_t g_step = 0;
+std::atomic<int64_t> g_launches{0};
+
+int set_err(int code, const std::string& msg, int64_t step = 0) {
+  g_msg = msg;
+  g_step = step;
+  return code;
+}
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) {                                                             \
+      return set_err(e_ == cudaErrorMemoryAllocation ? PF_ERR_OUT_OF_MEMORY : PF_ERR_CUDA,  \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                   \
+    }                                                                                    \
+  } while (0)
+
+#define LAUNCHED() g_launches.fetch_add(1, std::memory_order_relaxed)
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t count) {
+    if (count <= cap && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc((void**)&p, (count ? count : 1) * sizeof(T));
+    if (e == cudaSuccess) cap = count;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+int grid_for(int64_t n, int block, int cap = 148 * 16) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
+  }
+  return sms;
+}
+
+// ------------------------------------------------- weighted quantiles ---
+// filtering.py:135-140: stable argsort by value, fp64 cumulative weights in
+// that order, first position with cw >= p*cw[-1].  The stable radix sort on
+// the order-preserving bit image of the value reproduces argsort(kind=
+// "stable"); the scan order differs from numpy's sequential cumsum only in
+// rounding, which can move a quantile by one order statistic at an exact
+// near-tie.
+__global__ void qkeys_kernel(const double* __restrict__ v, int64_t n, uint64_t* __restrict__ keys,
+                             uint32_t* __restrict__ idx, const int64_t* fail) {
+  if (fail && *fail) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = ordered_bits(v[i]);
+    idx[i] = (uint32_t)i;
+  }
+}
+
+template <typename TQ>
+__global__ void qgather_kernel(const uint32_t* __restrict__ idx, WSrc src, int64_t n,
+                               double* __restrict__ ws, const int64_t* fail) {
+  if (fail && *fail) return;
+  const double M = src.mode == 0 ? *src.M : 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    ws[i] = (double)weight_of<TQ>(src.src[idx[i]], M, src.mode);
+}
+
+__global__ void qselect_kernel(const double* __restrict__ cw, const uint32_t* __restrict__ idx,
+                               const double* __restrict__ vals, int64_t n, const double* probs,
+                               int np, double* __restrict__ out, const int64_t* fail) {
+  if (fail && *fail) return;
+  const int k = threadIdx.x;
+  if (k >= np) return;
+  const double thr = probs[k] * cw[n - 1];
+  int64_t lo = 0, hi = n;  // first i with cw[i] >= thr
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (cw[mid] < thr) lo = mid + 1; else hi = mid;
+  }
+  if (lo > n - 1) lo = n - 1;
+  out[k] = vals[idx[lo]];
+}
+
+struct QuantileScratch {
+  DevBuf<uint64_t> kin, kout;
+  DevBuf<uint32_t> iin, iout;
+  DevBuf<double> ws;
+  DevBuf<unsigned char> tmp;
+  size_t tmp_bytes = 0;
+  cudaError_t ensure(int64_t n) {
+    cudaError_t e;
+    if ((e = kin.ensure(n)) || (e = kout.ensure(n)) || (e = iin.ensure(n)) || (e = iout.ensure(n)) ||
+        (e = ws.ensure(n)))
+      return e;
+    size_t b1 = 0, b2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b1, kin.p, kout.p, iin.p, iout.p, (int)n);
+    cub::DeviceScan::InclusiveSum(nullptr, b2, ws.p, ws.p, (int)n);
+    tmp_bytes = b1 > b2 ? b1 : b2;
+    return tmp.ensure(tmp_bytes);
+  }
+};
+
+template <typename TQ>
+int weighted_quantiles_dev(QuantileScratch& s, const double* vals, WSrc w, int64_t n,
+                           const double* d_probs, int np, double* d_out, cudaStream_t st,
+                           const int64_t* fail) {
+  const int g = grid_for(n, 256);
+  qkeys_kernel<<<g, 256, 0, st>>>(vals, n, s.kin.p, s.iin.p, fail);
+  LAUNCHED();
+  size_t b = s.tmp_bytes;
+  CK(cub::DeviceRadixSort::SortPairs(s.tmp.p, b, s.kin.p, s.kout.p, s.iin.p, s.iout.p, (int)n, 0,
+                                     64, st));
+  LAUNCHED();
+  qgather_kernel<TQ><<<g, 256, 0, st>>>(s.iout.p, w, n, s.ws.p, fail);
+  LAUNCHED();
+  b = s.tmp_bytes;
+  CK(cub::DeviceScan::InclusiveSum(s.tmp.p, b, s.ws.p, s.ws.p, (int)n, st));
+  LAUNCHED();
+  qselect_kernel<<<1, 32, 0, st>>>(s.ws.p, s.iout.p, vals, n, d_probs, np, d_out, fail);
+  LAUNCHED();
+  return PF_OK;
+}
+
+// ---------------------------------------------------------------- CDF ---
+struct CdfBufs {
+  CdfPlan plan;
+  DevBuf<unsigned char> tile_tot, chunk_tot, node, carry, total;
+  cudaError_t ensure(int64_t n, size_t esz) {
+    plan = cdf_plan(n);
+    cudaError_t e;
+    if ((e = tile_tot.ensure(plan.tiles * esz)) || (e = chunk_tot.ensure(plan.chunks * esz)) ||
+        (e = node.ensure(plan.chunks * esz)) || (e = carry.ensure(plan.chunks * esz)) ||
+        (e = total.ensure(2 * esz)))
+      return e;
+    return cudaSuccess;
+  }
+};
+
+template <typename T>
+int launch_cdf(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t* fail, int64_t step,
+               cudaStream_t st) {
+  const CdfPlan& p = b.plan;
+  T* total = (T*)b.total.p;
+  if (p.small) {
+    cdf_small_kernel<T><<<1, 256, 0, st>>>(src, n, q, cut, total, fail, step);
+    LAUNCHED();
+    return PF_OK;
+  }
+  T* tt = (T*)b.tile_tot.p;
+  T* ct = (T*)b.chunk_tot.p;
+  T* nd = (T*)b.node.p;
+  T* cr = (T*)b.carry.p;
+  cdf_reduce_kernel<T><<<(int)p.chunks, CDF_THREADS, 0, st>>>(src, p.R, tt, ct, fail);
+  LAUNCHED();
+  const size_t smem = 4 * p.chunks * sizeof(T);
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[sizeof(T) == 8]) {
+    CK(cudaFuncSetAttribute(cdf_top_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            4 * CDF_MAX_CHUNKS * (int)sizeof(T)));
+    attr_set[sizeof(T) == 8] = true;
+  }
+  cdf_top_kernel<T><<<1, 1024, smem, st>>>(ct, p.chunks, nd, cr, total, fail, step);
+  LAUNCHED();
+  cdf_expand_kernel<T><<<(int)p.chunks, CDF_THREADS, 0, st>>>(src, n, p.R, tt, nd, cr, total, q, cut,
+                                                              fail);
+  LAUNCHED();
+  return PF_OK;
+}
+
+}  // namespace
+
+// ================================================================ engine ===
+struct pf_engine {
+  pf_config cfg;
+  int64_t n = 0;
+  cudaStream_t st = nullptr;
+  int mode = 0;  // M_LS | M_LT | M_SINGLE
+  bool single = false;
+  DevBuf<Rec> rec[2];
+  DevBuf<double> lw;
+  DevBuf<uint64_t> u3;
+  DevBuf<unsigned char> q;
+  DevBuf<int32_t> cut;
+  DevBuf<int64_t> idx;
+  DevBuf<double> qx, qs, qt;
+  DevBuf<double> s2init;
+  DevBuf<Partial> partials;
+  DevBuf<Scalars> sc;
+  DevBuf<int64_t> fail;
+  CdfBufs cdf;
+  QuantileScratch qsc;
+  // per-run outputs (device)
+  DevBuf<double> o_fm, o_sm, o_ssd, o_tm, o_tsd, o_fq, o_sq, o_tq;
+  DevBuf<double> probs;  // [0..5) param probs, [5..8) state probs
+  // gamma tables for the shape schedule a0 + t/2, t = 0..T
+  DevBuf<double> tab_s, tab_t, shapes_buf;
+  std::vector<double> shapes_s, shapes_t;
+  bool shared_table = false;
+  // materialise scratch
+  DevBuf<double> m_x, m_s2, m_t2, m_as, m_bs, m_at, m_bt;
+  DevBuf<double> feed_buf;
+  // timing
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<cudaEvent_t> evs;
+  double last_total_ms = 0, last_step_ms = 0;
+  int64_t last_step_launches = 0, last_kernels = 0;
+  std::vector<double> y_host;
+};
+
+namespace {
+
+int build_tables(pf_engine* e, int64_t T) {
+  if (e->cfg.gamma_method != 0) return PF_OK;
+  const bool ls = e->cfg.learn && e->cfg.learn_sigma2, lt = e->cfg.learn && e->cfg.learn_tau2;
+  if (!ls && !lt) return PF_OK;
+  auto schedule = [&](double a0) {
+    std::vector<double> v((size_t)T + 1);
+    double a = a0;
+    v[0] = a;
+    for (int64_t t = 1; t <= T; ++t) {
+      a = a + 0.5;  // a_sig = a_sig + 0.5 (filtering.py:279)
+      v[(size_t)t] = a;
+    }
+    return v;
+  };
+  std::vector<double> ss = ls ? schedule(e->cfg.sigma2_shape) : std::vector<double>();
+  std::vector<double> tt = lt ? schedule(e->cfg.tau2_shape) : std::vector<double>();
+  auto covered = [](const std::vector<double>& have, const std::vector<double>& want) {
+    if (want.empty()) return true;
+    if (have.size() < want.size()) return false;
+    return std::memcmp(have.data(), want.data(), want.size() * sizeof(double)) == 0;
+  };
+  if (covered(e->shapes_s, ss) && covered(e->shapes_t, tt)) return PF_OK;
+  const bool share = ls && lt && e->cfg.sigma2_shape == e->cfg.tau2_shape;
+  auto build = [&](const std::vector<double>& sh, DevBuf<double>& tab) -> int {
+    CK(e->shapes_buf.ensure(sh.size()));
+    CK(tab.ensure(sh.size() * GT_TABLE_DOUBLES));
+    CK(cudaMemcpyAsync(e->shapes_buf.p, sh.data(), sh.size() * sizeof(double),
+                       cudaMemcpyHostToDevice, e->st));
+    dim3 grid(GT_NSEG, (unsigned)sh.size());
+    gamma_table_build_kernel<<<grid, 32, 0, e->st>>>(e->shapes_buf.p, tab.p);
+    LAUNCHED();
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(e->st));
+    return PF_OK;
+  };
+  int rc;
+  if (ls && (rc = build(ss, e->tab_s)) != PF_OK) return rc;
+  if (lt && !share && (rc = build(tt, e->tab_t)) != PF_OK) return rc;
+  e->shapes_s = ss;
+  e->shapes_t = share ? ss : tt;
+  e->shared_table = share;
+  return PF_OK;
+}
+
+GammaSrc gamma_src(pf_engine* e, bool sigma, int64_t t) {
+  GammaSrc g;
+  g.method = e->cfg.gamma_method;
+  const std::vector<double>& sh = sigma ? e->shapes_s : e->shapes_t;
+  const double a0 = sigma ? e->cfg.sigma2_shape : e->cfg.tau2_shape;
+  g.shape = sh.empty() ? a0 + 0.5 * t : sh[(size_t)t];
+  if (g.method == 1 && sh.empty()) {
+    double a = a0;
+    for (int64_t k = 0; k < t; ++k) a = a + 0.5;
+    g.shape = a;
+  }
+  const double* base = sigma || e->shared_table ? e->tab_s.p : e->tab_t.p;
+  g.table = base ? base + (size_t)t * GT_TABLE_DOUBLES : nullptr;
+  return g;
+}
+
+double shape_at(const pf_config& c, bool sigma, int64_t t) {
+  double a = sigma ? c.sigma2_shape : c.tau2_shape;
+  for (int64_t k = 0; k < t; ++k) a = a + 0.5;
+  return a;
+}
+
+struct RunSpec {
+  const double* y;
+  int64_t T;
+  const pf_feed* feed;
+  pf_outputs* out;  // null for resident runs
+  bool resident;
+};
+
+template <int MODE, typename TQ>
+int run_impl(pf_engine* e, const RunSpec& rs) {
+  constexpr bool LS = MODE & M_LS, LT = MODE & M_LT;
+  const pf_config& c = e->cfg;
+  const int64_t n = e->n, T = rs.T;
+  cudaStream_t st = e->st;
+  pf_outputs* out = rs.out;
+  const bool want_fq = out ? (out->filtered_quantiles != nullptr) : (c.track_quantiles != 0);
+  const bool want_sq = LS;
+  const bool want_tq = LT;
+  const bool keep_idx = out && out->indices;
+  const bool keep_final = out && (out->final_states || out->final_sigma2);
+  const bool store = out && out->hist_states;
+  const bool timing = out && c.phase_timing;
+  int rc;
+  if ((rc = build_tables(e, T)) != PF_OK) return rc;
+
+  const size_t TT = (size_t)(T > 0 ? T : 1);
+  CK(e->o_fm.ensure(TT));
+  if (LS) { CK(e->o_sm.ensure(TT)); CK(e->o_ssd.ensure(TT)); CK(e->o_sq.ensure(TT * 5)); }
+  if (LT) { CK(e->o_tm.ensure(TT)); CK(e->o_tsd.ensure(TT)); CK(e->o_tq.ensure(TT * 5)); }
+  if (want_fq) CK(e->o_fq.ensure(TT * 3));
+  if (want_fq) CK(e->qx.ensure(n));
+  if (want_sq) CK(e->qs.ensure(n));
+  if (want_tq) CK(e->qt.ensure(n));
+  if (want_fq || want_sq || want_tq) CK(e->qsc.ensure(n));
+  if (keep_idx) CK(e->idx.ensure(n));
+
+  // oracle feed: whole [T+1][n] arrays uploaded once
+  const double *fz = nullptr, *fgs = nullptr, *fgt = nullptr, *fw = nullptr;
+  if (rs.feed && (rs.feed->z || rs.feed->g_sigma || rs.feed->g_tau || rs.feed->w)) {
+    const size_t rows = (size_t)T + 1, per = rows * (size_t)n;
+    CK(e->feed_buf.ensure(4 * per));
+    double* base = e->feed_buf.p;
+    auto up = [&](const double* h, int k) -> const double* {
+      if (!h) return nullptr;
+      cudaMemcpyAsync(base + k * per, h, per * sizeof(double), cudaMemcpyHostToDevice, st);
+      return base + k * per;
+    };
+    fz = up(rs.feed->z, 0);
+    fgs = up(rs.feed->g_sigma, 1);
+    fgt = up(rs.feed->g_tau, 2);
+    fw = up(rs.feed->w, 3);
+    CK(cudaGetLastError());
+  }
+  auto row = [&](const double* p, int64_t t) -> const double* { return p ? p + (size_t)t * n : nullptr; };
+
+  // events
+  int nev = 0;
+  auto ev_record = [&]() -> int {
+    if (!timing) return 0;
+    if ((int)e->evs.size() <= nev) {
+      cudaEvent_t ev;
+      cudaEventCreate(&ev);
+      e->evs.push_back(ev);
+    }
+    cudaEventRecord(e->evs[nev], st);
+    return nev++;
+  };
+  std::vector<std::pair<int, int>> phase_marks;  // (event index, phase id)
+  enum { PH_INIT = 0, PH_CDF = 1, PH_RES = 2, PH_SORT = 3, PH_PROP = 4, PH_STORE = 5, PH_OTHER = 6 };
+  auto mark = [&](int phase) {
+    if (timing) phase_marks.push_back({ev_record(), phase});
+  };
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> step_evs;
+  if (rs.resident) step_evs.reserve((size_t)T);
+
+  CK(cudaEventRecord(e->ev0, st));
+  if (timing) ev_record();
+
+  // ---- scalars / status reset
+  Scalars s0h;
+  s0h.M = 0;
+  s0h.W = 0;
+  s0h.cs = (LS && c.sigma2_shape > 1.0) ? c.sigma2_scale / (c.sigma2_shape - 1.0) : 0.0;
+  s0h.ct = (LT && c.tau2_shape > 1.0) ? c.tau2_scale / (c.tau2_shape - 1.0) : 0.0;
+  s0h.counter = 0;
+  s0h.pad = 0;
+  CK(cudaMemcpyAsync(e->sc.p, &s0h, sizeof(Scalars), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(e->fail.p, 0, sizeof(int64_t), st));
+
+  // ---- K0 init
+  {
+    InitArgs a;
+    a.n = n;
+    a.seed = c.seed;
+    a.x0_mean = c.x0_mean;
+    a.sqrt_x0_var = c.sqrt_x0_var;
+    a.bs0 = c.sigma2_scale;
+    a.bt0 = c.tau2_scale;
+    a.sigma2_fixed = c.sigma2_fixed;
+    a.tau2_fixed = c.tau2_fixed;
+    a.gs = gamma_src(e, true, 0);
+    a.gt = gamma_src(e, false, 0);
+    a.feed_z = row(fz, 0);
+    a.feed_gs = row(fgs, 0);
+    a.feed_gt = row(fgt, 0);
+    a.rec = e->rec[0].p;
+    a.s2_init = nullptr;
+    if (T == 0 && keep_final && LS) {
+      CK(e->s2init.ensure(n));
+      a.s2_init = e->s2init.p;
+    }
+    init_kernel<MODE><<<grid_for(n, 256), 256, 0, st>>>(a);
+    LAUNCHED();
+  }
+  mark(PH_INIT);
+
+  const int sms = sm_count();
+  int step_grid = (int)((n + 255) / 256);
+  if (step_grid > sms * 8) step_grid = sms * 8;
+  int64_t per_block = (n + step_grid - 1) / step_grid;
+  per_block = (per_block + 255) / 256 * 256;
+  step_grid = (int)((n + per_block - 1) / per_block);
+
+  int cur = 0;
+  WSrc wsrc;
+  wsrc.src = e->lw.p;
+  wsrc.M = &e->sc.p->M;
+  wsrc.mode = fw ? 1 : 0;
+  TQ* qv = (TQ*)e->q.p;
+  int64_t step_launches = 0;
+
+  for (int64_t t = 1; t <= T; ++t) {
+    // ---- K1
+    StepArgs<TQ> a;
+    a.n = n;
+    a.t = t;
+    a.seed = c.seed;
+    a.y = rs.y ? rs.y[t - 1] : e->y_host[(size_t)(t - 1)];
+    a.sigma2_fixed = c.sigma2_fixed;
+    a.tau2_fixed = c.tau2_fixed;
+    a.sqrt_tau2_fixed = c.sqrt_tau2_fixed;
+    a.log_term_fixed = c.log_term_fixed;
+    a.gs = gamma_src(e, true, t);
+    a.gt = gamma_src(e, false, t);
+    a.rec_in = e->rec[cur].p;
+    a.rec_out = e->rec[cur ^ 1].p;
+    a.lw = e->lw.p;
+    a.u3 = e->u3.p;
+    a.q_prev = qv;
+    a.cut_prev = e->cut.p;
+    a.idx_out = (keep_idx && t > 1) ? e->idx.p : nullptr;
+    a.feed_z = row(fz, t);
+    a.feed_gs = row(fgs, t);
+    a.feed_gt = row(fgt, t);
+    a.feed_w = row(fw, t);
+    a.qx = want_fq ? e->qx.p : nullptr;
+    a.qs = want_sq ? e->qs.p : nullptr;
+    a.qt = want_tq ? e->qt.p : nullptr;
+    a.partials = e->partials.p;
+    a.sc = e->sc.p;
+    a.out.fmean = e->o_fm.p;
+    a.out.s_mean = e->o_sm.p;
+    a.out.s_sd = e->o_ssd.p;
+    a.out.t_mean = e->o_tm.p;
+    a.out.t_sd = e->o_tsd.p;
+    a.fail = e->fail.p;
+    a.per_block = per_block;
+    if (rs.resident) {
+      cudaEvent_t b0, b1;
+      cudaEventCreate(&b0);
+      cudaEventCreate(&b1);
+      cudaEventRecord(b0, st);
+      step_kernel<MODE, TQ><<<step_grid, 256, 0, st>>>(a);
+      cudaEventRecord(b1, st);
+      step_evs.push_back({b0, b1});
+    } else {
+      step_kernel<MODE, TQ><<<step_grid, 256, 0, st>>>(a);
+    }
+    LAUNCHED();
+    ++step_launches;
+    cur ^= 1;
+    mark(PH_PROP);
+    if (keep_idx && t > 1)
+      CK(cudaMemcpyAsync(out->indices + (size_t)(t - 2) * n, e->idx.p, n * sizeof(int64_t),
+                         cudaMemcpyDeviceToHost, st));
+
+    // ---- K5 summaries: weighted quantiles from the pre-resample set
+    if (want_fq)
+      if ((rc = weighted_quantiles_dev<TQ>(e->qsc, e->qx.p, wsrc, n, e->probs.p + 5, 3,
+                                           e->o_fq.p + (t - 1) * 3, st, e->fail.p)) != PF_OK)
+        return rc;
+    if (want_sq)
+      if ((rc = weighted_quantiles_dev<TQ>(e->qsc, e->qs.p, wsrc, n, e->probs.p, 5,
+                                           e->o_sq.p + (t - 1) * 5, st, e->fail.p)) != PF_OK)
+        return rc;
+    if (want_tq)
+      if ((rc = weighted_quantiles_dev<TQ>(e->qsc, e->qt.p, wsrc, n, e->probs.p, 5,
+                                           e->o_tq.p + (t - 1) * 5, st, e->fail.p)) != PF_OK)
+        return rc;
+    mark(PH_OTHER);
+
+    // ---- K2-K4 CDF + cut table
+    if ((rc = launch_cdf<TQ>(e->cdf, wsrc, n, qv, e->cut.p, e->fail.p, t, st)) != PF_OK) return rc;
+    mark(PH_CDF);
+
+    // ---- store: post-resample snapshot of step t
+    if (store) {
+      MatArgs<TQ> m;
+      m.n = n;
+      m.t = t;
+      m.seed = c.seed;
+      m.resample = 1;
+      m.rec = e->rec[cur].p;
+      m.u3 = e->u3.p;
+      m.q = qv;
+      m.cut = e->cut.p;
+      m.s2_direct = nullptr;
+      m.gs = gamma_src(e, true, t);
+      m.feed_gs = row(fgs, t);
+      m.learn_s = LS;
+      m.learn_t = LT;
+      m.sigma2_fixed = c.sigma2_fixed;
+      m.tau2_fixed = c.tau2_fixed;
+      m.a_s = shape_at(c, true, t);
+      m.a_t = shape_at(c, false, t);
+      m.idx = nullptr;
+      size_t off = (size_t)(t - 1) * n;
+      CK(e->m_x.ensure(n)); CK(e->m_s2.ensure(n)); CK(e->m_t2.ensure(n)); CK(e->m_as.ensure(n));
+      CK(e->m_bs.ensure(n)); CK(e->m_at.ensure(n)); CK(e->m_bt.ensure(n));
+      m.x = e->m_x.p; m.s2 = e->m_s2.p; m.t2 = e->m_t2.p; m.as = e->m_as.p; m.bs = e->m_bs.p;
+      m.at = e->m_at.p; m.bt = e->m_bt.p;
+      m.fail = e->fail.p;
+      materialize_kernel<TQ><<<grid_for(n, 256), 256, 0, st>>>(m);
+      LAUNCHED();
+      double* dst[7] = {out->hist_states, out->hist_sigma2, out->hist_tau2, out->hist_a_sigma,
+                        out->hist_b_sigma, out->hist_a_tau, out->hist_b_tau};
+      double* src[7] = {m.x, m.s2, m.t2, m.as, m.bs, m.at, m.bt};
+      for (int k = 0; k < 7; ++k)
+        if (dst[k]) CK(cudaMemcpyAsync(dst[k] + off, src[k], n * sizeof(double), cudaMemcpyDeviceToHost, st));
+      mark(PH_STORE);
+    }
+  }
+
+  // ---- final resample (keep_indices row T, keep_final)
+  if (T >= 1 && (keep_idx || keep_final)) {
+    MatArgs<TQ> m;
+    m.n = n;
+    m.t = T;
+    m.seed = c.seed;
+    m.resample = 1;
+    m.rec = e->rec[cur].p;
+    m.u3 = e->u3.p;
+    m.q = qv;
+    m.cut = e->cut.p;
+    m.s2_direct = nullptr;
+    m.gs = gamma_src(e, true, T);
+    m.feed_gs = row(fgs, T);
+    m.learn_s = LS;
+    m.learn_t = LT;
+    m.sigma2_fixed = c.sigma2_fixed;
+    m.tau2_fixed = c.tau2_fixed;
+    m.a_s = shape_at(c, true, T);
+    m.a_t = shape_at(c, false, T);
+    m.idx = keep_idx ? e->idx.p : nullptr;
+    m.x = keep_final ? out->final_states : nullptr;
+    m.fail = e->fail.p;
+    double* dst[7] = {out->final_states, out->final_sigma2, out->final_tau2, out->final_a_sigma,
+                      out->final_b_sigma, out->final_a_tau, out->final_b_tau};
+    DevBuf<double>* bufs[7] = {&e->m_x, &e->m_s2, &e->m_t2, &e->m_as, &e->m_bs, &e->m_at, &e->m_bt};
+    double** slots[7] = {&m.x, &m.s2, &m.t2, &m.as, &m.bs, &m.at, &m.bt};
+    for (int k = 0; k < 7; ++k) {
+      *slots[k] = nullptr;
+      if (keep_final && dst[k]) {
+        CK(bufs[k]->ensure(n));
+        *slots[k] = bufs[k]->p;
+      }
+    }
+    materialize_kernel<TQ><<<grid_for(n, 256), 256, 0, st>>>(m);
+    LAUNCHED();
+    if (keep_idx)
+      CK(cudaMemcpyAsync(out->indices + (size_t)(T - 1) * n, e->idx.p, n * sizeof(int64_t),
+                         cudaMemcpyDeviceToHost, st));
+    for (int k = 0; k < 7; ++k)
+      if (*slots[k]) CK(cudaMemcpyAsync(dst[k], *slots[k], n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    mark(PH_RES);
+  } else if (T == 0 && keep_final) {
+    MatArgs<TQ> m;
+    memset(&m, 0, sizeof(m));
+    m.n = n;
+    m.t = 0;
+    m.seed = c.seed;
+    m.resample = 0;
+    m.rec = e->rec[0].p;
+    m.s2_direct = LS ? e->s2init.p : nullptr;
+    m.gs = gamma_src(e, true, 0);
+    m.learn_s = LS;
+    m.learn_t = LT;
+    m.sigma2_fixed = c.sigma2_fixed;
+    m.tau2_fixed = c.tau2_fixed;
+    m.a_s = c.sigma2_shape;
+    m.a_t = c.tau2_shape;
+    m.fail = e->fail.p;
+    double* dst[7] = {out->final_states, out->final_sigma2, out->final_tau2, out->final_a_sigma,
+                      out->final_b_sigma, out->final_a_tau, out->final_b_tau};
+    DevBuf<double>* bufs[7] = {&e->m_x, &e->m_s2, &e->m_t2, &e->m_as, &e->m_bs, &e->m_at, &e->m_bt};
+    double** slots[7] = {&m.x, &m.s2, &m.t2, &m.as, &m.bs, &m.at, &m.bt};
+    for (int k = 0; k < 7; ++k) {
+      if (dst[k]) {
+        CK(bufs[k]->ensure(n));
+        *slots[k] = bufs[k]->p;
+      }
+    }
+    materialize_kernel<TQ><<<grid_for(n, 256), 256, 0, st>>>(m);
+    LAUNCHED();
+    for (int k = 0; k < 7; ++k)
+      if (*slots[k]) CK(cudaMemcpyAsync(dst[k], *slots[k], n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    mark(PH_OTHER);
+  }
+
+  // ---- outputs to host
+  if (out && T > 0) {
+    auto cp = [&](double* h, DevBuf<double>& d, size_t cnt) -> int {
+      if (h) CK(cudaMemcpyAsync(h, d.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
+      return PF_OK;
+    };
+    if ((rc = cp(out->filtered_mean, e->o_fm, T)) != PF_OK) return rc;
+    if (want_fq && (rc = cp(out->filtered_quantiles, e->o_fq, T * 3)) != PF_OK) return rc;
+    if (LS) {
+      if ((rc = cp(out->sigma2_mean, e->o_sm, T)) || (rc = cp(out->sigma2_sd, e->o_ssd, T)) ||
+          (rc = cp(out->sigma2_quantiles, e->o_sq, T * 5)))
+        return rc;
+    }
+    if (LT) {
+      if ((rc = cp(out->tau2_mean, e->o_tm, T)) || (rc = cp(out->tau2_sd, e->o_tsd, T)) ||
+          (rc = cp(out->tau2_quantiles, e->o_tq, T * 5)))
+        return rc;
+    }
+  }
+  mark(PH_OTHER);
+  int64_t fail_h = 0;
+  CK(cudaMemcpyAsync(&fail_h, e->fail.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(e->ev1, st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e->ev0, e->ev1);
+  e->last_total_ms = ms;
+  e->last_step_launches = step_launches;
+  if (rs.resident) {
+    double acc = 0;
+    for (auto& pr : step_evs) {
+      float k = 0;
+      cudaEventElapsedTime(&k, pr.first, pr.second);
+      acc += k;
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+    e->last_step_ms = step_evs.empty() ? 0.0 : acc / step_evs.size();
+  }
+  if (out) {
+    for (int k = 0; k < 7; ++k) out->phase_ns[k] = 0;
+    if (timing) {
+      for (size_t i = 0; i < phase_marks.size(); ++i) {
+        const int prev = i == 0 ? 0 : phase_marks[i - 1].first;
+        float d = 0;
+        cudaEventElapsedTime(&d, e->evs[prev], e->evs[phase_marks[i].first]);
+        out->phase_ns[phase_marks[i].second] += (int64_t)llround(d * 1e6);
+      }
+    } else {
+      out->phase_ns[PH_OTHER] = (int64_t)llround(ms * 1e6);
+    }
+    out->failed_step = fail_h;
+  }
+  if (fail_h > 0)
+    return set_err(PF_ERR_ALL_WEIGHTS_ZERO, "all particle weights are zero (at time step " +
+                                             std::to_string(fail_h) + ")", fail_h);
+  if (fail_h < 0) return set_err(PF_ERR_ALL_WEIGHTS_ZERO, "all particle weights are zero", 0);
+  return PF_OK;
+}
+
+using RunFn = int (*)(pf_engine*, const RunSpec&);
+
+RunFn pick_run(int mode) {
+  switch (mode) {
+    case 0: return run_impl<0, double>;
+    case 1: return run_impl<1, double>;
+    case 2: return run_impl<2, double>;
+    case 3: return run_impl<3, double>;
+    case 4: return run_impl<4, float>;
+    case 5: return run_impl<5, float>;
+    case 6: return run_impl<6, float>;
+    case 7: return run_impl<7, float>;
+  }
+  return nullptr;
+}
+
+}  // namespace
+
+// ================================================================ C ABI ===
+extern "C" {
+
+const char* pf_version(void) { return "parsmc-b200 0.1.0 (sm_100a)"; }
+const char* pf_last_error_message(void) { return g_msg.c_str(); }
+int64_t pf_last_error_step(void) { return g_step; }
+int64_t pf_launch_count(void) { return g_launches.load(); }
+
+int pf_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return c;
+}
+
+int pf_engine_create(const pf_config* cfg, pf_engine** out) {
+  if (!cfg || !out) return set_err(PF_ERR_VALUE, "null argument");
+  *out = nullptr;
+  const int64_t n = cfg->n;
+  if (n < 1) return set_err(PF_ERR_VALUE, "particle count must be >= 1");
+  if (!is_pow2(n)) return set_err(PF_ERR_NOT_POWER_OF_TWO, "particle count must be a power of two, got " + std::to_string(n));
+  if (n > (int64_t(1) << 28)) return set_err(PF_ERR_VALUE, "particle count above 2^28 per device");
+  if (pf_device_count() < 1) return set_err(PF_ERR_CUDA, "no CUDA device visible");
+  CK(cudaSetDevice(cfg->device));
+  pf_engine* e = new pf_engine();
+  e->cfg = *cfg;
+  e->n = n;
+  e->single = cfg->precision == PF_DTYPE_F32;
+  e->mode = (cfg->learn && cfg->learn_sigma2 ? M_LS : 0) | (cfg->learn && cfg->learn_tau2 ? M_LT : 0) |
+            (e->single ? M_SINGLE : 0);
+  auto bail = [&](cudaError_t err) {
+    int rc = set_err(err == cudaErrorMemoryAllocation ? PF_ERR_OUT_OF_MEMORY : PF_ERR_CUDA,
+                  std::string("engine allocation: ") + cudaGetErrorString(err));
+    pf_engine_destroy(e);
+    return rc;
+  };
+  cudaError_t err;
+  if ((err = cudaStreamCreateWithFlags(&e->st, cudaStreamNonBlocking))) return bail(err);
+  if ((err = e->rec[0].ensure(n)) || (err = e->rec[1].ensure(n)) || (err = e->lw.ensure(n)) ||
+      (err = e->u3.ensure(n)) || (err = e->q.ensure(n * (e->single ? 4 : 8))) ||
+      (err = e->cut.ensure(n)) || (err = e->partials.ensure(sm_count() * 8 + 8)) ||
+      (err = e->sc.ensure(1)) || (err = e->fail.ensure(1)) ||
+      (err = e->cdf.ensure(n, e->single ? 4 : 8)) || (err = e->probs.ensure(8)))
+    return bail(err);
+  const double probs[8] = {0.005, 0.05, 0.5, 0.95, 0.995, 0.05, 0.5, 0.95};
+  if ((err = cudaMemcpy(e->probs.p, probs, sizeof(probs), cudaMemcpyHostToDevice))) return bail(err);
+  if ((err = cudaEventCreate(&e->ev0)) || (err = cudaEventCreate(&e->ev1))) return bail(err);
+  *out = e;
+  return PF_OK;
+}
+
+int pf_engine_reconfigure(pf_engine* e, const pf_config* cfg) {
+  if (!e || !cfg) return set_err(PF_ERR_VALUE, "null argument");
+  if (cfg->n != e->n || (cfg->precision == PF_DTYPE_F32) != e->single || cfg->device != e->cfg.device)
+    return set_err(PF_ERR_VALUE, "reconfigure cannot change n, precision or device");
+  e->cfg = *cfg;
+  e->mode = (cfg->learn && cfg->learn_sigma2 ? M_LS : 0) | (cfg->learn && cfg->learn_tau2 ? M_LT : 0) |
+            (e->single ? M_SINGLE : 0);
+  return PF_OK;
+}
+
+int pf_engine_run(pf_engine* e, const double* y, int64_t t_len, const pf_feed* feed, pf_outputs* out) {
+  if (!e) return set_err(PF_ERR_VALUE, "null engine");
+  if (t_len < 0) return set_err(PF_ERR_VALUE, "negative series length");
+  for (int64_t i = 0; i < t_len; ++i)
+    if (!std::isfinite(y[i])) return set_err(PF_ERR_NON_FINITE_WEIGHT, "observations contain NaN or infinity");
+  CK(cudaSetDevice(e->cfg.device));
+  e->y_host.assign(y, y + t_len);
+  RunSpec rs{y, t_len, feed, out, false};
+  return pick_run(e->mode)(e, rs);
+}
+
+int pf_engine_run_resident(pf_engine* e, int64_t t_len) {
+  if (!e) return set_err(PF_ERR_VALUE, "null engine");
+  if (t_len > (int64_t)e->y_host.size()) return set_err(PF_ERR_VALUE, "resident run longer than the last series");
+  CK(cudaSetDevice(e->cfg.device));
+  RunSpec rs{nullptr, t_len, nullptr, nullptr, true};
+  const int64_t k0 = g_launches.load();
+  int rc = pick_run(e->mode)(e, rs);
+  e->last_kernels = g_launches.load() - k0;
+  return rc;
+}
+
+int pf_engine_last_timing(pf_engine* e, double* total_ms, double* step_kernel_ms,
+                          int64_t* step_kernel_launches, int64_t* kernels_launched) {
+  if (!e) return set_err(PF_ERR_VALUE, "null engine");
+  if (total_ms) *total_ms = e->last_total_ms;
+  if (step_kernel_ms) *step_kernel_ms = e->last_step_ms;
+  if (step_kernel_launches) *step_kernel_launches = e->last_step_launches;
+  if (kernels_launched) *kernels_launched = e->last_kernels;
+  return PF_OK;
+}
+
+int pf_engine_destroy(pf_engine* e) {
+  if (!e) return PF_OK;
+  cudaSetDevice(e->cfg.device);
+  if (e->st) cudaStreamSynchronize(e->st);
+  DevBuf<double>* bufs[] = {&e->lw, &e->qx, &e->qs, &e->qt, &e->s2init, &e->o_fm, &e->o_sm, &e->o_ssd,
+                            &e->o_tm, &e->o_tsd, &e->o_fq, &e->o_sq, &e->o_tq, &e->probs, &e->tab_s,
+                            &e->tab_t, &e->shapes_buf, &e->m_x, &e->m_s2, &e->m_t2, &e->m_as,
+                            &e->m_bs, &e->m_at, &e->m_bt, &e->feed_buf};
+  for (auto* b : bufs) b->release();
+  e->rec[0].release();
+  e->rec[1].release();
+  e->u3.release();
+  e->q.release();
+  e->cut.release();
+  e->idx.release();
+  e->partials.release();
+  e->sc.release();
+  e->fail.release();
+  e->cdf.tile_tot.release();
+  e->cdf.chunk_tot.release();
+  e->cdf.node.release();
+  e->cdf.carry.release();
+  e->cdf.total.release();
+  e->qsc.kin.release();
+  e->qsc.kout.release();
+  e->qsc.iin.release();
+  e->qsc.iout.release();
+  e->qsc.ws.release();
+  e->qsc.tmp.release();
+  for (auto ev : e->evs) cudaEventDestroy(ev);
+  if (e->ev0) cudaEventDestroy(e->ev0);
+  if (e->ev1) cudaEventDestroy(e->ev1);
+  if (e->st) cudaStreamDestroy(e->st);
+  delete e;
+  return PF_OK;
+}
+
+}  // extern "C"
+
+// ====================================================== kernel level ===
+namespace {
+
+__global__ void philox_kernel(uint64_t seed, const uint64_t* ids, int64_t n, uint64_t block,
+                              uint64_t* words) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const Philox4 P = philox_block(seed, ids[i], block);
+    for (int k = 0; k < 4; ++k) words[k * n + i] = P.w[k];
+  }
+}
+
+__global__ void philox_full_kernel(const uint64_t* c, const uint64_t* k, int64_t n, uint64_t* words) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const Philox4 P = philox4x64_10(c[i], c[n + i], c[2 * n + i], c[3 * n + i], k[i], k[n + i]);
+    for (int q = 0; q < 4; ++q) words[q * n + i] = P.w[q];
+  }
+}
+
+__global__ void uniforms_kernel(uint64_t seed, const uint64_t* ids, const uint64_t* ctr, int64_t n,
+                                double* u) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const Philox4 P = philox_block(seed, ids[i], ctr[i] >> 2);
+    u[i] = unit_open(P.w[ctr[i] & 3]);
+  }
+}
+
+__global__ void stream_uniforms_kernel(uint64_t seed, uint64_t counter, int64_t n, double* u) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const Philox4 P = philox_block(seed, (uint64_t)i, counter >> 2);
+    u[i] = unit_open(P.w[counter & 3]);
+  }
+}
+
+__global__ void ndtri_kernel(const double* u, int64_t n, double* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = ndtri(u[i]);
+}
+
+__global__ void gamma_kernel(GammaSrc g, const double* u, int64_t n, double* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = gamma_draw(g, u[i]);
+}
+
+template <typename T>
+__global__ void fwd_level_kernel(const T* prev, T* out, int64_t m) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = prev[2 * i] + prev[2 * i + 1];
+}
+
+template <typename T>
+__global__ void bwd_level_kernel(const T* parent, const T* w, T* child, int64_t m) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    child[2 * i + 1] = parent[i];
+    child[2 * i] = parent[i] - w[2 * i + 1];
+  }
+}
+
+template <typename T>
+__global__ void cut_table_kernel(const T* q, int64_t n, int32_t* cut) {
+  const T nf = (T)n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t Lp = i ? (int64_t)ceil(q[i - 1] * nf) : 0;
+    const int64_t L = (int64_t)ceil(q[i] * nf);
+    for (int64_t k = Lp; k < L; ++k) cut[k] = (int32_t)i;
+  }
+}
+
+template <typename T>
+__global__ void lookup_kernel(const T* q, const int32_t* cut, int64_t n, const double* u, int64_t m,
+                              int64_t* idx) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    idx[i] = cutpoint_lookup<T>(q, cut, n, u[i]) + 1;
+}
+
+__global__ void cuts_to_i32_kernel(const int64_t* c64, int64_t n, int32_t* c32) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    c32[i] = (int32_t)(c64[i] - 1);
+}
+
+__global__ void cuts_to_i64_kernel(const int32_t* c32, int64_t n, int64_t* c64) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    c64[i] = (int64_t)c32[i] + 1;
+}
+
+// RAII scratch for the synchronous kernel-level entry points.
+struct Scratch {
+  std::vector<void*> ptrs;
+  ~Scratch() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <typename T>
+  cudaError_t alloc(T** p, size_t count) {
+    cudaError_t e = cudaMalloc((void**)p, (count ? count : 1) * sizeof(T));
+    if (e == cudaSuccess) ptrs.push_back(*p);
+    return e;
+  }
+};
+
+int need_device() {
+  if (pf_device_count() < 1) return set_err(PF_ERR_CUDA, "no CUDA device visible");
+  return PF_OK;
+}
+
+int check_weights_host(const void* w, int64_t n, int32_t dtype) {
+  if (n < 1) return set_err(PF_ERR_VALUE, "weights must be a nonempty 1-d array");
+  for (int64_t i = 0; i < n; ++i) {
+    const double v = dtype == PF_DTYPE_F32 ? (double)((const float*)w)[i] : ((const double*)w)[i];
+    if (!std::isfinite(v)) return set_err(PF_ERR_NON_FINITE_WEIGHT, "weights contain NaN or infinity");
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    const double v = dtype == PF_DTYPE_F32 ? (double)((const float*)w)[i] : ((const double*)w)[i];
+    if (v < 0) return set_err(PF_ERR_VALUE, "weights must be nonnegative");
+  }
+  return PF_OK;
+}
+
+std::vector<double> as_f64(const void* w, int64_t n, int32_t dtype) {
+  std::vector<double> v((size_t)n);
+  for (int64_t i = 0; i < n; ++i)
+    v[(size_t)i] = dtype == PF_DTYPE_F32 ? (double)((const float*)w)[i] : ((const double*)w)[i];
+  return v;
+}
+
+template <typename T>
+int tree_cdf_impl(const std::vector<double>& w, int64_t n, T* q_host, double* total_host,
+                  int32_t* cut_dev_out, T** q_dev_out, Scratch& s) {
+  double* dw;
+  T* dq;
+  int32_t* dcut;
+  int64_t* dfail;
+  CK(s.alloc(&dw, n));
+  CK(s.alloc(&dq, n));
+  CK(s.alloc(&dcut, n));
+  CK(s.alloc(&dfail, 1));
+  CK(cudaMemcpy(dw, w.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemset(dfail, 0, sizeof(int64_t)));
+  CdfBufs b;
+  CK(b.ensure(n, sizeof(T)));
+  WSrc src;
+  src.src = dw;
+  src.M = nullptr;
+  src.mode = 1;
+  int rc = launch_cdf<T>(b, src, n, dq, dcut, dfail, 0, 0);
+  if (rc == PF_OK) {
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) rc = set_err(PF_ERR_CUDA, cudaGetErrorString(e));
+  }
+  int64_t fl = 0;
+  T tot = 0;
+  if (rc == PF_OK) {
+    cudaMemcpy(&fl, dfail, sizeof(int64_t), cudaMemcpyDeviceToHost);
+    cudaMemcpy(&tot, b.total.p, sizeof(T), cudaMemcpyDeviceToHost);
+    if (q_host) cudaMemcpy(q_host, dq, n * sizeof(T), cudaMemcpyDeviceToHost);
+    if (cut_dev_out) cudaMemcpy(cut_dev_out, dcut, n * sizeof(int32_t), cudaMemcpyDeviceToDevice);
+  }
+  b.tile_tot.release(); b.chunk_tot.release(); b.node.release(); b.carry.release(); b.total.release();
+  if (rc != PF_OK) return rc;
+  if (total_host) *total_host = (double)tot;
+  if (!std::isfinite((double)tot)) return set_err(PF_ERR_ALL_WEIGHTS_ZERO, "weight total is not finite");
+  if (fl != 0 || !(tot > 0)) return set_err(PF_ERR_ALL_WEIGHTS_ZERO, "all particle weights are zero");
+  if (q_dev_out) *q_dev_out = dq;
+  return PF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pf_philox_block(uint64_t seed, const uint64_t* ids, int64_t n, uint64_t block, uint64_t* words_out) {
+  int rc;
+  if ((rc = need_device())) return rc;
+  if (n <= 0) return PF_OK;
+  Scratch s;
+  uint64_t *di, *dw;
+  CK(s.alloc(&di, n));
+  CK(s.alloc(&dw, 4 * n));
+  CK(cudaMemcpy(di, ids, n * 8, cudaMemcpyHostToDevice));
+  philox_kernel<<<grid_for(n, 256), 256>>>(seed, di, n, block, dw);
+  LAUNCHED();
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(words_out, dw, 4 * n * 8, cudaMemcpyDeviceToHost));
+  return PF_OK;
+}
+
+int pf_philox4x64(const uint64_t* counters, const uint64_t* keys, int64_t n, uint64_t* words_out) {
+  int rc;
+  if ((rc = need_device())) return rc;
+  if (n <= 0) return PF_OK;
+  Scratch s;
+  uint64_t *dc, *dk, *dw;
+  CK(s.alloc(&dc, 4 * n));
+  CK(s.alloc(&dk, 2 * n));
+  CK(s.alloc(&dw, 4 * n));
+  CK(cudaMemcpy(dc, counters, 4 * n * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dk, keys, 2 * n * 8, cudaMemcpyHostToDevice));
+  philox_full_kernel<<<grid_for(n, 256), 256>>>(dc, dk, n, dw);
+  LAUNCHED();
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(words_out, dw, 4 * n * 8, cudaMemcpyDeviceToHost));
+  return PF_OK;
+}
+
+int pf_uniforms_at(uint64_t seed, const uint64_t* ids, const uint64_t* ctr, int64_t n, double* u_out) {
+  int rc;
+  if ((rc = need_device())) return rc;
+  if (n <= 0) return PF_OK;
+  Scratch s;
+  uint64_t *di, *dc;
+  double* du;
+  CK(s.alloc(&di, n));
+  CK(s.alloc(&dc, n));
+  CK(s.alloc(&du, n));
+  CK(cudaMemcpy(di, ids, n * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dc, ctr, n * 8, cudaMemcpyHostToDevice));
+  uniforms_kernel<<<grid_for(n, 256), 256>>>(seed, di, dc, n, du);
+  LAUNCHED();
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(u_out, du, n * 8, cudaMemcpyDeviceToHost));
+  return PF_OK;
+}
+
+int pf_ndtri(const double* u, int64_t n, double* out) {
+  int rc;
+  if ((rc = need_device())) return rc;
+  if (n <= 0) return PF_OK;
+  Scratch s;
+  double *du, *dz;
+  CK(s.alloc(&du, n));
+  CK(s.alloc(&dz, n));
+  CK(cudaMemcpy(du, u, n * 8, cudaMemcpyHostToDevice));
+  ndtri_kernel<<<grid_for(n, 256), 256>>>(du, n, dz);
+  LAUNCHED();
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(out, dz, n * 8, cudaMemcpyDeviceToHost));
+  return PF_OK;
+}
+
+int pf_gammaincinv(double a, const double* u, int64_t n, int32_t method, double* out) {
+  int rc;
+  if ((rc = need_device())) return rc;
+  if (!(a > 0)) return set_err(PF_ERR_VALUE, "shape must be positive");
+  if (n <= 0) return PF_OK;
+  Scratch s;
+  double *du, *dg, *tab = nullptr, *dsh;
+  CK(s.alloc(&du, n));
+  CK(s.alloc(&dg, n));
+  CK(cudaMemcpy(du, u, n * 8, cudaMemcpyHostToDevice));
+  GammaSrc g;
+  g.method = method;
+  g.shape = a;
+  g.table = nullptr;
+  if (method == 0) {
+    CK(s.alloc(&tab, GT_TABLE_DOUBLES));
+    CK(s.alloc(&dsh, 1));
+    CK(cudaMemcpy(dsh, &a, 8, cudaMemcpyHostToDevice));
+    gamma_table_build_kernel<<<dim3(GT_NSEG, 1), 32>>>(dsh, tab);
+    LAUNCHED();
+    g.table = tab;
+  }
+  gamma_kernel<<<grid_for(n, 256), 256>>>(g, du, n, dg);
+  LAUNCHED();
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(out, dg, n * 8, cudaMemcpyDeviceToHost));
+  return PF_OK;
+}
+
+int pf_tree_cdf(const void* w, int64_t n, int32_t dtype, void* q_out, double* total_out) {
+  int rc;
+  if ((rc = check_weights_host(w, n, dtype))) return rc;
+  if (!is_pow2(n)) return set_err(PF_ERR_NOT_POWER_OF_TWO, "parallel CDF needs a power-of-two particle count, got " + std::to_string(n));
+  if ((rc = need_device())) return rc;
+  Scratch s;
+  std::vector<double> wd = as_f64(w, n, dtype);
+  if (dtype == PF_DTYPE_F32) return tree_cdf_impl<float>(wd, n, (float*)q_out, total_out, nullptr, nullptr, s);
+  return tree_cdf_impl<double>(wd, n, (double*)q_out, total_out, nullptr, nullptr, s);
+}
+
+int pf_adder_tree(const void* w, int64_t n, int32_t dtype, void* levels_out, void* prefix_out) {
+  int rc;
+  if (n < 1 || !is_pow2(n)) return set_err(PF_ERR_NOT_POWER_OF_TWO, "forward adder needs a power-of-two input, got " + std::to_string(n));
+  if ((rc = need_device())) return rc;
+  const size_t es = dtype == PF_DTYPE_F32 ? 4 : 8;
+  Scratch s;
+  unsigned char *lv, *pa, *pb;
+  CK(s.alloc(&lv, (2 * n - 1) * es));
+  CK(s.alloc(&pa, n * es));
+  CK(s.alloc(&pb, n * es));
+  CK(cudaMemcpy(lv, w, n * es, cudaMemcpyHostToDevice));
+  // forward: level offsets n, n/2, ...
+  size_t off = 0;
+  int64_t len = n;
+  std::vector<size_t> offs{0};
+  while (len > 1) {
+    const int64_t m = len / 2;
+    if (es == 8)
+      fwd_level_kernel<double><<<grid_for(m, 256), 256>>>((double*)lv + off, (double*)lv + off + len, m);
+    else
+      fwd_level_kernel<float><<<grid_for(m, 256), 256>>>((float*)lv + off, (float*)lv + off + len, m);
+    LAUNCHED();
+    off += len;
+    len = m;
+    offs.push_back(off);
+  }
+  // backward from the root
+  CK(cudaMemcpy(pa, lv + off * es, es, cudaMemcpyDeviceToDevice));
+  int64_t plen = 1;
+  for (int d = (int)offs.size() - 2; d >= 0; --d) {
+    if (es == 8)
+      bwd_level_kernel<double><<<grid_for(plen, 256), 256>>>((double*)pa, (double*)lv + offs[d], (double*)pb, plen);
+    else
+      bwd_level_kernel<float><<<grid_for(plen, 256), 256>>>((float*)pa, (float*)lv + offs[d], (float*)pb, plen);
+    LAUNCHED();
+    std::swap(pa, pb);
+    plen *= 2;
+  }
+  CK(cudaGetLastError());
+  if (levels_out) CK(cudaMemcpy(levels_out, lv, (2 * n - 1) * es, cudaMemcpyDeviceToHost));
+  if (prefix_out) CK(cudaMemcpy(prefix_out, pa, n * es, cudaMemcpyDeviceToHost));
+  return PF_OK;
+}
+
+int pf_cut_table(const void* q, int64_t n, int32_t dtype, int64_t* cuts_out) {
+  int rc;
+  if (n < 1) return set_err(PF_ERR_VALUE, "empty CDF");
+  if ((rc = need_device())) return rc;
+  const size_t es = dtype == PF_DTYPE_F32 ? 4 : 8;
+  Scratch s;
+  unsigned char* dq;
+  int32_t* dc;
+  int64_t* d64;
+  CK(s.alloc(&dq, n * es));
+  CK(s.alloc(&dc, n));
+  CK(s.alloc(&d64, n));
+  CK(cudaMemcpy(dq, q, n * es, cudaMemcpyHostToDevice));
+  CK(cudaMemset(dc, 0, n * 4));
+  if (es == 8)
+    cut_table_kernel<double><<<grid_for(n, 256), 256>>>((double*)dq, n, dc);
+  else
+    cut_table_kernel<float><<<grid_for(n, 256), 256>>>((float*)dq, n, dc);
+  LAUNCHED();
+  cuts_to_i64_kernel<<<grid_for(n, 256), 256>>>(dc, n, d64);
+  LAUNCHED();
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(cuts_out, d64, n * 8, cudaMemcpyDeviceToHost));
+  return PF_OK;
+}
+
+int pf_cutpoint_lookup(const void* q, const int64_t* cuts, int64_t n, int32_t dtype, const double* u,
+                       int64_t m, int64_t* idx_out) {
+  int rc;
+  if (n < 1) return set_err(PF_ERR_VALUE, "empty CDF");
+  if ((rc = need_device())) return rc;
+  if (m <= 0) return PF_OK;
+  const size_t es = dtype == PF_DTYPE_F32 ? 4 : 8;
+  Scratch s;
+  unsigned char* dq;
+  int64_t *d64, *di;
+  int32_t* dc;
+  double* du;
+  CK(s.alloc(&dq, n * es));
+  CK(s.alloc(&d64, n));
+  CK(s.alloc(&dc, n));
+  CK(s.alloc(&du, m));
+  CK(s.alloc(&di, m));
+  CK(cudaMemcpy(dq, q, n * es, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d64, cuts, n * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(du, u, m * 8, cudaMemcpyHostToDevice));
+  cuts_to_i32_kernel<<<grid_for(n, 256), 256>>>(d64, n, dc);
+  LAUNCHED();
+  if (es == 8)
+    lookup_kernel<double><<<grid_for(m, 256), 256>>>((double*)dq, dc, n, du, m, di);
+  else
+    lookup_kernel<float><<<grid_for(m, 256), 256>>>((float*)dq, dc, n, du, m, di);
+  LAUNCHED();
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(idx_out, di, m * 8, cudaMemcpyDeviceToHost));
+  return PF_OK;
+}
+
+int pf_resample_cutpoint(const void* q, int64_t n, int32_t dtype, uint64_t seed, uint64_t counter,
+                         int64_t* idx_out) {
+  int rc;
+  if (n < 1) return set_err(PF_ERR_VALUE, "empty CDF");
+  if ((rc = need_device())) return rc;
+  const size_t es = dtype == PF_DTYPE_F32 ? 4 : 8;
+  Scratch s;
+  unsigned char* dq;
+  int32_t* dc;
+  double* du;
+  int64_t* di;
+  CK(s.alloc(&dq, n * es));
+  CK(s.alloc(&dc, n));
+  CK(s.alloc(&du, n));
+  CK(s.alloc(&di, n));
+  CK(cudaMemcpy(dq, q, n * es, cudaMemcpyHostToDevice));
+  stream_uniforms_kernel<<<grid_for(n, 256), 256>>>(seed, counter, n, du);
+  LAUNCHED();
+  if (es == 8) {
+    cut_table_kernel<double><<<grid_for(n, 256), 256>>>((double*)dq, n, dc);
+    lookup_kernel<double><<<grid_for(n, 256), 256>>>((double*)dq, dc, n, du, n, di);
+  } else {
+    cut_table_kernel<float><<<grid_for(n, 256), 256>>>((float*)dq, n, dc);
+    lookup_kernel<float><<<grid_for(n, 256), 256>>>((float*)dq, dc, n, du, n, di);
+  }
+  LAUNCHED();
+  LAUNCHED();
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(idx_out, di, n * 8, cudaMemcpyDeviceToHost));
+  return PF_OK;
+}
+
+int pf_weighted_quantiles(const double* values, const void* weights, int32_t wdtype, int64_t n,
+                          const double* probs, int32_t nprobs, double* out) {
+  int rc;
+  if (n < 1) return set_err(PF_ERR_VALUE, "empty values");
+  if (nprobs < 1 || nprobs > 32) return set_err(PF_ERR_VALUE, "1..32 probabilities supported");
+  if ((rc = need_device())) return rc;
+  Scratch s;
+  double *dv, *dw, *dp, *dout;
+  int64_t* dfail;
+  CK(s.alloc(&dv, n));
+  CK(s.alloc(&dw, n));
+  CK(s.alloc(&dp, nprobs));
+  CK(s.alloc(&dout, nprobs));
+  CK(s.alloc(&dfail, 1));
+  std::vector<double> wd = as_f64(weights, n, wdtype);
+  CK(cudaMemcpy(dv, values, n * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dw, wd.data(), n * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dp, probs, nprobs * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemset(dfail, 0, 8));
+  QuantileScratch qs;
+  CK(qs.ensure(n));
+  WSrc src;
+  src.src = dw;
+  src.M = nullptr;
+  src.mode = 1;
+  if (wdtype == PF_DTYPE_F32)
+    rc = weighted_quantiles_dev<float>(qs, dv, src, n, dp, nprobs, dout, 0, dfail);
+  else
+    rc = weighted_quantiles_dev<double>(qs, dv, src, n, dp, nprobs, dout, 0, dfail);
+  if (rc == PF_OK) {
+    cudaError_t e = cudaMemcpy(out, dout, nprobs * 8, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = set_err(PF_ERR_CUDA, cudaGetErrorString(e));
+  }
+  qs.kin.release(); qs.kout.release(); qs.iin.release(); qs.iout.release(); qs.ws.release(); qs.tmp.release();
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,440 @@
+// Particle kernels of the full PF / PL cycle (filtering.py:220-358).
+//
+//  K0  init_kernel        x0, sigma2_0, tau2_0 per slot (filtering.py:225-252)
+//  K1  step_kernel        for slot j at step t:
+//                           resample of step t-1: cut-point lookup of
+//                           u(j, 4(t-1)+3) against q_{t-1} and a joint gather
+//                           of the ancestor's record (filtering.py:305-330)
+//                           -- fused here so the gathered tuple never makes an
+//                           extra trip through HBM;
+//                           propagate + sufficient statistics + parameter
+//                           draws from Philox block t (filtering.py:272-290);
+//                           log-weight (filtering.py:293);
+//                           block max and online-rescaled moment partials
+//                           for the summaries (filtering.py:344-355); the
+//                           last CTA reduces them (max is NaN-propagating,
+//                           AllWeightsZeroError(step) if not finite).
+//  K6  materialize_kernel post-resample particle system (store / keep_final).
+#pragma once
+#include "cdf.cuh"
+#include "philox.cuh"
+#include "special.cuh"
+
+namespace pf {
+
+constexpr double LOG_TWO_PI = 1.8378770664093453;  // math.log(2*math.pi), models.py:20
+
+// Carried per-slot state.  sigma2 is not carried: it is redrawn before it
+// is used (filtering.py:280) and recomputed from the record when a
+// post-resample system is materialised.  a_sigma / a_tau are per-step
+// scalars (every particle adds 1/2 per step, filtering.py:279,285).
+struct alignas(32) Rec {
+  double x, tau2, bs, bt;
+};
+
+enum : int { M_LS = 1, M_LT = 2, M_SINGLE = 4 };
+
+struct GammaSrc {
+  const double* table;  // GT_TABLE_DOUBLES for this step's shape (method 0)
+  double shape;         // method 1
+  int method;
+};
+
+PF_D double gamma_draw(const GammaSrc& g, double u) {
+  if (g.method == 0) return gt_eval(g.table, u);
+  return gamma_quantile_accurate(g.shape, u);
+}
+
+// -------------------------------------------------------- table build ---
+__global__ void __launch_bounds__(32)
+gamma_table_build_kernel(const double* __restrict__ shapes, double* __restrict__ tables) {
+  const int seg = blockIdx.x;
+  const double a = shapes[blockIdx.y];
+  double* out = tables + (size_t)blockIdx.y * GT_TABLE_DOUBLES + seg * GT_NC;
+  __shared__ double f[GT_NC];
+  const int j = threadIdx.x;
+  const double PI = 3.14159265358979323846;
+  if (j < GT_NC) {
+    const double tj = cos(PI * (j + 0.5) / GT_NC);
+    double u, v;
+    bool up;
+    gt_point(seg, tj, &u, &v, &up);
+    f[j] = gamma_quantile_pv(a, u, v, !up);
+  }
+  __syncthreads();
+  if (j == 0) {
+    double c[GT_NC];
+    for (int k = 0; k < GT_NC; ++k) {
+      double s = 0.0;
+      for (int i = 0; i < GT_NC; ++i) s += f[i] * cos(PI * k * (i + 0.5) / GT_NC);
+      c[k] = s * (2.0 / GT_NC);
+    }
+    c[0] *= 0.5;
+    double tm[GT_NC] = {0}, tk[GT_NC] = {0}, mono[GT_NC] = {0};
+    tm[0] = 1.0;
+    tk[1] = 1.0;
+    mono[0] = c[0];
+    for (int i = 0; i < GT_NC; ++i) mono[i] += c[1] * tk[i];
+    for (int k = 2; k < GT_NC; ++k) {
+      double tn[GT_NC];
+      for (int i = 0; i < GT_NC; ++i) tn[i] = (i ? 2.0 * tk[i - 1] : 0.0) - tm[i];
+      for (int i = 0; i < GT_NC; ++i) {
+        mono[i] += c[k] * tn[i];
+        tm[i] = tk[i];
+        tk[i] = tn[i];
+      }
+    }
+    for (int i = 0; i < GT_NC; ++i) out[i] = mono[i];
+  }
+}
+
+// --------------------------------------------------------------- init ---
+struct InitArgs {
+  int64_t n;
+  uint64_t seed;
+  double x0_mean, sqrt_x0_var;
+  double bs0, bt0;          // prior scales
+  double sigma2_fixed, tau2_fixed;
+  GammaSrc gs, gt;
+  const double* feed_z;     // row 0 of the oracle feed (or null)
+  const double* feed_gs;
+  const double* feed_gt;
+  Rec* rec;
+  double* s2_init;          // optional: sigma2 draws (T == 0 keep_final)
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(256) init_kernel(InitArgs a) {
+  constexpr bool LS = MODE & M_LS, LT = MODE & M_LT, SINGLE = MODE & M_SINGLE;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const Philox4 P = philox_block(a.seed, (uint64_t)j, 0);
+    const double z = a.feed_z ? a.feed_z[j] : ndtri(unit_open(P.w[0]));
+    double x0 = a.x0_mean + a.sqrt_x0_var * z;
+    if (SINGLE) x0 = (double)(float)x0;
+    double s2 = a.sigma2_fixed, t2 = a.tau2_fixed;
+    if (LS) s2 = a.bs0 / (a.feed_gs ? a.feed_gs[j] : gamma_draw(a.gs, unit_open(P.w[1])));
+    if (LT) t2 = a.bt0 / (a.feed_gt ? a.feed_gt[j] : gamma_draw(a.gt, unit_open(P.w[2])));
+    Rec r;
+    r.x = x0;
+    r.tau2 = t2;
+    r.bs = a.bs0;
+    r.bt = a.bt0;
+    a.rec[j] = r;
+    if (a.s2_init) a.s2_init[j] = s2;
+  }
+}
+
+// ---------------------------------------------------------------- step ---
+struct Partial {
+  double m, s0, sx, s1s, s2s, s1t, s2t, bad;
+};
+
+struct Scalars {
+  double M;        // max log-weight of the current step
+  double W;        // total weight (moment normalizer)
+  double cs, ct;   // moment shifts (previous step means)
+  unsigned int counter;
+  unsigned int pad;
+};
+
+struct StepOut {   // device arrays indexed by t-1
+  double* fmean;
+  double* s_mean;
+  double* s_sd;
+  double* t_mean;
+  double* t_sd;
+};
+
+template <typename TQ>
+struct StepArgs {
+  int64_t n;
+  int64_t t;             // 1-based step
+  uint64_t seed;
+  double y;
+  double sigma2_fixed, tau2_fixed, sqrt_tau2_fixed, log_term_fixed;
+  GammaSrc gs, gt;
+  const Rec* rec_in;
+  Rec* rec_out;
+  double* lw;            // log-weights (or fed weights when feed_w)
+  uint64_t* u3;          // resampling word of the previous step (in), this step (out)
+  const TQ* q_prev;      // CDF of step t-1 (t > 1)
+  const int32_t* cut_prev;
+  int64_t* idx_out;      // optional 1-based ancestors of step t-1
+  const double* feed_z;  // oracle feed rows for step t (or null)
+  const double* feed_gs;
+  const double* feed_gt;
+  const double* feed_w;
+  double* qx;            // optional SoA copies for the weighted quantiles
+  double* qs;
+  double* qt;
+  Partial* partials;
+  Scalars* sc;
+  StepOut out;
+  int64_t* fail;
+  int64_t per_block;     // particles per CTA (multiple of blockDim)
+};
+
+PF_D double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+PF_D double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <int MODE, typename TQ>
+__global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
+  constexpr bool LS = MODE & M_LS, LT = MODE & M_LT, SINGLE = MODE & M_SINGLE;
+  if (*a.fail) return;
+  const bool feedw = a.feed_w != nullptr;
+  const double cs = a.sc->cs, ct = a.sc->ct;
+  double m = feedw ? 0.0 : -INFINITY;
+  double s0 = 0, sx = 0, s1s = 0, s2s = 0, s1t = 0, s2t = 0;
+  bool bad = false;
+
+  const int64_t lo = blockIdx.x * a.per_block;
+  const int64_t hi = lo + a.per_block < a.n ? lo + a.per_block : a.n;
+  for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
+    // ---- resample of step t-1: cut-point lookup + joint gather
+    int64_t anc = j;
+    if (a.t > 1) {
+      const double u = unit_open(a.u3[j]);
+      anc = cutpoint_lookup<TQ>(a.q_prev, a.cut_prev, a.n, u);
+      if (a.idx_out) a.idx_out[j] = anc + 1;
+    }
+    const Rec r = a.rec_in[anc];
+    // ---- propagate with Philox block t of stream j
+    const Philox4 P = philox_block(a.seed, (uint64_t)j, (uint64_t)a.t);
+    a.u3[j] = P.w[3];
+    const double z = a.feed_z ? a.feed_z[j] : ndtri(unit_open(P.w[0]));
+    const double sq = LT ? sqrt(r.tau2) : a.sqrt_tau2_fixed;
+    const double step = sq * z;
+    double xn = r.x + step;
+    if (SINGLE) xn = (double)(float)xn;
+    const double resid = a.y - xn;
+    const double h = (0.5 * resid) * resid;
+    Rec o;
+    o.x = xn;
+    o.bs = r.bs;
+    o.bt = r.bt;
+    double s2 = a.sigma2_fixed, t2 = a.tau2_fixed;
+    if (LS) {
+      o.bs = r.bs + h;
+      const double g = a.feed_gs ? a.feed_gs[j] : gamma_draw(a.gs, unit_open(P.w[1]));
+      s2 = o.bs / g;
+    }
+    if (LT) {
+      o.bt = r.bt + (0.5 * step) * step;
+      const double g = a.feed_gt ? a.feed_gt[j] : gamma_draw(a.gt, unit_open(P.w[2]));
+      t2 = o.bt / g;
+    }
+    o.tau2 = t2;
+    a.rec_out[j] = o;
+    // ---- log-weight (filtering.py:293)
+    double lw;
+    if (LS)
+      lw = (-0.5) * (LOG_TWO_PI + log(s2)) - h / s2;
+    else
+      lw = a.log_term_fixed - h / s2;
+    double e;
+    if (feedw) {
+      e = a.feed_w[j];
+      a.lw[j] = e;
+    } else {
+      a.lw[j] = lw;
+      if (!(lw == lw) || lw == INFINITY) bad = true;
+      if (lw > m) {
+        const double sc = exp(m - lw);
+        s0 *= sc; sx *= sc; s1s *= sc; s2s *= sc; s1t *= sc; s2t *= sc;
+        m = lw;
+        e = 1.0;
+      } else if (lw > -INFINITY) {
+        e = exp(lw - m);
+      } else {
+        e = 0.0;
+      }
+    }
+    if (a.qx) a.qx[j] = xn;
+    if (a.qs) a.qs[j] = s2;
+    if (a.qt) a.qt[j] = t2;
+    s0 += e;
+    sx = fma(e, xn, sx);
+    const double ds = s2 - cs, dt = t2 - ct;
+    const double eds = e * ds, edt = e * dt;
+    s1s += eds;
+    s2s = fma(eds, ds, s2s);
+    s1t += edt;
+    s2t = fma(edt, dt, s2t);
+  }
+
+  // ---- CTA reduction with rescaling to the CTA max
+  __shared__ double red[8][8];
+  __shared__ double mblk;
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double wm = warp_max(m);
+  if (lane == 0) red[warp][0] = wm;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mm = red[0][0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mm = fmax(mm, red[w][0]);
+    mblk = mm;
+  }
+  __syncthreads();
+  const double mb = mblk;
+  const double scl = (m == -INFINITY) ? 0.0 : exp(m - mb);
+  double v[7] = {s0 * scl, sx * scl, s1s * scl, s2s * scl, s1t * scl, s2t * scl, bad ? 1.0 : 0.0};
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 7; ++k) {
+    const double s = warp_sum(v[k]);
+    if (lane == 0) red[warp][k] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+      for (int k = 0; k < 7; ++k) acc[k] += red[w][k];
+    Partial p;
+    p.m = mb;
+    p.s0 = acc[0]; p.sx = acc[1]; p.s1s = acc[2]; p.s2s = acc[3]; p.s1t = acc[4]; p.s2t = acc[5];
+    p.bad = acc[6];
+    a.partials[blockIdx.x] = p;
+    __threadfence();
+    const unsigned int ticket = atomicAdd(&a.sc->counter, 1u);
+    last = (ticket == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+
+  // ---- last CTA: combine the partials (fixed order -> deterministic)
+  __threadfence();
+  const int G = gridDim.x;
+  double M = -INFINITY, badsum = 0.0;
+  for (int b = threadIdx.x; b < G; b += blockDim.x) {
+    const double mb2 = __ldcg(&a.partials[b].m);
+    M = fmax(M, mb2);
+    badsum += __ldcg(&a.partials[b].bad);
+  }
+  M = warp_max(M);
+  badsum = warp_sum(badsum);
+  __syncthreads();
+  if (lane == 0) { red[warp][0] = M; red[warp][1] = badsum; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mm = red[0][0], bb = red[0][1];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { mm = fmax(mm, red[w][0]); bb += red[w][1]; }
+    mblk = (bb > 0.0) ? NAN : mm;
+  }
+  __syncthreads();
+  M = mblk;
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  for (int b = threadIdx.x; b < G; b += blockDim.x) {
+    const double mb2 = __ldcg(&a.partials[b].m);
+    const double f = (mb2 == -INFINITY) ? 0.0 : exp(mb2 - M);
+    acc[0] += f * __ldcg(&a.partials[b].s0);
+    acc[1] += f * __ldcg(&a.partials[b].sx);
+    acc[2] += f * __ldcg(&a.partials[b].s1s);
+    acc[3] += f * __ldcg(&a.partials[b].s2s);
+    acc[4] += f * __ldcg(&a.partials[b].s1t);
+    acc[5] += f * __ldcg(&a.partials[b].s2t);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const double s = warp_sum(acc[k]);
+    if (lane == 0) red[warp][k] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double S[6] = {0, 0, 0, 0, 0, 0};
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+      for (int k = 0; k < 6; ++k) S[k] += red[w][k];
+    const int64_t i = a.t - 1;
+    const double W = S[0];
+    a.out.fmean[i] = S[1] / W;
+    if (LS) {
+      const double d = S[2] / W;
+      const double var = S[3] / W - d * d;
+      a.out.s_mean[i] = cs + d;
+      a.out.s_sd[i] = sqrt(fmax(var, 0.0));
+      a.sc->cs = cs + d;
+    }
+    if (LT) {
+      const double d = S[4] / W;
+      const double var = S[5] / W - d * d;
+      a.out.t_mean[i] = ct + d;
+      a.out.t_sd[i] = sqrt(fmax(var, 0.0));
+      a.sc->ct = ct + d;
+    }
+    a.sc->M = feedw ? 0.0 : M;
+    a.sc->W = W;
+    a.sc->counter = 0;
+    if (!feedw && !(M > -INFINITY && M < INFINITY))
+      atomicCAS((unsigned long long*)a.fail, 0ull, (unsigned long long)a.t);
+  }
+}
+
+// -------------------------------------------------------- materialize ---
+template <typename TQ>
+struct MatArgs {
+  int64_t n;
+  int64_t t;               // block index of the draws (0 = init system)
+  uint64_t seed;
+  int resample;            // 1: ancestors by lookup of u3 against q/cut
+  const Rec* rec;
+  const uint64_t* u3;
+  const TQ* q;
+  const int32_t* cut;
+  const double* s2_direct; // sigma2 per slot when no resample (init)
+  GammaSrc gs;
+  const double* feed_gs;   // oracle feed row t (indexed by ancestor)
+  int learn_s, learn_t;
+  double sigma2_fixed, tau2_fixed, a_s, a_t;
+  int64_t* idx;            // outputs (each optional)
+  double* x;
+  double* s2;
+  double* t2;
+  double* as;
+  double* bs;
+  double* at;
+  double* bt;
+  const int64_t* fail;
+};
+
+template <typename TQ>
+__global__ void __launch_bounds__(256) materialize_kernel(MatArgs<TQ> a) {
+  if (*a.fail) return;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    int64_t anc = j;
+    if (a.resample) anc = cutpoint_lookup<TQ>(a.q, a.cut, a.n, unit_open(a.u3[j]));
+    if (a.idx) a.idx[j] = anc + 1;
+    const Rec r = a.rec[anc];
+    if (a.x) a.x[j] = r.x;
+    if (a.s2) {
+      double s2 = a.sigma2_fixed;
+      if (a.learn_s) {
+        if (a.s2_direct) {
+          s2 = a.s2_direct[anc];
+        } else {
+          const Philox4 P = philox_block(a.seed, (uint64_t)anc, (uint64_t)a.t);
+          const double g = a.feed_gs ? a.feed_gs[anc] : gamma_draw(a.gs, unit_open(P.w[1]));
+          s2 = r.bs / g;
+        }
+      }
+      a.s2[j] = s2;
+    }
+    if (a.t2) a.t2[j] = a.learn_t ? r.tau2 : a.tau2_fixed;
+    if (a.as) a.as[j] = a.learn_s ? a.a_s : 0.0;
+    if (a.bs) a.bs[j] = a.learn_s ? r.bs : 0.0;
+    if (a.at) a.at[j] = a.learn_t ? a.a_t : 0.0;
+    if (a.bt) a.bt[j] = a.learn_t ? r.bt : 0.0;
+  }
+}
+
+}  // namespace pf

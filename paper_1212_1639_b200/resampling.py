@@ -1,0 +1,124 @@
+"""Exact multinomial resampling by the cut-point method, on the device.
+
+``cut_points_parallel`` (resampling.py:110-134): slot j owns cut-table
+entries (L_{j-1}, L_j] with L_j = ceil(N q_j); ``cutpoint_indices``
+(resampling.py:146-158): start at I_ceil(N u) and advance while u > q(k),
+i.e. the smallest 1-based k with u <= q(k).  Inside the filter loop the same
+lookup runs fused into the step kernel (csrc/step.cuh); these wrappers expose
+it at kernel level with the reference's signatures and 1-based indices.
+
+The reference's sequential baselines (naive / sorted / stratified /
+systematic, resampling.py:29-87) are CPU comparators built on a sequential
+cumsum; they are not part of the cut-point hot path and are not implemented
+on the device in this release (``NotImplementedError``).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .rng import uniforms_at
+
+
+def _cdf_array(cdf):
+    q = np.asarray(cdf)
+    if q.dtype not in (np.float32, np.float64):
+        q = q.astype(np.float64)
+    return np.ascontiguousarray(q)
+
+
+def cut_points_bruteforce(cdf):
+    """O(N^2) oracle: idx[j] = min{ i : q(i) > (j-1)/N } (resampling.py:93-107)."""
+    q = np.asarray(cdf)
+    n = len(q)
+    thresholds = np.arange(n, dtype=q.dtype) / q.dtype.type(n)
+    out = np.empty(n, dtype=np.int64)
+    block = max(1, (1 << 24) // n)
+    for lo in range(0, n, block):
+        hi = min(lo + block, n)
+        out[lo:hi] = np.argmax(q[None, :] > thresholds[lo:hi, None], axis=1) + 1
+    return out
+
+
+def cut_points_parallel(cdf, backend=None):
+    """1-based cut-point table (resampling.py:110-134)."""
+    q = _cdf_array(cdf)
+    out = np.empty(len(q), dtype=np.int64)
+    lib = _lib.require_device()
+    _lib.check(lib.pf_cut_table(_lib.vptr(q), len(q), _lib.dtype_code(q.dtype),
+                                _lib.ptr(out, _lib.C.c_int64)), lib)
+    return out
+
+
+def cutpoint_indices(cdf, cuts, u):
+    """Cut-point lookup for an array of uniforms (resampling.py:146-158)."""
+    q = _cdf_array(cdf)
+    cuts = np.ascontiguousarray(np.asarray(cuts, dtype=np.int64))
+    u = np.ascontiguousarray(np.asarray(u, dtype=np.float64))
+    shape = u.shape
+    u = u.reshape(-1)
+    out = np.empty(len(u), dtype=np.int64)
+    lib = _lib.require_device()
+    _lib.check(lib.pf_cutpoint_lookup(_lib.vptr(q), _lib.ptr(cuts, _lib.C.c_int64), len(q),
+                                      _lib.dtype_code(q.dtype), _lib.ptr(u), len(u),
+                                      _lib.ptr(out, _lib.C.c_int64)), lib)
+    return out.reshape(shape)
+
+
+def cut_point_draw(cdf, cuts, u):
+    """One cut-point lookup (resampling.py:137-143)."""
+    return int(cutpoint_indices(cdf, cuts, np.array([float(u)]))[0])
+
+
+def resample_cutpoint(cdf, streams, backend=None):
+    """Exact multinomial resampling (resampling.py:161-177): one uniform per
+    stream, cut table, lookup; 1-based indices."""
+    q = _cdf_array(cdf)
+    n = len(q)
+    c = streams.lockstep_counter() if hasattr(streams, "lockstep_counter") else None
+    lib = _lib.require_device()
+    if c is not None and len(streams) == n and np.array_equal(
+            streams.stream_ids, np.arange(n, dtype=np.uint64)):
+        out = np.empty(n, dtype=np.int64)
+        _lib.check(lib.pf_resample_cutpoint(_lib.vptr(q), n, _lib.dtype_code(q.dtype),
+                                            np.uint64(streams.seed), np.uint64(c),
+                                            _lib.ptr(out, _lib.C.c_int64)), lib)
+        streams.skip(1)
+        return out
+    u = streams.uniforms()
+    return cutpoint_indices(q, cut_points_parallel(q), u)
+
+
+def merge_indices(cdf, u):
+    """Smallest 1-based i with u < q(i) (resampling.py:29-36)."""
+    return np.searchsorted(np.asarray(cdf), u, side="right") + 1
+
+
+def _not_on_device(name):
+    raise NotImplementedError(
+        f"{name}: the sequential baseline resamplers are CPU comparators of the "
+        "reference and are not implemented on the device; use resample_cutpoint")
+
+
+def resample_naive(cdf, streams):
+    _not_on_device("resample_naive")
+
+
+def resample_sorted(cdf, streams):
+    _not_on_device("resample_sorted")
+
+
+def resample_stratified(cdf, streams):
+    _not_on_device("resample_stratified")
+
+
+def resample_systematic(cdf, stream):
+    _not_on_device("resample_systematic")
+
+
+__all__ = [
+    "cut_point_draw", "cut_points_bruteforce", "cut_points_parallel", "cutpoint_indices",
+    "merge_indices", "resample_cutpoint", "resample_naive", "resample_sorted",
+    "resample_stratified", "resample_systematic", "uniforms_at",
+]

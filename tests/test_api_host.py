@@ -1,0 +1,122 @@
+"""Host-side API behaviour that needs no device: validation order and error
+classes (filtering.py:126-148, 191-192, 203-210), model / prior specs,
+Backend, estimators' sklearn contract, kalman oracle."""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_1212_1639_b200 as P
+
+
+def test_non_power_of_two_rejected_before_device():
+    with pytest.raises(P.NotPowerOfTwoError):
+        P.run_particle_filter(P.TrendNoiseModel(), [1.0], 100, resampler="cutpoint")
+
+
+def test_nan_observations_rejected():
+    with pytest.raises(P.NonFiniteWeightError):
+        P.run_particle_filter(P.TrendNoiseModel(), [1.0, float("nan")], 16)
+
+
+def test_unknown_resampler_and_precision_rejected():
+    with pytest.raises(ValueError):
+        P.run_particle_filter(P.TrendNoiseModel(), [1.0], 16, resampler="bogus")
+    with pytest.raises(ValueError):
+        P.run_particle_filter(P.TrendNoiseModel(), [1.0], 16, precision="half")
+
+
+def test_bad_particle_count():
+    with pytest.raises(ValueError):
+        P.run_particle_filter(P.TrendNoiseModel(), [1.0], 0)
+
+
+def test_priors_type_required():
+    with pytest.raises(TypeError):
+        P.run_particle_learning(P.TrendNoiseModel(), [1.0], 16)
+
+
+def test_observations_must_be_1d():
+    with pytest.raises(ValueError):
+        P.run_particle_filter(P.TrendNoiseModel(), np.ones((2, 2)), 16)
+
+
+def test_model_and_prior_validation():
+    with pytest.raises(ValueError):
+        P.TrendNoiseModel(sigma2=0.0)
+    with pytest.raises(ValueError):
+        P.TrendNoiseModel(tau2=-0.1)
+    with pytest.raises(ValueError):
+        P.InverseGammaPrior(0.0, 1.0)
+    with pytest.raises(ValueError):
+        P.Priors(tau2=-1.0)
+    p = P.Priors(sigma2=P.InverseGammaPrior(5, 4), tau2=0.1)
+    assert p.learns_sigma2 and not p.learns_tau2
+    assert P.InverseGammaPrior(5.0, 4.0).mean == pytest.approx(1.0)
+    assert P.InverseGammaPrior(1.0, 4.0).mean == math.inf
+
+
+def test_backend_modes_and_split():
+    with P.Backend("parallel", lanes=3, min_chunk=3) as b:
+        assert b.split(10) == [(0, 4), (4, 7), (7, 10)]
+    assert P.Backend().mode == "cuda"
+    with pytest.raises(ValueError):
+        P.Backend("gpu-ish")
+    with pytest.raises(ValueError):
+        P.Backend("parallel", lanes=0)
+
+
+def test_check_weights_and_normalize():
+    with pytest.raises(P.NonFiniteWeightError):
+        P.check_weights([1.0, np.inf])
+    with pytest.raises(ValueError):
+        P.check_weights([1.0, -1.0])
+    with pytest.raises(P.AllWeightsZeroError):
+        P.normalize_weights(np.zeros(3))
+    assert np.allclose(P.normalize_weights([1.0, 3.0]), [0.25, 0.75])
+    assert P.is_power_of_two(1024) and not P.is_power_of_two(0)
+
+
+def test_all_weights_zero_message_carries_step():
+    e = P.AllWeightsZeroError(step=7)
+    assert e.step == 7 and "time step 7" in str(e)
+
+
+def test_kalman_filter_closed_forms():
+    m, v = P.kalman_filter([2.0], sigma2=1.0, tau2=0.0, m0=0.0, c0=10.0)
+    assert m[0] == pytest.approx(20.0 / 11.0, rel=1e-14)
+    rng = np.random.default_rng(2)
+    _, v = P.kalman_filter(rng.normal(size=100), 1.0, 0.0, 0.0, 10.0)
+    assert v[-1] == pytest.approx(10.0 / (1.0 + 100 * 10.0), abs=1e-9)
+
+
+def test_log_likelihood_matches_formula():
+    model = P.TrendNoiseModel(sigma2=1.0)
+    assert P.log_likelihood(model, 2.0, 2.0) == pytest.approx(-0.5 * math.log(2 * math.pi))
+    with pytest.raises(P.NonFiniteWeightError):
+        P.log_likelihood(model, float("nan"), 0.0)
+
+
+def test_estimators_sklearn_contract():
+    from sklearn.base import clone
+    from sklearn.exceptions import NotFittedError
+
+    est = P.ParticleLearner(n_particles=256, seed=3)
+    c = clone(est)
+    assert c.get_params()["n_particles"] == 256 and c.get_params()["mode"] == "cuda"
+    with pytest.raises(NotFittedError):
+        c.predict()
+    f = P.ParticleFilter(sigma2=2.0)
+    assert f.get_params()["sigma2"] == 2.0
+
+
+def test_param_summary_accessor():
+    s = P.ParamSummary(mean=np.zeros(2), sd=np.zeros(2), quantiles=np.arange(10.0).reshape(2, 5))
+    assert np.array_equal(s.quantile(0.5), [2.0, 7.0])
+
+
+def test_phase_timings_total():
+    t = P.PhaseTimings(initialize=1, cdf=2, resample=3, resample_sort_only=1, propagate=4,
+                       store=5, other=6)
+    assert t.total == 21 and t.as_dict()["cdf_ns"] == 2

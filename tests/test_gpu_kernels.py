@@ -1,0 +1,223 @@
+"""Kernel-level parity of the sm_100a kernels against the reference's golden
+vectors (tests/golden, produced by the reference itself) and the reference
+test suite's known answers.  Integer / index / tree work must be bit-exact."""
+
+import numpy as np
+import pytest
+
+import paper_1212_1639_b200 as P
+from conftest import golden, random_cdf
+from oracle import restate as R
+from paper_1212_1639_b200 import rng as prng
+
+pytestmark = pytest.mark.gpu
+
+
+# ------------------------------------------------------------- Philox ---
+def test_philox_block_lanes_bit_exact(gpu):
+    d = golden("philox")
+    for i, s in enumerate(d["seeds"]):
+        for j, b in enumerate(d["blocks"]):
+            got = prng.philox_block_lanes(int(b), int(s), d["ids"])
+            assert np.array_equal(got, d["words"][i, j]), (int(s), int(b))
+
+
+def test_philox_matches_numpy_bit_generator(gpu):
+    rng = np.random.default_rng(2024)
+    for _ in range(25):
+        counter = rng.integers(0, 2**64 - 2, size=4, dtype=np.uint64)
+        key = rng.integers(0, 2**64, size=2, dtype=np.uint64)
+        want = np.random.Philox(counter=counter, key=key).random_raw(4)
+        c = [int(x) for x in counter]
+        for k in range(4):  # numpy pre-increments its 256-bit counter
+            c[k] = (c[k] + 1) % 2**64
+            if c[k]:
+                break
+        got = prng.philox4x64_block(*(np.uint64(x) for x in c), key[0], key[1])
+        assert [int(g) for g in got] == [int(w) for w in want]
+
+
+def test_uniforms_at_bit_exact(gpu):
+    d = golden("philox")
+    got = P.uniforms_at(int(d["u_seed"]), d["u_streams"], d["u_counters"])
+    assert np.array_equal(got, d["u_values"])
+    u = P.uniforms_at(3, np.arange(4096, dtype=np.uint64), np.zeros(4096, dtype=np.uint64))
+    assert (u > 0).all() and (u < 1).all()
+
+
+def test_stream_classes(gpu):
+    s = P.RngStream(seed=4, stream_id=2)
+    s.advance(17)
+    assert s.uniform() == P.RngStream(seed=4, stream_id=2, counter=17).uniform()
+    sa = P.StreamArray.for_lanes(21, 128)
+    ids = np.arange(128, dtype=np.uint64)
+    for k in range(6):
+        assert np.array_equal(sa.uniforms(), R.uniforms_at(21, ids, np.full(128, k, dtype=np.uint64)))
+
+
+# ------------------------------------------------------ special funcs ---
+def test_ndtri_vs_scipy(gpu):
+    d = golden("special")
+    u, want = d["u"], d["ndtri"]
+    got = prng.ndtri(u)
+    central = (u > 0.13533528323661269189) & (u < 1 - 0.13533528323661269189)
+    # central branch: only +,-,*,/ -> bit-identical to scipy's Cephes
+    assert np.array_equal(got[central], want[central])
+    # tails go through log(): at most 2 ulp from glibc-based scipy
+    ulp = np.abs(got - want) / np.spacing(np.abs(want))
+    assert ulp.max() <= 2, ulp.max()
+
+
+@pytest.mark.parametrize("method", ["table", "accurate"])
+def test_gammaincinv_vs_scipy(gpu, method):
+    d = golden("special")
+    u = d["u_g"]
+    worst = 0.0
+    for k, a in enumerate(d["shapes"]):
+        got = prng.gammaincinv(float(a), u, method=method)
+        rel = np.abs(got - d["gammaincinv"][k]) / d["gammaincinv"][k]
+        worst = max(worst, float(rel.max()))
+    assert worst <= 2e-13, worst
+
+
+# ------------------------------------------------------------ tree CDF ---
+def test_parallel_cdf_bit_exact_on_reference_fixtures(gpu):
+    d = golden("cdf")
+    for k in range(int(d["count"])):
+        w = d[f"c{k}_w"]
+        q = P.parallel_cdf(w)
+        assert q.dtype == w.dtype
+        assert np.array_equal(q, d[f"c{k}_q"]), str(d[f"c{k}_tag"])
+
+
+@pytest.mark.parametrize("n", [1, 2, 4, 1024, 2048, 4096, 1 << 16, 1 << 20, 1 << 23])
+def test_parallel_cdf_bit_exact_vs_oracle_sizes(gpu, n):
+    rng = np.random.default_rng(n)
+    w = rng.exponential(size=n)
+    w[rng.random(n) < 0.1] = 0.0
+    w[0] += 1.0
+    q = P.parallel_cdf(w)
+    assert np.array_equal(q, R.tree_cdf(w))
+
+
+def test_parallel_cdf_fp32(gpu):
+    rng = np.random.default_rng(4)
+    for n in (4, 512, 1 << 15):
+        w = rng.exponential(size=n).astype(np.float32)
+        assert np.array_equal(P.parallel_cdf(w), R.tree_cdf(w))
+
+
+def test_table1_and_known_answers(gpu):
+    tree = P.forward_adder(np.array([2.0, 4.0, 3.0, 1.0]))
+    assert [list(lv) for lv in tree.levels] == [[2, 4, 3, 1], [6, 4], [10]]
+    assert np.array_equal(P.backward_adder(tree), [2, 6, 9, 10])
+    assert np.array_equal(P.parallel_cdf(np.ones(4)), [0.25, 0.5, 0.75, 1.0])
+    q = P.parallel_cdf(np.array([2.0, 4.0, 3.0, 1.0]))
+    assert np.allclose(q, [0.2, 0.6, 0.9, 1.0]) and q[-1] == 1.0
+
+
+def test_integer_weights_exact(gpu):
+    rng = np.random.default_rng(5)
+    for k in range(0, 17):
+        w = rng.integers(0, 1024, size=1 << k).astype(np.float64)
+        w[0] += 1
+        assert np.array_equal(P.backward_adder(P.forward_adder(w)), np.cumsum(w))
+
+
+def test_cdf_errors(gpu):
+    with pytest.raises(P.AllWeightsZeroError):
+        P.parallel_cdf(np.zeros(8))
+    with pytest.raises(P.NotPowerOfTwoError):
+        P.parallel_cdf(np.ones(6))
+    with pytest.raises(P.NonFiniteWeightError):
+        P.parallel_cdf(np.array([1.0, np.nan]))
+    q = P.parallel_cdf(np.array([1.0, 1.0, 2.0]), pad=True)
+    assert len(q) == 4 and q[-1] == 1.0 and q[-2] == 1.0
+
+
+# --------------------------------------------------- cut points/lookup ---
+def test_cut_table_and_lookup_on_reference_fixtures(gpu):
+    d = golden("cdf")
+    for k in range(int(d["count"])):
+        q = d[f"c{k}_q"]
+        cuts = P.cut_points_parallel(q)
+        assert np.array_equal(cuts, d[f"c{k}_cuts"]), str(d[f"c{k}_tag"])
+        idx = P.cutpoint_indices(q, cuts, d[f"c{k}_u"])
+        assert np.array_equal(idx, d[f"c{k}_idx"])
+        # resample_cutpoint draws the same uniforms from the streams
+        sa = P.StreamArray.for_lanes(11 + k, len(q))
+        assert np.array_equal(P.resample_cutpoint(q, sa), d[f"c{k}_idx"])
+
+
+def test_cutpoint_hand_traces(gpu):
+    q4 = np.array([0.2, 0.6, 0.9, 1.0])
+    cuts = P.cut_points_parallel(q4)
+    assert np.array_equal(cuts, [1, 2, 2, 3])
+    assert P.cut_point_draw(q4, cuts, 0.55) == 2
+    assert P.cut_point_draw(q4, cuts, 0.95) == 4
+    assert np.array_equal(P.cutpoint_indices(q4, cuts, np.array([0.55, 0.95, 0.05, 0.70])),
+                          [2, 4, 1, 3])
+    q = np.array([0.0, 0.0, 1.0, 1.0])
+    assert (P.resample_cutpoint(q, P.StreamArray.for_lanes(3, 4)) == 3).all()
+
+
+def test_cut_table_equals_bruteforce_random(gpu):
+    rng = np.random.default_rng(10)
+    for n in (2, 4, 8, 16, 32, 64, 128, 256):
+        for _ in range(20):
+            q = random_cdf(rng, n, zero_fraction=float(rng.random() < 0.3) * 0.4)
+            assert np.array_equal(P.cut_points_parallel(q), P.cut_points_bruteforce(q))
+    for n in (2, 4, 8, 32):
+        for atom in range(n):
+            q = np.zeros(n)
+            q[atom:] = 1.0
+            assert np.array_equal(P.cut_points_parallel(q), P.cut_points_bruteforce(q))
+
+
+def test_lookup_equals_searchsorted_left_large(gpu):
+    rng = np.random.default_rng(7)
+    n = 1 << 20
+    w = rng.exponential(size=n) * (rng.random(n) > 0.2)
+    w[0] = 1.0
+    q = R.tree_cdf(w)
+    u = rng.random(1 << 20)
+    idx = P.cutpoint_indices(q, P.cut_points_parallel(q), u)
+    assert np.array_equal(idx, np.searchsorted(q, u, side="left") + 1)
+
+
+def test_never_selects_zero_weight(gpu):
+    rng = np.random.default_rng(19)
+    q = random_cdf(rng, 128, zero_fraction=0.5)
+    idx = P.resample_cutpoint(q, P.StreamArray.for_lanes(21, 128))
+    mass = np.diff(q, prepend=0.0)
+    assert (mass[idx - 1] > 0).all()
+
+
+def test_multinomial_frequencies(gpu):
+    q = R.tree_cdf(np.array([2.0, 4.0, 3.0, 1.0, 5.0, 8.0, 2.0, 7.0]))
+    m = 200_000
+    u = P.RngStream(23, 0).uniforms(m)
+    idx = P.cutpoint_indices(q, P.cut_points_parallel(q), u)
+    counts = np.bincount(idx, minlength=9)[1:]
+    p = np.diff(q, prepend=0.0)
+    se = np.sqrt(m * p * (1 - p))
+    assert (np.abs(counts - m * p) <= 4 * se).all()
+
+
+# --------------------------------------------------- weighted quantiles ---
+def test_weighted_quantiles_semantics(gpu):
+    v = np.array([5.0, 1.0, 3.0])
+    w = np.array([0.0, 1.0, 0.0])
+    assert (P.weighted_quantiles(v, w, (0.05, 0.5, 0.95)) == 1.0).all()
+    assert P.weighted_quantiles(np.arange(101.0), np.ones(101), (0.5,))[0] == 50.0
+    rng = np.random.default_rng(0)
+    for n in (7, 200, 5000, 1 << 18):
+        v = rng.normal(size=n)
+        w = rng.random(n)
+        probs = (0.005, 0.05, 0.5, 0.95, 0.995)
+        assert np.array_equal(P.weighted_quantiles(v, w, probs), R.weighted_quantiles(v, w, probs))
+    # ties resolved by value, float32 weights
+    v = np.repeat(np.arange(50.0), 20)
+    w = rng.random(1000).astype(np.float32)
+    assert np.array_equal(P.weighted_quantiles(v, w, (0.1, 0.5, 0.9)),
+                          R.weighted_quantiles(v, w, (0.1, 0.5, 0.9)))
