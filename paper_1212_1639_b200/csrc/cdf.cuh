@@ -248,10 +248,13 @@ cdf_expand_kernel(WSrc src, int64_t n, int R, const T* __restrict__ tile_tot,
       plen *= 2;
       for (int i = 0; i < plen; ++i) bw[i] = nb[i];
     }
+    // carries are node values (prefix-sum units); the running max of q over
+    // the preceding elements is (max node) / total since division by a
+    // positive total is monotone.
     T m = carry[chunk];
     for (int r = 0; r < R; ++r) {
       tnode[r] = bw[r];
-      tcarry[r] = m;
+      tcarry[r] = m / total;
       m = fmax(m, bw[r]);
     }
   }
