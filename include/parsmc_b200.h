@@ -138,6 +138,10 @@ int pf_engine_run_resident(pf_engine* e, int64_t t_len);
  * average duration and launch count of the step kernel inside it. */
 int pf_engine_last_timing(pf_engine* e, double* total_ms, double* step_kernel_ms,
                           int64_t* step_kernel_launches, int64_t* kernels_launched);
+/* Weighted-quantile diagnostics of the last run: [0] quantiles resolved on
+ * a truncated candidate set (should be 0), [1] window misses that needed
+ * the fallback pass, [2] largest candidate list, [3] resolves performed. */
+int pf_engine_quantile_stats(pf_engine* e, int64_t* stats4);
 int pf_engine_destroy(pf_engine* e);
 
 /* ------------------------------------------------- kernel level (L2) --- */

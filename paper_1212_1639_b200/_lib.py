@@ -87,6 +87,7 @@ SIGNATURES = {
     "pf_engine_run": (C.c_int, [C.c_void_p, _dp, C.c_int64, C.POINTER(PfFeed), C.POINTER(PfOutputs)]),
     "pf_engine_run_resident": (C.c_int, [C.c_void_p, C.c_int64]),
     "pf_engine_last_timing": (C.c_int, [C.c_void_p, _dp, _dp, _i64p, _i64p]),
+    "pf_engine_quantile_stats": (C.c_int, [C.c_void_p, _i64p]),
     "pf_engine_destroy": (C.c_int, [C.c_void_p]),
     "pf_philox_block": (C.c_int, [C.c_uint64, _u64p, C.c_int64, C.c_uint64, _u64p]),
     "pf_philox4x64": (C.c_int, [_u64p, _u64p, C.c_int64, _u64p]),

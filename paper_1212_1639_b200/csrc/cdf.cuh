@@ -25,6 +25,7 @@
 #include <math.h>
 
 #include "common.cuh"
+#include "philox.cuh"
 
 namespace pf {
 
@@ -207,16 +208,48 @@ cdf_top_kernel(const T* __restrict__ chunk_tot, int64_t G, T* __restrict__ node,
   }
 }
 
+// ------------------------------------------------ stratum lookup tables ---
+// For N = 2^n with n >= 21 the cut-point lookup runs on integers.  A uniform
+// u = K 2^-53 (K odd, 53 bits: unit_open) falls in stratum s = ceil(N u) =
+// (K >> B) + 1 with B = 53 - n, at offset r = K & (2^B - 1).  A particle k
+// whose CDF value lies in the same stratum (L_k = ceil(N q_k) = s) has
+// F_k = floor(q_k 2^53 - (s-1) 2^B) < 2^32, and u > q_k  <=>  r > F_k
+// exactly (r is an integer).  So the table per stratum is the cut point
+// I_s plus F of that first candidate (a sentinel when its CDF value lies
+// beyond the stratum), and the walk continues over per-particle (L, F)
+// pairs only when u lies past the first candidate.  Same answer as
+// cutpoint_indices (resampling.py:146-158), bit for bit.
+struct SRec {
+  int32_t first;  // 0-based I_s
+  uint32_t f;     // F of I_s if L_{I_s} == s, else 0xFFFFFFFF
+};
+struct PRec {
+  int32_t L;      // ceil(N q_k) (0 for a zero-mass prefix)
+  uint32_t f;
+};
+constexpr int STRATA_MIN_LOG2N = 21;
+
+template <typename T>
+PF_D uint32_t strata_f(T q, int64_t L, int B) {
+  if (L <= 0) return 0u;
+  const double x = (double)q * 9007199254740992.0;          // q 2^53, exact
+  const double sub = (double)(L - 1) * ldexp(1.0, B);       // exact
+  const double d = floor(x - sub);                          // exact (Sterbenz)
+  return d >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)d;
+}
+
 // ------------------------------------------------------------------ K4 ---
 template <typename T>
 PF_D T clip01(T x) { return fmin(fmax(x, (T)0), (T)1); }
 
-template <typename T>
+template <typename T, bool STRATA = false>
 __global__ void __launch_bounds__(CDF_THREADS)
 cdf_expand_kernel(WSrc src, int64_t n, int R, const T* __restrict__ tile_tot,
                   const T* __restrict__ node, const T* __restrict__ carry,
                   const T* __restrict__ total_p, T* __restrict__ q_out,
-                  int32_t* __restrict__ cut_out, const int64_t* __restrict__ fail) {
+                  int32_t* __restrict__ cut_out, const int64_t* __restrict__ fail,
+                  SRec* __restrict__ srec_out = nullptr, PRec* __restrict__ pf_out = nullptr,
+                  int B = 0) {
   if (fail && *fail) return;
   __shared__ T wt[CDF_THREADS / 32];
   __shared__ T wmax[CDF_THREADS / 32];
@@ -334,11 +367,27 @@ cdf_expand_kernel(WSrc src, int64_t n, int R, const T* __restrict__ tile_tot,
       if (base + i == n - 1) qi = (T)1;
       qv[i] = qi;
       const int64_t L = (int64_t)ceil(qi * nf);
-      for (int64_t kk = Lprev; kk < L; ++kk) cut_out[kk] = (int32_t)(base + i);
+      if (STRATA) {
+        const uint32_t f = strata_f<T>(qi, L, B);
+        PRec pr;
+        pr.L = (int32_t)L;
+        pr.f = f;
+        pf_out[base + i] = pr;
+        for (int64_t kk = Lprev; kk < L; ++kk) {
+          SRec sr;
+          sr.first = (int32_t)(base + i);
+          sr.f = (kk == L - 1) ? f : 0xFFFFFFFFu;
+          srec_out[kk] = sr;
+        }
+      } else {
+        for (int64_t kk = Lprev; kk < L; ++kk) cut_out[kk] = (int32_t)(base + i);
+      }
       Lprev = L > Lprev ? L : Lprev;
     }
+    if (!STRATA) {
 #pragma unroll
-    for (int i = 0; i < CDF_V; ++i) q_out[base + i] = qv[i];
+      for (int i = 0; i < CDF_V; ++i) q_out[base + i] = qv[i];
+    }
     __syncthreads();
   }
 }
@@ -411,6 +460,41 @@ PF_D int64_t cutpoint_lookup(const T* __restrict__ q, const int32_t* __restrict_
   int64_t k = cut[s - 1];
   while (u > (double)q[k]) ++k;
   return k;
+}
+
+// The resampling table of one step: (q, cut) for small n, strata tables
+// for n >= 2^21 (see SRec).  ancestor_of() takes the raw Philox word whose
+// unit_open() is the resampling uniform.
+template <typename TQ>
+struct Lookup {
+  const TQ* q;
+  const int32_t* cut;
+  const SRec* srec;  // non-null: strata path
+  const PRec* pf;
+  int B;
+  int64_t n;
+};
+
+template <typename TQ>
+PF_D int64_t ancestor_of(const Lookup<TQ>& L, uint64_t w3) {
+  if (L.srec) {
+    const uint64_t K = ((w3 >> 12) << 1) | 1ull;  // u = K 2^-53
+    const uint64_t s0 = K >> L.B;                 // stratum - 1
+    const uint32_t r = (uint32_t)(K & ((1ull << L.B) - 1ull));
+    const SRec R = L.srec[s0];
+    int64_t k = R.first;
+    if (r > R.f) {
+      ++k;
+      const int32_t s = (int32_t)s0 + 1;
+      for (;;) {
+        const PRec p = L.pf[k];
+        if (p.L != s || r <= p.f) break;
+        ++k;
+      }
+    }
+    return k;
+  }
+  return cutpoint_lookup<TQ>(L.q, L.cut, L.n, unit_open(w3));
 }
 
 }  // namespace pf

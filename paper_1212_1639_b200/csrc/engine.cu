@@ -10,7 +10,9 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -18,7 +20,7 @@
 #include <vector>
 
 #include "../../include/parsmc_b200.h"
-#include "step.cuh"
+#include "quantile.cuh"
 
 using namespace pf;
 
@@ -180,9 +182,19 @@ struct CdfBufs {
   }
 };
 
+struct StrataOut {
+  SRec* srec = nullptr;
+  PRec* pf = nullptr;
+  int B = 0;
+};
+
+template <typename T>
+int launch_cdf_tail(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t* fail, int64_t step,
+                    cudaStream_t st, StrataOut so = StrataOut());
+
 template <typename T>
 int launch_cdf(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t* fail, int64_t step,
-               cudaStream_t st) {
+               cudaStream_t st, StrataOut so = StrataOut()) {
   const CdfPlan& p = b.plan;
   T* total = (T*)b.total.p;
   if (p.small) {
@@ -190,12 +202,22 @@ int launch_cdf(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t* fai
     LAUNCHED();
     return PF_OK;
   }
+  cdf_reduce_kernel<T><<<(int)p.chunks, CDF_THREADS, 0, st>>>(src, p.R, (T*)b.tile_tot.p,
+                                                              (T*)b.chunk_tot.p, fail);
+  LAUNCHED();
+  return launch_cdf_tail<T>(b, src, n, q, cut, fail, step, st, so);
+}
+
+// K3 + K4 (after K2, or after the quantile-fused K2).
+template <typename T>
+int launch_cdf_tail(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t* fail, int64_t step,
+                    cudaStream_t st, StrataOut so) {
+  const CdfPlan& p = b.plan;
+  T* total = (T*)b.total.p;
   T* tt = (T*)b.tile_tot.p;
   T* ct = (T*)b.chunk_tot.p;
   T* nd = (T*)b.node.p;
   T* cr = (T*)b.carry.p;
-  cdf_reduce_kernel<T><<<(int)p.chunks, CDF_THREADS, 0, st>>>(src, p.R, tt, ct, fail);
-  LAUNCHED();
   const size_t smem = 4 * p.chunks * sizeof(T);
   static bool attr_set[2] = {false, false};
   if (!attr_set[sizeof(T) == 8]) {
@@ -205,8 +227,12 @@ int launch_cdf(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t* fai
   }
   cdf_top_kernel<T><<<1, 1024, smem, st>>>(ct, p.chunks, nd, cr, total, fail, step);
   LAUNCHED();
-  cdf_expand_kernel<T><<<(int)p.chunks, CDF_THREADS, 0, st>>>(src, n, p.R, tt, nd, cr, total, q, cut,
-                                                              fail);
+  if (so.srec)
+    cdf_expand_kernel<T, true><<<(int)p.chunks, CDF_THREADS, 0, st>>>(src, n, p.R, tt, nd, cr, total, q, cut,
+                                                                    fail, so.srec, so.pf, so.B);
+  else
+    cdf_expand_kernel<T, false><<<(int)p.chunks, CDF_THREADS, 0, st>>>(src, n, p.R, tt, nd, cr, total, q, cut,
+                                                                     fail);
   LAUNCHED();
   return PF_OK;
 }
@@ -221,25 +247,38 @@ struct pf_engine {
   int mode = 0;  // M_LS | M_LT | M_SINGLE
   bool single = false;
   DevBuf<Rec> rec[2];
-  DevBuf<double> lw;
+  DevBuf<double> lw;      // log-weights, double-buffered by step parity: [2][n]
   DevBuf<uint64_t> u3;
   DevBuf<unsigned char> q;
   DevBuf<int32_t> cut;
+  DevBuf<SRec> srec;      // strata tables (n >= 2^21) replace q / cut
+  DevBuf<PRec> pfr;
+  bool strata = false;
   DevBuf<int64_t> idx;
-  DevBuf<double> qx, qs, qt;
+  DevBuf<uint32_t> keys;  // quantile keys [2 parities][3 quantities][n]
   DevBuf<double> s2init;
+  // weighted-quantile machinery (quantile.cuh)
+  DevBuf<QTarget> qtg;
+  DevBuf<QShared> qsh;    // [2] by step parity
+  DevBuf<QCand> qcand;
+  DevBuf<double> qpart, qscratch;
+  DevBuf<double> mbuf;    // max log-weight per parity
+  DevBuf<unsigned long long> qhist, qfhist;
+  DevBuf<unsigned int> qunres;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_b = nullptr, ev_e = nullptr;
   DevBuf<Partial> partials;
   DevBuf<Scalars> sc;
   DevBuf<int64_t> fail;
   CdfBufs cdf;
-  QuantileScratch qsc;
   // per-run outputs (device)
   DevBuf<double> o_fm, o_sm, o_ssd, o_tm, o_tsd, o_fq, o_sq, o_tq;
   DevBuf<double> probs;  // [0..5) param probs, [5..8) state probs
   // gamma tables for the shape schedule a0 + t/2, t = 0..T
-  DevBuf<double> tab_s, tab_t, shapes_buf;
-  std::vector<double> shapes_s, shapes_t;
-  bool shared_table = false;
+  const double* tab_s = nullptr;  // cached per-step gamma tables (not owned)
+  const double* tab_t = nullptr;
+  const std::vector<double>* sh_s = nullptr;
+  const std::vector<double>* sh_t = nullptr;
   // materialise scratch
   DevBuf<double> m_x, m_s2, m_t2, m_as, m_bs, m_at, m_bt;
   DevBuf<double> feed_buf;
@@ -247,68 +286,91 @@ struct pf_engine {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<cudaEvent_t> evs;
   double last_total_ms = 0, last_step_ms = 0;
+  int64_t qstats[4] = {0, 0, 0, 0};  // quantile: unresolved, fallbacks, max candidates, resolves
   int64_t last_step_launches = 0, last_kernels = 0;
   std::vector<double> y_host;
 };
 
 namespace {
 
+// Process-wide cache of per-step inverse-gamma tables, keyed by (device,
+// prior shape).  The schedule a0, a0+1/2, ... is a prefix-closed sequence, so
+// one table set built for T serves every run with T' <= T; it grows by
+// doubling and is kept for the life of the process (tables are ~41 KB/step).
+struct TableEntry {
+  int device;
+  double a0;
+  std::vector<double> shapes;
+  double* tab;
+};
+std::vector<TableEntry> g_tables;
+std::mutex g_tables_mu;
+
+int cached_table(int device, double a0, int64_t T, cudaStream_t st, const TableEntry** out) {
+  std::lock_guard<std::mutex> lk(g_tables_mu);
+  for (auto& te : g_tables)
+    if (te.device == device && te.a0 == a0 && (int64_t)te.shapes.size() > T) {
+      *out = &te;
+      return PF_OK;
+    }
+  int64_t prev = 0;
+  for (auto& te : g_tables)
+    if (te.device == device && te.a0 == a0) prev = std::max<int64_t>(prev, (int64_t)te.shapes.size());
+  const int64_t len = std::max<int64_t>(T + 1, std::max<int64_t>(2 * prev, 64));
+  TableEntry te;
+  te.device = device;
+  te.a0 = a0;
+  te.shapes.resize((size_t)len);
+  double a = a0;
+  te.shapes[0] = a;
+  for (int64_t t = 1; t < len; ++t) {
+    a = a + 0.5;  // a_sig = a_sig + 0.5 (filtering.py:279, 285)
+    te.shapes[(size_t)t] = a;
+  }
+  double* dsh = nullptr;
+  CK(cudaMalloc((void**)&te.tab, (size_t)len * GT_TABLE_DOUBLES * sizeof(double)));
+  CK(cudaMalloc((void**)&dsh, (size_t)len * sizeof(double)));
+  CK(cudaMemcpyAsync(dsh, te.shapes.data(), len * sizeof(double), cudaMemcpyHostToDevice, st));
+  for (int64_t lo = 0; lo < len; lo += 60000) {
+    const int64_t cnt = std::min<int64_t>(60000, len - lo);
+    gamma_table_build_kernel<<<dim3(GT_NSEG, (unsigned)cnt), 32, 0, st>>>(dsh + lo, te.tab + (size_t)lo * GT_TABLE_DOUBLES);
+    LAUNCHED();
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
+  cudaFree(dsh);
+  g_tables.push_back(std::move(te));
+  *out = &g_tables.back();
+  return PF_OK;
+}
+
 int build_tables(pf_engine* e, int64_t T) {
+  e->tab_s = e->tab_t = nullptr;
+  e->sh_s = e->sh_t = nullptr;
   if (e->cfg.gamma_method != 0) return PF_OK;
   const bool ls = e->cfg.learn && e->cfg.learn_sigma2, lt = e->cfg.learn && e->cfg.learn_tau2;
-  if (!ls && !lt) return PF_OK;
-  auto schedule = [&](double a0) {
-    std::vector<double> v((size_t)T + 1);
-    double a = a0;
-    v[0] = a;
-    for (int64_t t = 1; t <= T; ++t) {
-      a = a + 0.5;  // a_sig = a_sig + 0.5 (filtering.py:279)
-      v[(size_t)t] = a;
-    }
-    return v;
-  };
-  std::vector<double> ss = ls ? schedule(e->cfg.sigma2_shape) : std::vector<double>();
-  std::vector<double> tt = lt ? schedule(e->cfg.tau2_shape) : std::vector<double>();
-  auto covered = [](const std::vector<double>& have, const std::vector<double>& want) {
-    if (want.empty()) return true;
-    if (have.size() < want.size()) return false;
-    return std::memcmp(have.data(), want.data(), want.size() * sizeof(double)) == 0;
-  };
-  if (covered(e->shapes_s, ss) && covered(e->shapes_t, tt)) return PF_OK;
-  const bool share = ls && lt && e->cfg.sigma2_shape == e->cfg.tau2_shape;
-  auto build = [&](const std::vector<double>& sh, DevBuf<double>& tab) -> int {
-    CK(e->shapes_buf.ensure(sh.size()));
-    CK(tab.ensure(sh.size() * GT_TABLE_DOUBLES));
-    CK(cudaMemcpyAsync(e->shapes_buf.p, sh.data(), sh.size() * sizeof(double),
-                       cudaMemcpyHostToDevice, e->st));
-    dim3 grid(GT_NSEG, (unsigned)sh.size());
-    gamma_table_build_kernel<<<grid, 32, 0, e->st>>>(e->shapes_buf.p, tab.p);
-    LAUNCHED();
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(e->st));
-    return PF_OK;
-  };
+  const TableEntry* te;
   int rc;
-  if (ls && (rc = build(ss, e->tab_s)) != PF_OK) return rc;
-  if (lt && !share && (rc = build(tt, e->tab_t)) != PF_OK) return rc;
-  e->shapes_s = ss;
-  e->shapes_t = share ? ss : tt;
-  e->shared_table = share;
+  if (ls) {
+    if ((rc = cached_table(e->cfg.device, e->cfg.sigma2_shape, T, e->st, &te)) != PF_OK) return rc;
+    e->tab_s = te->tab;
+    e->sh_s = &te->shapes;
+  }
+  if (lt) {
+    if ((rc = cached_table(e->cfg.device, e->cfg.tau2_shape, T, e->st, &te)) != PF_OK) return rc;
+    e->tab_t = te->tab;
+    e->sh_t = &te->shapes;
+  }
   return PF_OK;
 }
 
 GammaSrc gamma_src(pf_engine* e, bool sigma, int64_t t) {
   GammaSrc g;
   g.method = e->cfg.gamma_method;
-  const std::vector<double>& sh = sigma ? e->shapes_s : e->shapes_t;
-  const double a0 = sigma ? e->cfg.sigma2_shape : e->cfg.tau2_shape;
-  g.shape = sh.empty() ? a0 + 0.5 * t : sh[(size_t)t];
-  if (g.method == 1 && sh.empty()) {
-    double a = a0;
-    for (int64_t k = 0; k < t; ++k) a = a + 0.5;
-    g.shape = a;
-  }
-  const double* base = sigma || e->shared_table ? e->tab_s.p : e->tab_t.p;
+  double a = sigma ? e->cfg.sigma2_shape : e->cfg.tau2_shape;
+  for (int64_t k = 0; k < t; ++k) a = a + 0.5;
+  g.shape = a;
+  const double* base = sigma ? e->tab_s : e->tab_t;
   g.table = base ? base + (size_t)t * GT_TABLE_DOUBLES : nullptr;
   return g;
 }
@@ -330,6 +392,7 @@ struct RunSpec {
 template <int MODE, typename TQ>
 int run_impl(pf_engine* e, const RunSpec& rs) {
   constexpr bool LS = MODE & M_LS, LT = MODE & M_LT;
+  constexpr int SINGLE = (MODE & M_SINGLE) ? 1 : 0;
   const pf_config& c = e->cfg;
   const int64_t n = e->n, T = rs.T;
   cudaStream_t st = e->st;
@@ -349,11 +412,61 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   if (LS) { CK(e->o_sm.ensure(TT)); CK(e->o_ssd.ensure(TT)); CK(e->o_sq.ensure(TT * 5)); }
   if (LT) { CK(e->o_tm.ensure(TT)); CK(e->o_tsd.ensure(TT)); CK(e->o_tq.ensure(TT * 5)); }
   if (want_fq) CK(e->o_fq.ensure(TT * 3));
-  if (want_fq) CK(e->qx.ensure(n));
-  if (want_sq) CK(e->qs.ensure(n));
-  if (want_tq) CK(e->qt.ensure(n));
-  if (want_fq || want_sq || want_tq) CK(e->qsc.ensure(n));
   if (keep_idx) CK(e->idx.ensure(n));
+
+  // ---- weighted-quantile targets (filtering.py:346-355): state probs when
+  // tracked, five parameter probs per learned variance.
+  std::vector<QTarget> tgs;
+  {
+    const double sp[3] = {0.05, 0.5, 0.95};
+    const double pp[5] = {0.005, 0.05, 0.5, 0.95, 0.995};
+    auto add = [&](int q, const double* ps, int np) {
+      for (int i = 0; i < np; ++i) {
+        QTarget t;
+        memset(&t, 0, sizeof(t));
+        t.p = ps[i];
+        t.q = q;
+        t.col = i;
+        t.zprev = ndtri(ps[i]);  // normal start; learned from step 1 on
+        t.h = 0.25;
+        tgs.push_back(t);
+      }
+    };
+    if (want_fq) add(0, sp, 3);
+    if (want_sq) add(1, pp, 5);
+    if (want_tq) add(2, pp, 5);
+  }
+  const int ntg = (int)tgs.size();
+  const uint32_t qcap = (uint32_t)std::max<int64_t>(4096, n / 4);
+  QArgs qa;
+  memset(&qa, 0, sizeof(qa));
+  qa.ntarget = ntg;
+  if (ntg) {
+    CK(e->keys.ensure((size_t)6 * n));
+    CK(e->qtg.ensure(Q_MAXT));
+    CK(e->qsh.ensure(2));
+    CK(e->qcand.ensure((size_t)ntg * qcap));
+    CK(e->qscratch.ensure((size_t)ntg * qcap));
+    CK(e->qpart.ensure((size_t)std::max<int64_t>(CDF_MAX_CHUNKS, sm_count() * 8) * (Q_MAXT + 1)));
+    CK(e->qhist.ensure((size_t)Q_MAXT * Q_SUB));
+    CK(e->qfhist.ensure((size_t)Q_MAXT * Q_FB));
+    CK(e->qunres.ensure(4));
+    CK(cudaMemcpyAsync(e->qtg.p, tgs.data(), ntg * sizeof(QTarget), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(e->qsh.p, 0, 2 * sizeof(QShared), st));
+    CK(cudaMemsetAsync(e->qhist.p, 0, (size_t)Q_MAXT * Q_SUB * 8, st));
+    CK(cudaMemsetAsync(e->qfhist.p, 0, (size_t)Q_MAXT * Q_FB * 8, st));
+    CK(cudaMemsetAsync(e->qunres.p, 0, 4 * sizeof(unsigned int), st));
+    qa.stats = e->qunres.p;
+    qa.tg = e->qtg.p;
+    qa.cand = e->qcand.p;
+    qa.cap = qcap;
+    qa.part = e->qpart.p;
+    qa.hist = e->qhist.p;
+    qa.fhist = e->qfhist.p;
+    qa.fx_scale = std::ldexp(1.0, 62 - ilog2(n));  // sum of all n weights (each <= 1) fits
+  }
+  // both CUDA streams must see the reset before the loop
+  CK(cudaEventRecord(e->ev_e, st));
 
   // oracle feed: whole [T+1][n] arrays uploaded once
   const double *fz = nullptr, *fgs = nullptr, *fgt = nullptr, *fw = nullptr;
@@ -442,15 +555,49 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   per_block = (per_block + 255) / 256 * 256;
   step_grid = (int)((n + per_block - 1) / per_block);
 
+  // shared-memory copies of the step's gamma table(s)
+  const bool share_tab = LS && LT && e->tab_s == e->tab_t && c.gamma_method == 0;
+  const size_t step_smem = c.gamma_method == 0
+      ? (size_t)((LS ? 1 : 0) + (LT && !share_tab ? 1 : 0)) * GT_TABLE_DOUBLES * sizeof(double) : 0;
+  {
+    static bool attr[8] = {false};
+    if (!attr[MODE]) {
+      CK(cudaFuncSetAttribute(step_kernel<MODE, TQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              2 * GT_TABLE_DOUBLES * (int)sizeof(double)));
+      attr[MODE] = true;
+    }
+  }
+
   int cur = 0;
   WSrc wsrc;
-  wsrc.src = e->lw.p;
-  wsrc.M = &e->sc.p->M;
   wsrc.mode = fw ? 1 : 0;
   TQ* qv = (TQ*)e->q.p;
   int64_t step_launches = 0;
+  const CdfPlan plan = cdf_plan(n);
+  StrataOut so;
+  Lookup<TQ> lk;
+  lk.q = qv;
+  lk.cut = e->cut.p;
+  lk.srec = nullptr;
+  lk.pf = nullptr;
+  lk.B = 53 - ilog2(n);
+  lk.n = n;
+  if (e->strata) {
+    so.srec = e->srec.p;
+    so.pf = e->pfr.p;
+    so.B = lk.B;
+    lk.srec = e->srec.p;
+    lk.pf = e->pfr.p;
+  }
+  const int fb_grid = grid_for(n, 256, sms * 4);
 
   for (int64_t t = 1; t <= T; ++t) {
+    const int par = (int)(t & 1);
+    double* lwp = e->lw.p + (size_t)par * n;
+    wsrc.src = lwp;
+    wsrc.M = e->mbuf.p + par;
+    uint32_t* kbase = ntg ? e->keys.p + (size_t)par * 3 * n : nullptr;
+    QShared* qshp = ntg ? e->qsh.p + par : nullptr;
     // ---- K1
     StepArgs<TQ> a;
     a.n = n;
@@ -465,18 +612,19 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     a.gt = gamma_src(e, false, t);
     a.rec_in = e->rec[cur].p;
     a.rec_out = e->rec[cur ^ 1].p;
-    a.lw = e->lw.p;
+    a.lw = lwp;
+    a.Mout = e->mbuf.p + par;
     a.u3 = e->u3.p;
-    a.q_prev = qv;
-    a.cut_prev = e->cut.p;
+    a.lk = lk;
     a.idx_out = (keep_idx && t > 1) ? e->idx.p : nullptr;
     a.feed_z = row(fz, t);
     a.feed_gs = row(fgs, t);
     a.feed_gt = row(fgt, t);
     a.feed_w = row(fw, t);
-    a.qx = want_fq ? e->qx.p : nullptr;
-    a.qs = want_sq ? e->qs.p : nullptr;
-    a.qt = want_tq ? e->qt.p : nullptr;
+    a.kx = want_fq ? kbase : nullptr;
+    a.ks = want_sq ? kbase + n : nullptr;
+    a.kt = want_tq ? kbase + 2 * (size_t)n : nullptr;
+    a.qmom = ntg ? &qshp->mean[0] : nullptr;
     a.partials = e->partials.p;
     a.sc = e->sc.p;
     a.out.fmean = e->o_fm.p;
@@ -491,11 +639,11 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       cudaEventCreate(&b0);
       cudaEventCreate(&b1);
       cudaEventRecord(b0, st);
-      step_kernel<MODE, TQ><<<step_grid, 256, 0, st>>>(a);
+      step_kernel<MODE, TQ><<<step_grid, 256, step_smem, st>>>(a);
       cudaEventRecord(b1, st);
       step_evs.push_back({b0, b1});
     } else {
-      step_kernel<MODE, TQ><<<step_grid, 256, 0, st>>>(a);
+      step_kernel<MODE, TQ><<<step_grid, 256, step_smem, st>>>(a);
     }
     LAUNCHED();
     ++step_launches;
@@ -505,23 +653,71 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       CK(cudaMemcpyAsync(out->indices + (size_t)(t - 2) * n, e->idx.p, n * sizeof(int64_t),
                          cudaMemcpyDeviceToHost, st));
 
-    // ---- K5 summaries: weighted quantiles from the pre-resample set
-    if (want_fq)
-      if ((rc = weighted_quantiles_dev<TQ>(e->qsc, e->qx.p, wsrc, n, e->probs.p + 5, 3,
-                                           e->o_fq.p + (t - 1) * 3, st, e->fail.p)) != PF_OK)
-        return rc;
-    if (want_sq)
-      if ((rc = weighted_quantiles_dev<TQ>(e->qsc, e->qs.p, wsrc, n, e->probs.p, 5,
-                                           e->o_sq.p + (t - 1) * 5, st, e->fail.p)) != PF_OK)
-        return rc;
-    if (want_tq)
-      if ((rc = weighted_quantiles_dev<TQ>(e->qsc, e->qt.p, wsrc, n, e->probs.p, 5,
-                                           e->o_tq.p + (t - 1) * 5, st, e->fail.p)) != PF_OK)
-        return rc;
-    mark(PH_OTHER);
-
-    // ---- K2-K4 CDF + cut table
-    if ((rc = launch_cdf<TQ>(e->cdf, wsrc, n, qv, e->cut.p, e->fail.p, t, st)) != PF_OK) return rc;
+    // ---- K2-K4 CDF + cut table; K5 weighted quantiles ride on K2
+    if (ntg) {
+      qa.sh = qshp;
+      qa.keys[0] = want_fq ? kbase : nullptr;
+      qa.keys[1] = want_sq ? kbase + n : nullptr;
+      qa.keys[2] = want_tq ? kbase + 2 * (size_t)n : nullptr;
+      // previous step's resolve updated the window predictor
+      CK(cudaStreamWaitEvent(st, e->ev_e, 0));
+      if (plan.small) {
+        q_window_kernel<TQ><<<grid_for(n, 256), 256, 0, st>>>(wsrc, n, e->fail.p, qa);
+        LAUNCHED();
+        if ((rc = launch_cdf<TQ>(e->cdf, wsrc, n, qv, e->cut.p, e->fail.p, t, st, so)) != PF_OK) return rc;
+      } else {
+        CdfBufs& b = e->cdf;
+        cdf_reduce_q_kernel<TQ><<<(int)plan.chunks, CDF_THREADS, 0, st>>>(
+            wsrc, plan.R, (TQ*)b.tile_tot.p, (TQ*)b.chunk_tot.p, e->fail.p, qa);
+        LAUNCHED();
+        if ((rc = launch_cdf_tail<TQ>(e->cdf, wsrc, n, qv, e->cut.p, e->fail.p, t, st, so)) != PF_OK) return rc;
+      }
+      CK(cudaEventRecord(e->ev_b, st));
+      // side stream: resolve (overlaps the next step's propagation)
+      cudaStream_t ss = e->side;
+      CK(cudaStreamWaitEvent(ss, e->ev_b, 0));
+      QValueSrc vs;
+      vs.rec = e->rec[cur].p;
+      vs.seed = c.seed;
+      vs.t = t;
+      vs.gs = gamma_src(e, true, t);
+      vs.feed_gs = row(fgs, t);
+      vs.sigma2_fixed = c.sigma2_fixed;
+      vs.tau2_fixed = c.tau2_fixed;
+      vs.learn_s = LS;
+      vs.learn_t = LT;
+      double *ox = e->o_fq.p, *os = e->o_sq.p, *ot = e->o_tq.p;
+      const int hgrid = std::max(1, std::min(64, (int)((n / 64 + 255) / 256)));
+      static bool resolve_attr = false;
+      if (!resolve_attr) {
+        CK(cudaFuncSetAttribute(q_resolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                Q_RESOLVE_SMEM));
+        resolve_attr = true;
+      }
+      for (int round = 0; round < 2; ++round) {
+        q_hist_kernel<<<dim3(hgrid, ntg), 256, 0, ss>>>(qa, e->fail.p, round);
+        q_resolve_kernel<<<ntg, 1024, Q_RESOLVE_SMEM, ss>>>(qa, vs, ox, os, ot, t, e->fail.p, round);
+        if (round == 0) {
+          // misses: bounded re-window (attempt 0), whole side (attempt 1)
+          for (int attempt = 0; attempt < 2; ++attempt) {
+            q_fallback_prep_kernel<<<1, 32, 0, ss>>>(qa, attempt, e->fail.p);
+            q_fallback_hist_kernel<<<fb_grid, 256, 0, ss>>>(qa, lwp, wsrc.mode, wsrc.M, n, SINGLE, attempt,
+                                                            e->fail.p);
+            q_fallback_select_kernel<<<ntg, 1024, 0, ss>>>(qa, attempt, e->fail.p);
+            g_launches.fetch_add(3);
+          }
+          q_fallback_fill_kernel<<<fb_grid, 256, 0, ss>>>(qa, lwp, wsrc.mode, wsrc.M, n, SINGLE, e->fail.p);
+          g_launches.fetch_add(1);
+        }
+        g_launches.fetch_add(2);
+      }
+      q_select_kernel<<<ntg, 1024, 0, ss>>>(qa, vs, e->qscratch.p, ox, os, ot, t, e->fail.p, e->qunres.p);
+      q_step_end_kernel<<<1, 1024, 0, ss>>>(qa, 1);
+      g_launches.fetch_add(2);
+      CK(cudaEventRecord(e->ev_e, ss));
+    } else {
+      if ((rc = launch_cdf<TQ>(e->cdf, wsrc, n, qv, e->cut.p, e->fail.p, t, st, so)) != PF_OK) return rc;
+    }
     mark(PH_CDF);
 
     // ---- store: post-resample snapshot of step t
@@ -533,8 +729,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       m.resample = 1;
       m.rec = e->rec[cur].p;
       m.u3 = e->u3.p;
-      m.q = qv;
-      m.cut = e->cut.p;
+      m.lk = lk;
       m.s2_direct = nullptr;
       m.gs = gamma_src(e, true, t);
       m.feed_gs = row(fgs, t);
@@ -571,8 +766,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     m.resample = 1;
     m.rec = e->rec[cur].p;
     m.u3 = e->u3.p;
-    m.q = qv;
-    m.cut = e->cut.p;
+    m.lk = lk;
     m.s2_direct = nullptr;
     m.gs = gamma_src(e, true, T);
     m.feed_gs = row(fgs, T);
@@ -638,7 +832,8 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     mark(PH_OTHER);
   }
 
-  // ---- outputs to host
+  // ---- join the quantile side stream, then outputs to host
+  if (ntg) CK(cudaStreamWaitEvent(st, e->ev_e, 0));
   if (out && T > 0) {
     auto cp = [&](double* h, DevBuf<double>& d, size_t cnt) -> int {
       if (h) CK(cudaMemcpyAsync(h, d.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -663,6 +858,12 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   CK(cudaEventRecord(e->ev1, st));
   CK(cudaStreamSynchronize(st));
   CK(cudaGetLastError());
+  for (int k = 0; k < 4; ++k) e->qstats[k] = 0;
+  if (ntg) {
+    unsigned int h[4];
+    CK(cudaMemcpy(h, e->qunres.p, sizeof(h), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < 4; ++k) e->qstats[k] = h[k];
+  }
   float ms = 0;
   cudaEventElapsedTime(&ms, e->ev0, e->ev1);
   e->last_total_ms = ms;
@@ -757,12 +958,24 @@ int pf_engine_create(const pf_config* cfg, pf_engine** out) {
   };
   cudaError_t err;
   if ((err = cudaStreamCreateWithFlags(&e->st, cudaStreamNonBlocking))) return bail(err);
-  if ((err = e->rec[0].ensure(n)) || (err = e->rec[1].ensure(n)) || (err = e->lw.ensure(n)) ||
-      (err = e->u3.ensure(n)) || (err = e->q.ensure(n * (e->single ? 4 : 8))) ||
-      (err = e->cut.ensure(n)) || (err = e->partials.ensure(sm_count() * 8 + 8)) ||
+  // The step kernel's reads are random 32-byte records; do not let L2
+  // promote each miss into a 64/128-byte DRAM fetch.
+  cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32);
+  if ((err = cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking))) return bail(err);
+  if ((err = cudaEventCreateWithFlags(&e->ev_b, cudaEventDisableTiming)) ||
+      (err = cudaEventCreateWithFlags(&e->ev_e, cudaEventDisableTiming)) || (err = e->mbuf.ensure(2)))
+    return bail(err);
+  if ((err = e->rec[0].ensure(n)) || (err = e->rec[1].ensure(n)) || (err = e->lw.ensure(2 * n)) ||
+      (err = e->u3.ensure(n)) || (err = e->partials.ensure(sm_count() * 8 + 8)) ||
       (err = e->sc.ensure(1)) || (err = e->fail.ensure(1)) ||
       (err = e->cdf.ensure(n, e->single ? 4 : 8)) || (err = e->probs.ensure(8)))
     return bail(err);
+  e->strata = ilog2(n) >= STRATA_MIN_LOG2N;
+  if (e->strata) {
+    if ((err = e->srec.ensure(n)) || (err = e->pfr.ensure(n))) return bail(err);
+  } else {
+    if ((err = e->q.ensure(n * (e->single ? 4 : 8))) || (err = e->cut.ensure(n))) return bail(err);
+  }
   const double probs[8] = {0.005, 0.05, 0.5, 0.95, 0.995, 0.05, 0.5, 0.95};
   if ((err = cudaMemcpy(e->probs.p, probs, sizeof(probs), cudaMemcpyHostToDevice))) return bail(err);
   if ((err = cudaEventCreate(&e->ev0)) || (err = cudaEventCreate(&e->ev1))) return bail(err);
@@ -802,6 +1015,12 @@ int pf_engine_run_resident(pf_engine* e, int64_t t_len) {
   return rc;
 }
 
+int pf_engine_quantile_stats(pf_engine* e, int64_t* stats4) {
+  if (!e || !stats4) return set_err(PF_ERR_VALUE, "null argument");
+  for (int k = 0; k < 4; ++k) stats4[k] = e->qstats[k];
+  return PF_OK;
+}
+
 int pf_engine_last_timing(pf_engine* e, double* total_ms, double* step_kernel_ms,
                           int64_t* step_kernel_launches, int64_t* kernels_launched) {
   if (!e) return set_err(PF_ERR_VALUE, "null engine");
@@ -816,9 +1035,8 @@ int pf_engine_destroy(pf_engine* e) {
   if (!e) return PF_OK;
   cudaSetDevice(e->cfg.device);
   if (e->st) cudaStreamSynchronize(e->st);
-  DevBuf<double>* bufs[] = {&e->lw, &e->qx, &e->qs, &e->qt, &e->s2init, &e->o_fm, &e->o_sm, &e->o_ssd,
-                            &e->o_tm, &e->o_tsd, &e->o_fq, &e->o_sq, &e->o_tq, &e->probs, &e->tab_s,
-                            &e->tab_t, &e->shapes_buf, &e->m_x, &e->m_s2, &e->m_t2, &e->m_as,
+  DevBuf<double>* bufs[] = {&e->lw, &e->s2init, &e->o_fm, &e->o_sm, &e->o_ssd,
+                            &e->o_tm, &e->o_tsd, &e->o_fq, &e->o_sq, &e->o_tq, &e->probs, &e->m_x, &e->m_s2, &e->m_t2, &e->m_as,
                             &e->m_bs, &e->m_at, &e->m_bt, &e->feed_buf};
   for (auto* b : bufs) b->release();
   e->rec[0].release();
@@ -826,6 +1044,8 @@ int pf_engine_destroy(pf_engine* e) {
   e->u3.release();
   e->q.release();
   e->cut.release();
+  e->srec.release();
+  e->pfr.release();
   e->idx.release();
   e->partials.release();
   e->sc.release();
@@ -835,12 +1055,20 @@ int pf_engine_destroy(pf_engine* e) {
   e->cdf.node.release();
   e->cdf.carry.release();
   e->cdf.total.release();
-  e->qsc.kin.release();
-  e->qsc.kout.release();
-  e->qsc.iin.release();
-  e->qsc.iout.release();
-  e->qsc.ws.release();
-  e->qsc.tmp.release();
+  e->keys.release();
+  e->qtg.release();
+  e->qsh.release();
+  e->qcand.release();
+  e->qpart.release();
+  e->qscratch.release();
+  e->mbuf.release();
+  e->qhist.release();
+  e->qfhist.release();
+  e->qunres.release();
+  if (e->side) cudaStreamSynchronize(e->side);
+  if (e->side) cudaStreamDestroy(e->side);
+  if (e->ev_b) cudaEventDestroy(e->ev_b);
+  if (e->ev_e) cudaEventDestroy(e->ev_e);
   for (auto ev : e->evs) cudaEventDestroy(ev);
   if (e->ev0) cudaEventDestroy(e->ev0);
   if (e->ev1) cudaEventDestroy(e->ev1);

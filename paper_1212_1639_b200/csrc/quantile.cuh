@@ -1,0 +1,768 @@
+// Exact weighted quantiles of the per-step particle summaries
+// (filtering.py:135-155: smallest value, in stable value order, whose
+// cumulative weight reaches p * W), without sorting N values per step.
+//
+//  1. The step kernel writes a 32-bit monotone key per particle and quantity
+//     (float32 rounded down, order-preserving bit image) and the step's
+//     weighted mean / sd of each quantity.
+//  2. The CDF reduce pass (which already forms the exact weight w) predicts a
+//     narrow key window per target -- mean_t + sd_t * (standardized quantile
+//     of step t-1) +- h -- and, per particle, adds w to "weight below the
+//     window" or appends (key, index, w) to the target's candidate list.
+//  3. On a side stream, per target: a fixed-point (exact, order-independent)
+//     sub-bin histogram of the candidates locates the sub-bin holding the
+//     crossing; the candidates of that sub-bin and its neighbours are ordered
+//     by their exact value (recomputed from the particle record) and index
+//     (argsort(kind="stable")), and summed in that order from the exact
+//     weight below them.  The window half-width h adapts to the observed
+//     prediction error.
+//  4. If the crossing is not inside the window (or the window overflowed),
+//     conditional fallback kernels histogram the missed interval over all
+//     particles, re-window to one bin and resolve again.  They exit at once
+//     when nothing missed.
+// The weight sums differ from numpy's sequential cumsum only in rounding, so
+// a quantile can move by one order statistic only at an exact near-tie.
+#pragma once
+#include "step.cuh"
+
+namespace pf {
+
+constexpr int Q_MAXQ = 3;        // quantities: 0 = x, 1 = sigma2, 2 = tau2
+constexpr int Q_MAXT = 13;       // targets: 3 state + 5 + 5 parameter probs
+constexpr int Q_SUB = 2048;      // sub-bins per window
+constexpr int Q_FB = 4096;       // fallback bins per missed interval
+constexpr int Q_LIST = 4096;     // exact-resolve list capacity (per target)
+constexpr int Q_RESOLVE_SMEM = (Q_SUB + 1) * 8 + Q_LIST * (8 + 8 + 4);
+
+enum : uint32_t { QS_OK = 0, QS_MISS_LO = 1, QS_MISS_HI = 2, QS_OVERFLOW = 3, QS_CROWD = 4,
+                  QS_REFILL = 5, QS_FB = 6, QS_RETRY = 7 };
+
+PF_HD uint32_t key_of_float(float f) {
+  union { float f; uint32_t u; } c;
+  c.f = f;
+  return (c.u & 0x80000000u) ? ~c.u : (c.u | 0x80000000u);
+}
+PF_D uint32_t key_rd(double v) { return key_of_float(__double2float_rd(v)); }
+PF_D uint32_t key_ru(double v) { return key_of_float(__double2float_ru(v)); }
+
+struct QCand {
+  uint32_t key;
+  uint32_t idx;
+  double w;
+};
+
+// Persistent (across steps) per-target state + per-step scratch.
+struct QTarget {
+  double p;          // probability
+  int q;             // quantity
+  int col;           // output column
+  double zprev;      // standardized quantile of the previous step
+  double h;          // window half-width (standardized units)
+  double ema;        // running prediction error
+  // per step
+  uint32_t klo, khi; // key window (inclusive)
+  double wbelow;     // weight with key < klo
+  uint32_t count;    // candidates appended
+  uint32_t status;
+  uint32_t ilo, ihi; // fallback interval
+  double ibelow;     // weight below the fallback interval
+  uint32_t missed;   // the predicted window missed this step
+  double wmass;      // candidate weight inside the window
+  int side;          // fallback retry side (-1 below, +1 above)
+};
+
+PF_HD double normal_pdf(double z) { return 0.3989422804014327 * exp(-0.5 * z * z); }
+
+struct QShared {
+  double W;                    // total weight of the step (fp64 sum of w)
+  double mean[Q_MAXQ], sd[Q_MAXQ];
+  unsigned int counter;        // last-CTA ticket of the reduce pass
+  unsigned int fb_counter;
+  int any_miss;
+  int fb_active[2];
+  int ntarget;
+};
+
+struct QArgs {
+  int ntarget;                 // 0 = quantiles off
+  QTarget* tg;
+  QShared* sh;
+  const uint32_t* keys[Q_MAXQ];  // this step's keys (null if quantity absent)
+  QCand* cand;                 // [ntarget][cap]
+  uint32_t cap;
+  double* part;                // reduce-pass partials [grid][Q_MAXT+1]
+  unsigned long long* hist;    // [ntarget][Q_SUB] fixed-point weights
+  unsigned long long* fhist;   // [ntarget][Q_FB]
+  double fx_scale;             // fixed-point units per unit weight
+  unsigned int* stats;         // [0] unresolved, [1] fallbacks, [2] max candidates, [3] resolves
+};
+
+// Window of target k for this step from mean/sd of its quantity.
+PF_D void window_of(const QTarget& t, double mean, double sd, uint32_t* lo, uint32_t* hi) {
+  if (!(sd > 0.0) || !isfinite(sd) || !isfinite(mean)) {
+    *lo = 0u;
+    *hi = 0xFFFFFFFFu;
+    return;
+  }
+  const double c = mean + sd * t.zprev;
+  *lo = key_rd(c - t.h * sd);
+  *hi = key_ru(c + t.h * sd);
+}
+
+PF_D uint32_t sub_bin(uint32_t key, uint32_t lo, uint32_t hi, int nb) {
+  const uint64_t span = (uint64_t)(hi - lo) + 1;
+  return (uint32_t)(((uint64_t)(key - lo) * (uint64_t)nb) / span);
+}
+
+// Exact value of quantity q for particle idx at step t (resolve side).
+struct QValueSrc {
+  const Rec* rec;        // records written by step t
+  uint64_t seed;
+  int64_t t;
+  GammaSrc gs;           // step t's sigma2 table
+  const double* feed_gs; // oracle feed row t
+  double sigma2_fixed, tau2_fixed;
+  int learn_s, learn_t;
+};
+
+PF_D double quantity_value(const QValueSrc& s, int q, uint32_t idx) {
+  const Rec r = s.rec[idx];
+  if (q == 0) return r.x;
+  if (q == 2) return s.learn_t ? r.tau2 : s.tau2_fixed;
+  if (!s.learn_s) return s.sigma2_fixed;
+  double g;
+  if (s.feed_gs) {
+    g = s.feed_gs[idx];
+  } else {
+    const Philox4 P = philox_block(s.seed, (uint64_t)idx, (uint64_t)s.t);
+    g = gamma_draw(s.gs, unit_open(P.w[1]));
+  }
+  return r.bs / g;
+}
+
+// --------------------------------------------- classify (in CDF reduce) ---
+// Called by cdf_reduce for every element; accumulates below-window weight
+// into acc[k] and appends window candidates (warp-aggregated).
+struct QWin {
+  uint32_t lo[Q_MAXT], hi[Q_MAXT];
+  int q[Q_MAXT];
+  int n;
+};
+
+PF_D void q_classify(const QArgs& qa, const QWin& win, uint32_t i, double w, double (&acc)[Q_MAXT],
+                     bool valid) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t k0 = (valid && qa.keys[0]) ? qa.keys[0][i] : 0u;
+  const uint32_t k1 = (valid && qa.keys[1]) ? qa.keys[1][i] : 0u;
+  const uint32_t k2 = (valid && qa.keys[2]) ? qa.keys[2][i] : 0u;
+  uint32_t inwin = 0;
+#pragma unroll
+  for (int k = 0; k < Q_MAXT; ++k) {  // unrolled: acc[] stays in registers
+    if (k < win.n) {
+      const int q = win.q[k];
+      const uint32_t key = q == 0 ? k0 : (q == 1 ? k1 : k2);
+      if (valid && key < win.lo[k]) acc[k] += w;
+      else if (valid && key <= win.hi[k]) inwin |= 1u << k;
+    }
+  }
+  uint32_t any = __reduce_or_sync(0xffffffffu, inwin);
+  while (any) {
+    const int k = __ffs(any) - 1;
+    any &= any - 1;
+    const unsigned m = __ballot_sync(0xffffffffu, (inwin >> k) & 1u);
+    uint32_t base = 0;
+    const int leader = __ffs(m) - 1;
+    if (lane == leader) base = atomicAdd(&qa.tg[k].count, (uint32_t)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if ((inwin >> k) & 1u) {
+      const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
+      if (pos < qa.cap) {
+        QCand c;
+        c.key = win.q[k] == 0 ? k0 : (win.q[k] == 1 ? k1 : k2);
+        c.idx = i;
+        c.w = w;
+        qa.cand[(size_t)k * qa.cap + pos] = c;
+      }
+    }
+  }
+}
+
+// Block-reduce the below-window sums and W, combine CTAs in fixed order.
+PF_D void q_reduce_partials(const QArgs& qa, const QWin& win, double (&acc)[Q_MAXT], double wsum) {
+  __shared__ double red[8][Q_MAXT + 1];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nv = win.n + 1;
+#pragma unroll
+  for (int k = 0; k <= Q_MAXT; ++k) {  // unrolled: static indices keep acc[] in registers
+    if (k < nv) {
+      double v = k < win.n ? acc[k < Q_MAXT ? k : 0] : wsum;
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red[warp][k] = v;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < nv) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w][threadIdx.x];
+    qa.part[(size_t)blockIdx.x * (Q_MAXT + 1) + threadIdx.x] = s;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&qa.sh->counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < nv) {
+    double s = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(&qa.part[(size_t)b * (Q_MAXT + 1) + threadIdx.x]);
+    if (threadIdx.x < win.n) {
+      qa.tg[threadIdx.x].wbelow = s;
+      qa.tg[threadIdx.x].klo = win.lo[threadIdx.x];
+      qa.tg[threadIdx.x].khi = win.hi[threadIdx.x];
+    } else {
+      qa.sh->W = s;
+    }
+  }
+  if (threadIdx.x == 0) qa.sh->counter = 0;
+}
+
+// Windows of this step (identical in every CTA: same inputs, same code).
+PF_D void q_make_windows(const QArgs& qa, QWin& win) {
+  if (threadIdx.x == 0) {
+    win.n = qa.ntarget;
+    for (int k = 0; k < qa.ntarget; ++k) {
+      const QTarget& t = qa.tg[k];
+      win.q[k] = t.q;
+      window_of(t, qa.sh->mean[t.q], qa.sh->sd[t.q], &win.lo[k], &win.hi[k]);
+    }
+  }
+  __syncthreads();
+}
+
+// K2 with the quantile window pass fused in: the tile's exact subtree sum
+// (as cdf_reduce_kernel) plus, for every element, the below-window weight /
+// candidate classification against this step's windows.
+template <typename T>
+__global__ void __launch_bounds__(CDF_THREADS)
+cdf_reduce_q_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ chunk_tot,
+                    const int64_t* __restrict__ fail, QArgs qa) {
+  if (fail && *fail) return;
+  __shared__ T wt[CDF_THREADS / 32];
+  __shared__ T tt[64];
+  __shared__ QWin win;
+  q_make_windows(qa, win);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double M = src.mode == 0 ? *src.M : 0.0;
+  const int64_t chunk = blockIdx.x;
+  double acc[Q_MAXT];
+#pragma unroll
+  for (int k = 0; k < Q_MAXT; ++k) acc[k] = 0.0;
+  double wsum = 0.0;
+  for (int r = 0; r < R; ++r) {
+    const int64_t tile = chunk * R + r;
+    const int64_t base = tile * CDF_TILE + threadIdx.x * CDF_V;
+    T v[CDF_V], l1[4], l2[2], g;
+    load_tile_weights<T>(src, base, M, v);
+#pragma unroll
+    for (int e = 0; e < CDF_V; ++e) {
+      const double w = (double)v[e];
+      wsum += w;
+      q_classify(qa, win, (uint32_t)(base + e), w, acc, true);
+    }
+    thread_tree8<T>(v, l1, l2, g);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) g = g + __shfl_xor_sync(0xffffffffu, g, o);
+    if (lane == 0) wt[warp] = g;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      T a0 = wt[0] + wt[1], a1 = wt[2] + wt[3], a2 = wt[4] + wt[5], a3 = wt[6] + wt[7];
+      T tot = (a0 + a1) + (a2 + a3);
+      tt[r] = tot;
+      tile_tot[tile] = tot;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    for (int len = R; len > 1; len >>= 1)
+      for (int i = 0; i < len / 2; ++i) tt[i] = tt[2 * i] + tt[2 * i + 1];
+    chunk_tot[chunk] = tt[0];
+  }
+  q_reduce_partials(qa, win, acc, wsum);
+}
+
+// Window pass on its own (n below one CDF tile, where K2 is not used).
+template <typename T>
+__global__ void __launch_bounds__(256)
+q_window_kernel(WSrc src, int64_t n, const int64_t* __restrict__ fail, QArgs qa) {
+  if (fail && *fail) return;
+  __shared__ QWin win;
+  q_make_windows(qa, win);
+  const double M = src.mode == 0 ? *src.M : 0.0;
+  double acc[Q_MAXT];
+#pragma unroll
+  for (int k = 0; k < Q_MAXT; ++k) acc[k] = 0.0;
+  double wsum = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t iters = (n + stride - 1) / stride;
+  for (int64_t it = 0; it < iters; ++it) {  // uniform trip count: warp-collective classify
+    const int64_t i = it * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool valid = i < n;
+    const double w = valid ? (double)weight_of<T>(src.src[i], M, src.mode) : 0.0;
+    wsum += w;
+    q_classify(qa, win, (uint32_t)(valid ? i : 0), w, acc, valid);
+  }
+  q_reduce_partials(qa, win, acc, wsum);
+}
+
+// ------------------------------------------------------- resolve (side) ---
+// Exclusive scan, in place, of n (a multiple of blockDim.x) values in shared
+// memory; returns the total.  Integer addition: exact in any order.
+PF_D unsigned long long block_exclusive_scan(unsigned long long* a, int n) {
+  __shared__ unsigned long long ws[32];
+  __shared__ unsigned long long total;
+  const int per = n / blockDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  unsigned long long loc = 0;
+  for (int i = 0; i < per; ++i) loc += a[threadIdx.x * per + i];
+  unsigned long long inc = loc;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) ws[warp] = inc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long s = 0;
+    for (int w = 0; w < nw; ++w) {
+      const unsigned long long t = ws[w];
+      ws[w] = s;
+      s += t;
+    }
+    total = s;
+  }
+  __syncthreads();
+  unsigned long long run = ws[warp] + inc - loc;
+  for (int i = 0; i < per; ++i) {
+    const unsigned long long t = a[threadIdx.x * per + i];
+    a[threadIdx.x * per + i] = run;
+    run += t;
+  }
+  __syncthreads();
+  return total;
+}
+
+// R1: fixed-point sub-bin histogram of every target's candidates.
+__global__ void __launch_bounds__(256) q_hist_kernel(QArgs qa, const int64_t* fail, int fallback_round) {
+  if (*fail) return;
+  const int k = blockIdx.y;
+  if (k >= qa.ntarget) return;
+  QTarget& t = qa.tg[k];
+  if (fallback_round && t.status != QS_REFILL) return;
+  const uint32_t n = min(t.count, qa.cap);
+  const uint32_t lo = t.klo, hi = t.khi;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const QCand c = qa.cand[(size_t)k * qa.cap + i];
+    const uint32_t b = sub_bin(c.key, lo, hi, Q_SUB);
+    atomicAdd(&qa.hist[(size_t)k * Q_SUB + b], (unsigned long long)llrint(c.w * qa.fx_scale));
+  }
+}
+
+// Bitonic sort of (value, idx, w) triples in shared memory, ascending by
+// (value, idx) -- the order of np.argsort(values, kind="stable").
+PF_D void bitonic_sort(double* v, uint32_t* id, double* w, int n2) {
+  for (int k = 2; k <= n2; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          const bool gt = (v[i] > v[l]) || (v[i] == v[l] && id[i] > id[l]);
+          if (gt == up) {
+            double tv = v[i]; v[i] = v[l]; v[l] = tv;
+            uint32_t ti = id[i]; id[i] = id[l]; id[l] = ti;
+            double tw = w[i]; w[i] = w[l]; w[l] = tw;
+          }
+        }
+      }
+      __syncthreads();
+    }
+}
+
+// R2: one CTA per target.  Locate the crossing sub-bin, order its candidates
+// exactly, write the quantile, update the predictor.  Misses set status.
+__global__ void __launch_bounds__(1024)
+q_resolve_kernel(QArgs qa, QValueSrc vs, double* out_x, double* out_s, double* out_t, int64_t t_step,
+                 const int64_t* fail, int fallback_round) {
+  if (*fail) return;
+  const int k = blockIdx.x;
+  QTarget& tg = qa.tg[k];
+  if (fallback_round && tg.status != QS_REFILL) return;
+  // dynamic smem: pre[Q_SUB+1] u64 | sv[Q_LIST] f64 | sw[Q_LIST] f64 | sid[Q_LIST] u32
+  extern __shared__ unsigned long long qsm[];
+  unsigned long long* pre = qsm;
+  double* sv = reinterpret_cast<double*>(qsm + Q_SUB + 1);
+  double* sw = sv + Q_LIST;
+  uint32_t* sid = reinterpret_cast<uint32_t*>(sw + Q_LIST);
+  __shared__ int bstar, nlist;
+  __shared__ uint32_t status;
+  const double W = qa.sh->W;
+  const double T = tg.p * W;
+  const double wb = tg.wbelow;
+  const unsigned long long* H = qa.hist + (size_t)k * Q_SUB;
+  for (int b = threadIdx.x; b < Q_SUB; b += blockDim.x) pre[b] = H[b];
+  __syncthreads();
+  const unsigned long long tot = block_exclusive_scan(pre, Q_SUB);
+  if (threadIdx.x == 0) {
+    atomicMax(&qa.stats[2], tg.count);
+    atomicAdd(&qa.stats[3], 1u);
+    pre[Q_SUB] = tot;
+    status = QS_OK;
+    if (tg.count > qa.cap) status = QS_OVERFLOW;
+    else if (!(T > wb)) status = QS_MISS_LO;
+    else if (T > wb + (double)tot / qa.fx_scale) status = QS_MISS_HI;
+    bstar = Q_SUB - 1;
+    nlist = 0;
+  }
+  __syncthreads();
+  // first sub-bin whose inclusive cumulative weight reaches T
+  for (int j = threadIdx.x; j < Q_SUB; j += blockDim.x)
+    if (wb + (double)pre[j + 1] / qa.fx_scale >= T && !(wb + (double)pre[j] / qa.fx_scale >= T))
+      atomicMin(&bstar, j);
+  __syncthreads();
+  if (status != QS_OK) {
+    if (threadIdx.x == 0) {
+      tg.status = status;
+      tg.wmass = (double)tot / qa.fx_scale;
+      qa.sh->any_miss = 1;
+    }
+    return;
+  }
+  const int b0 = max(bstar - 1, 0), b1 = min(bstar + 1, Q_SUB - 1);
+  const uint32_t n = tg.count;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const QCand c = qa.cand[(size_t)k * qa.cap + i];
+    const int b = (int)sub_bin(c.key, tg.klo, tg.khi, Q_SUB);
+    if (b >= b0 && b <= b1) {
+      const int pos = atomicAdd(&nlist, 1);
+      if (pos < Q_LIST) {
+        sid[pos] = c.idx;
+        sw[pos] = c.w;
+      }
+    }
+  }
+  __syncthreads();
+  const int m = nlist;
+  if (m > Q_LIST) {
+    if (threadIdx.x == 0) {
+      tg.status = QS_CROWD;
+      qa.sh->any_miss = 1;
+    }
+    return;
+  }
+  int n2 = 1;
+  while (n2 < m) n2 <<= 1;
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+    if (i < m) sv[i] = quantity_value(vs, tg.q, sid[i]);
+    else { sv[i] = INFINITY; sid[i] = 0xFFFFFFFFu; sw[i] = 0.0; }
+  }
+  __syncthreads();
+  bitonic_sort(sv, sid, sw, n2);
+  if (threadIdx.x == 0) {
+    double cum = wb + (double)pre[b0] / qa.fx_scale;
+    double val = m > 0 ? sv[m - 1] : NAN;
+    for (int i = 0; i < m; ++i) {
+      cum += sw[i];
+      if (cum >= T) { val = sv[i]; break; }
+    }
+    double* o = tg.q == 0 ? out_x : (tg.q == 1 ? out_s : out_t);
+    const int ncol = tg.q == 0 ? 3 : 5;
+    o[(t_step - 1) * ncol + tg.col] = val;
+    // predictor update: standardized position; the half-width is sized in
+    // probability mass (the step-to-step drift of a quantile is ~0.1-0.4%
+    // of mass whether it sits in the bulk or a tail), converted to
+    // standardized units through a normal-density proxy.
+    const double mean = qa.sh->mean[tg.q], sd = qa.sh->sd[tg.q];
+    if (sd > 0.0 && isfinite(val)) {
+      const double z = (val - mean) / sd;
+      const double phi = fmax(normal_pdf(z), 1e-4);
+      const double em = fabs(z - tg.zprev) * phi;
+      tg.ema = 0.7 * tg.ema + 0.3 * em;
+      const double mass = fmin(0.03, fmax(1e-3, 4.0 * fmax(em, tg.ema)));
+      tg.h = fmin(2.0, mass / phi);
+      tg.zprev = z;
+    }
+    if (fallback_round == 0) tg.wmass = (double)tot / qa.fx_scale;
+    tg.status = QS_OK;
+  }
+}
+
+// F0: interval for each target that missed.  Attempt 0 uses a secant
+// estimate from the missing mass, bounded so the histogram pass touches few
+// particles; attempt 1 (only if attempt 0's interval did not hold the
+// crossing either) takes everything on the missing side.
+__global__ void q_fallback_prep_kernel(QArgs qa, int attempt, const int64_t* fail) {
+  if (*fail || !qa.sh->any_miss) return;
+  const int k = threadIdx.x;
+  if (k >= qa.ntarget) return;
+  QTarget& t = qa.tg[k];
+  const uint32_t st = t.status;
+  const double W = qa.sh->W, T = t.p * W;
+  const double mean = qa.sh->mean[t.q], sd = qa.sh->sd[t.q];
+  uint32_t lo, hi;
+  if (attempt == 0 && (st == QS_MISS_LO || st == QS_MISS_HI || st == QS_OVERFLOW || st == QS_CROWD)) {
+    const bool ok_sd = sd > 0.0 && isfinite(sd) && isfinite(mean);
+    if (st == QS_MISS_LO) {
+      lo = 0;
+      hi = t.klo ? t.klo - 1 : 0;
+      if (ok_sd) {
+        const double zc = t.zprev - t.h;
+        const double dm = fmax(t.wbelow - T, 0.0) / W;
+        const double dz = 3.0 * dm / fmax(normal_pdf(zc), 1e-3) + 0.05;
+        const uint32_t l = key_rd(mean + sd * (zc - dz));
+        if (l <= hi) lo = l;
+      }
+    } else if (st == QS_MISS_HI) {
+      lo = t.khi == 0xFFFFFFFFu ? t.khi : t.khi + 1;
+      hi = 0xFFFFFFFFu;
+      if (ok_sd) {
+        const double zc = t.zprev + t.h;
+        const double dm = fmax(T - t.wbelow - t.wmass, 0.0) / W;
+        const double dz = 3.0 * dm / fmax(normal_pdf(zc), 1e-3) + 0.05;
+        const uint32_t h2 = key_ru(mean + sd * (zc + dz));
+        if (h2 >= lo) hi = h2;
+      }
+    } else {
+      lo = t.klo;
+      hi = t.khi;
+    }
+  } else if (attempt == 1 && st == QS_RETRY) {
+    if (t.side < 0) { lo = 0; hi = t.ilo ? t.ilo - 1 : 0; }
+    else { lo = t.ihi == 0xFFFFFFFFu ? t.ihi : t.ihi + 1; hi = 0xFFFFFFFFu; }
+  } else {
+    return;
+  }
+  t.ilo = lo;
+  t.ihi = hi;
+  t.status = QS_FB;
+  t.missed = 1;
+  qa.sh->fb_active[attempt] = 1;
+}
+
+// F1: full pass over the particles for targets in fallback: fixed-point
+// histogram of the interval + fp64 weight below it.
+__global__ void __launch_bounds__(256)
+q_fallback_hist_kernel(QArgs qa, const double* __restrict__ lw, int wmode, const double* Mp, int64_t n,
+                       int single, int attempt, const int64_t* fail) {
+  if (*fail || !qa.sh->fb_active[attempt]) return;
+  __shared__ uint32_t ilo[Q_MAXT], ihi[Q_MAXT];
+  __shared__ int act[Q_MAXT];
+  __shared__ bool last;
+  if (threadIdx.x < qa.ntarget) {
+    const QTarget& t = qa.tg[threadIdx.x];
+    act[threadIdx.x] = t.status == QS_FB;
+    ilo[threadIdx.x] = t.ilo;
+    ihi[threadIdx.x] = t.ihi;
+  }
+  __syncthreads();
+  const double M = wmode == 0 ? *Mp : 0.0;
+  double acc[Q_MAXT];
+  for (int k = 0; k < Q_MAXT; ++k) acc[k] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double w = wmode == 0 ? exp(lw[i] - M) : lw[i];
+    if (single) w = (double)(float)w;
+    for (int k = 0; k < qa.ntarget; ++k) {
+      if (!act[k]) continue;
+      const uint32_t key = qa.keys[qa.tg[k].q][i];
+      if (key < ilo[k]) acc[k] += w;
+      else if (key <= ihi[k])
+        atomicAdd(&qa.fhist[(size_t)k * Q_FB + sub_bin(key, ilo[k], ihi[k], Q_FB)],
+                  (unsigned long long)llrint(w * qa.fx_scale));
+    }
+  }
+  // deterministic combine of the below-interval sums
+  __shared__ double red[8][Q_MAXT];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = 0; k < Q_MAXT; ++k) {
+    double v = acc[k];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < Q_MAXT) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += red[w][threadIdx.x];
+    qa.part[(size_t)blockIdx.x * (Q_MAXT + 1) + threadIdx.x] = s;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&qa.sh->fb_counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < qa.ntarget && act[threadIdx.x]) {
+    double s = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(&qa.part[(size_t)b * (Q_MAXT + 1) + threadIdx.x]);
+    qa.tg[threadIdx.x].ibelow = s;
+  }
+  if (threadIdx.x == 0) qa.sh->fb_counter = 0;
+}
+
+// F2: pick the fallback bin holding the crossing; it becomes the new window
+// (one CTA per target).  If the interval does not hold it (attempt 0's
+// bounded guess fell short) the target is marked for attempt 1.
+__global__ void __launch_bounds__(1024) q_fallback_select_kernel(QArgs qa, int attempt, const int64_t* fail) {
+  if (*fail || !qa.sh->fb_active[attempt]) return;
+  const int k = blockIdx.x;
+  QTarget& t = qa.tg[k];
+  if (t.status != QS_FB) return;
+  __shared__ unsigned long long pre[Q_FB + 1];
+  __shared__ int bsel;
+  const double T = t.p * qa.sh->W;
+  unsigned long long* F = qa.fhist + (size_t)k * Q_FB;
+  for (int j = threadIdx.x; j < Q_FB; j += blockDim.x) {
+    pre[j] = F[j];
+    F[j] = 0ull;  // leave the row clean for the next attempt / step
+  }
+  if (threadIdx.x == 0) bsel = Q_FB;
+  __syncthreads();
+  const unsigned long long tot = block_exclusive_scan(pre, Q_FB);
+  if (threadIdx.x == 0) pre[Q_FB] = tot;
+  __syncthreads();
+  for (int j = threadIdx.x; j < Q_FB; j += blockDim.x)
+    if (t.ibelow + (double)pre[j + 1] / qa.fx_scale >= T && !(t.ibelow + (double)pre[j] / qa.fx_scale >= T))
+      atomicMin(&bsel, j);
+  __syncthreads();
+  // clear this target's sub-bin histogram for the resolve round that follows
+  for (int j = threadIdx.x; j < Q_SUB; j += blockDim.x) qa.hist[(size_t)k * Q_SUB + j] = 0ull;
+  if (threadIdx.x != 0) return;
+  atomicAdd(&qa.stats[1], 1u);
+  const bool below = !(T > t.ibelow);
+  const bool above = T > t.ibelow + (double)tot / qa.fx_scale;
+  if ((below || above) && attempt == 0 && !(t.ilo == 0 && below) && !(t.ihi == 0xFFFFFFFFu && above)) {
+    t.side = below ? -1 : 1;
+    t.status = QS_RETRY;
+    return;
+  }
+  const int b = bsel < Q_FB ? bsel : (below ? 0 : Q_FB - 1);
+  const unsigned long long s = pre[b];
+  // key range of fallback bin b: smallest keys mapping to b and b+1
+  const uint64_t span = (uint64_t)(t.ihi - t.ilo) + 1;
+  const uint64_t lo_off = ((uint64_t)b * span + Q_FB - 1) / Q_FB;
+  const uint64_t hi_off = ((uint64_t)(b + 1) * span + Q_FB - 1) / Q_FB;  // exclusive
+  t.klo = (uint32_t)(t.ilo + lo_off);
+  t.khi = (uint32_t)(t.ilo + (hi_off > lo_off ? hi_off - 1 : lo_off));
+  t.wbelow = t.ibelow + (double)s / qa.fx_scale;
+  t.count = 0;
+  t.status = QS_REFILL;
+}
+
+// F3: append the candidates of the re-windowed targets.
+__global__ void __launch_bounds__(256) q_fallback_fill_kernel(QArgs qa, const double* __restrict__ lw, int wmode,
+                                                              const double* Mp, int64_t n, int single,
+                                                              const int64_t* fail) {
+  if (*fail || !qa.sh->fb_active[0]) return;
+  const double M = wmode == 0 ? *Mp : 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int k = 0; k < qa.ntarget; ++k) {
+      QTarget& t = qa.tg[k];
+      if (t.status != QS_REFILL) continue;
+      const uint32_t key = qa.keys[t.q][i];
+      if (key >= t.klo && key <= t.khi) {
+        double w = wmode == 0 ? exp(lw[i] - M) : lw[i];
+        if (single) w = (double)(float)w;
+        const uint32_t pos = atomicAdd(&t.count, 1u);
+        if (pos < qa.cap) {
+          QCand c;
+          c.key = key;
+          c.idx = (uint32_t)i;
+          c.w = w;
+          qa.cand[(size_t)k * qa.cap + pos] = c;
+        }
+      }
+    }
+  }
+}
+
+// S: last resort for a target whose re-windowed candidates still crowd the
+// exact list (heavy ties): weighted radix select over the exact 64-bit value
+// images of all candidates (one CTA per target).  Smallest value v with
+// wbelow + sum_{value <= v} w >= p W -- the same answer as the stable-order
+// cumulative search.
+__global__ void __launch_bounds__(1024)
+q_select_kernel(QArgs qa, QValueSrc vs, double* __restrict__ scratch, double* out_x, double* out_s,
+                double* out_t, int64_t t_step, const int64_t* fail, unsigned int* unresolved) {
+  if (*fail || !qa.sh->any_miss) return;
+  const int k = blockIdx.x;
+  QTarget& tg = qa.tg[k];
+  if (tg.status == QS_OK) return;
+  __shared__ unsigned long long hist[256];
+  __shared__ uint64_t prefix;
+  __shared__ double base;
+  const uint32_t m = min(tg.count, qa.cap);
+  double* val = scratch + (size_t)k * qa.cap;
+  const QCand* cand = qa.cand + (size_t)k * qa.cap;
+  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) val[i] = quantity_value(vs, tg.q, cand[i].idx);
+  const double T = tg.p * qa.sh->W;
+  if (threadIdx.x == 0) {
+    prefix = 0;
+    base = tg.wbelow;
+  }
+  __syncthreads();
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const uint64_t pfx = prefix;
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+      const uint64_t b = ordered_bits(val[i]);
+      if (shift == 56 || (b >> (shift + 8)) == pfx)
+        atomicAdd(&hist[(b >> shift) & 255], (unsigned long long)llrint(cand[i].w * qa.fx_scale));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long s = 0;
+      int d = -1, lastnz = 0;
+      for (int j = 0; j < 256; ++j) {
+        if (hist[j]) lastnz = j;
+        if (d < 0 && hist[j] && base + (double)(s + hist[j]) / qa.fx_scale >= T) d = j;
+        if (d < 0) s += hist[j];
+      }
+      if (d < 0) { d = lastnz; s -= hist[lastnz]; }
+      base += (double)s / qa.fx_scale;
+      prefix = (pfx << 8) | (uint64_t)d;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const uint64_t b = prefix;
+    union { uint64_t u; double d; } c;
+    c.u = (b >> 63) ? (b & 0x7FFFFFFFFFFFFFFFull) : ~b;
+    const double v = m ? c.d : NAN;
+    double* o = tg.q == 0 ? out_x : (tg.q == 1 ? out_s : out_t);
+    const int ncol = tg.q == 0 ? 3 : 5;
+    o[(t_step - 1) * ncol + tg.col] = v;
+    if (tg.count > qa.cap) atomicAdd(unresolved, 1u);
+    tg.status = QS_OK;
+  }
+}
+
+// End of step: widen windows that missed, clear the per-step histograms
+// and counters for the next step.
+__global__ void __launch_bounds__(1024) q_step_end_kernel(QArgs qa, int had_miss_possible) {
+  for (int i = threadIdx.x; i < qa.ntarget * Q_SUB; i += blockDim.x) qa.hist[i] = 0ull;
+  __syncthreads();
+  const int k = threadIdx.x;
+  if (k < qa.ntarget) {
+    QTarget& t = qa.tg[k];
+    t.missed = 0;
+    t.count = 0;
+    t.status = QS_OK;
+  }
+  if (k == 0) {
+    qa.sh->any_miss = 0;
+    qa.sh->fb_active[0] = qa.sh->fb_active[1] = 0;
+  }
+  (void)had_miss_possible;
+}
+
+}  // namespace pf

@@ -132,7 +132,7 @@ PF_HD double gamma_pq(double a, double x, bool lower, double* dprefac) {
     for (int n = 1; n < 100000; ++n) {
       term *= x / (a + n);
       sum += term;
-      if (term < sum * 1e-18) break;
+      if (term < sum * 1e-17) break;
     }
     double P = D * sum;
     return lower ? P : 1.0 - P;
@@ -150,7 +150,7 @@ PF_HD double gamma_pq(double a, double x, bool lower, double* dprefac) {
     dd = 1.0 / dd;
     double del = dd * c;
     h *= del;
-    if (fabs(del - 1.0) < 1e-18) break;
+    if (fabs(del - 1.0) < 4e-16) break;  // del == 1 to within an ulp
   }
   double Q = D * a * h;
   return lower ? 1.0 - Q : Q;
@@ -172,7 +172,8 @@ PF_HD double gamma_quantile_pv(double a, double p, double v, bool lower) {
       x = fmax(a, -log(v) + (a - 1.0) * log(fmax(1.0, -log(v))));
   }
   double lo = 0.0, hi = INFINITY;
-  for (int it = 0; it < 200; ++it) {
+  double last_step = INFINITY;
+  for (int it = 0; it < 80; ++it) {
     double D;
     double f = gamma_pq(a, x, lower, &D);
     double F = lower ? (f - p) : (v - f);  // increasing in x
@@ -187,10 +188,13 @@ PF_HD double gamma_quantile_pv(double a, double p, double v, bool lower) {
     if (!(xn > lo && xn < hi) || !(dF > 0.0)) {
       xn = (hi == INFINITY) ? (lo > 0 ? lo * 2.0 : x * 2.0) : (lo > 0.0 ? sqrt(lo * hi) : 0.5 * hi);
     }
-    if (fabs(xn - x) <= 2e-16 * x) {
+    const double dx = fabs(xn - x);
+    // converged to an ulp, or Halley has started to oscillate at rounding level
+    if (dx <= 4e-16 * x || (it > 3 && dx >= last_step && dx <= 1e-13 * x)) {
       x = xn;
       break;
     }
+    last_step = dx;
     x = xn;
   }
   return x;

@@ -24,6 +24,13 @@ namespace pf {
 
 constexpr double LOG_TWO_PI = 1.8378770664093453;  // math.log(2*math.pi), models.py:20
 
+// Order-preserving 32-bit image of a double (float32 rounded down, sign
+// folded): the quantile keys of quantile.cuh.
+PF_D uint32_t key_rd_(double v) {
+  const uint32_t b = __float_as_uint(__double2float_rd(v));
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
 // Carried per-slot state.  sigma2 is not carried: it is redrawn before it
 // is used (filtering.py:280) and recomputed from the record when a
 // post-resample system is materialised.  a_sigma / a_tau are per-step
@@ -43,6 +50,21 @@ struct GammaSrc {
 PF_D double gamma_draw(const GammaSrc& g, double u) {
   if (g.method == 0) return gt_eval(g.table, u);
   return gamma_quantile_accurate(g.shape, u);
+}
+
+// Per-step tables staged in shared memory by the step kernel; indexing the
+// extern symbol directly keeps the loads LDS (not generic LD).
+extern __shared__ double pf_gtab[];
+
+PF_D double gamma_draw_slot(const GammaSrc& g, int slot, double u) {
+  if (slot < 0) return gamma_draw(g, u);
+  double t;
+  const int seg = gt_segment(u, &t);
+  const double* c = pf_gtab + slot * GT_TABLE_DOUBLES + seg * GT_NC;
+  double r = c[GT_DEG];
+#pragma unroll
+  for (int k = GT_DEG - 1; k >= 0; --k) r = fma(r, t, c[k]);
+  return r;
 }
 
 // -------------------------------------------------------- table build ---
@@ -127,13 +149,14 @@ __global__ void __launch_bounds__(256) init_kernel(InitArgs a) {
 
 // ---------------------------------------------------------------- step ---
 struct Partial {
-  double m, s0, sx, s1s, s2s, s1t, s2t, bad;
+  double m, s0, sx, s2x, s1s, s2s, s1t, s2t, bad;
 };
 
 struct Scalars {
   double M;        // max log-weight of the current step
   double W;        // total weight (moment normalizer)
   double cs, ct;   // moment shifts (previous step means)
+  double cx;
   unsigned int counter;
   unsigned int pad;
 };
@@ -157,17 +180,18 @@ struct StepArgs {
   const Rec* rec_in;
   Rec* rec_out;
   double* lw;            // log-weights (or fed weights when feed_w)
+  double* Mout;          // max log-weight of this step (per-parity slot)
   uint64_t* u3;          // resampling word of the previous step (in), this step (out)
-  const TQ* q_prev;      // CDF of step t-1 (t > 1)
-  const int32_t* cut_prev;
+  Lookup<TQ> lk;         // resampling table of step t-1 (t > 1)
   int64_t* idx_out;      // optional 1-based ancestors of step t-1
   const double* feed_z;  // oracle feed rows for step t (or null)
   const double* feed_gs;
   const double* feed_gt;
   const double* feed_w;
-  double* qx;            // optional SoA copies for the weighted quantiles
-  double* qs;
-  double* qt;
+  uint32_t* kx;          // optional order-preserving 32-bit keys for the
+  uint32_t* ks;          // weighted quantiles (quantile.cuh)
+  uint32_t* kt;
+  double* qmom;          // optional: mean[3], sd[3] of x, sigma2, tau2
   Partial* partials;
   Scalars* sc;
   StepOut out;
@@ -190,10 +214,29 @@ template <int MODE, typename TQ>
 __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
   constexpr bool LS = MODE & M_LS, LT = MODE & M_LT, SINGLE = MODE & M_SINGLE;
   if (*a.fail) return;
+  // This step's inverse-gamma table(s) -> shared memory (41 KB each; one
+  // copy when sigma2 and tau2 share the shape schedule).
+  const GammaSrc gs = a.gs, gt = a.gt;
+  int slot_s = -1, slot_t = -1;  // table slots in pf_gtab (shared), -1 = not tabulated
+  {
+    const double* srcs[2] = {LS && gs.method == 0 ? gs.table : nullptr,
+                             LT && gt.method == 0 && !(LS && gt.table == gs.table) ? gt.table : nullptr};
+    int slot = 0;
+    for (int k = 0; k < 2; ++k) {
+      if (!srcs[k]) continue;
+      const double2* s2p = reinterpret_cast<const double2*>(srcs[k]);
+      double2* d2p = reinterpret_cast<double2*>(pf_gtab + slot * GT_TABLE_DOUBLES);
+      for (int i = threadIdx.x; i < GT_TABLE_DOUBLES / 2; i += blockDim.x) d2p[i] = __ldg(&s2p[i]);
+      if (k == 0) slot_s = slot; else slot_t = slot;
+      ++slot;
+    }
+    if (LS && LT && gs.method == 0 && a.gt.table == a.gs.table) slot_t = slot_s;
+    __syncthreads();
+  }
   const bool feedw = a.feed_w != nullptr;
-  const double cs = a.sc->cs, ct = a.sc->ct;
+  const double cs = a.sc->cs, ct = a.sc->ct, cx = a.sc->cx;
   double m = feedw ? 0.0 : -INFINITY;
-  double s0 = 0, sx = 0, s1s = 0, s2s = 0, s1t = 0, s2t = 0;
+  double s0 = 0, sx = 0, s2x = 0, s1s = 0, s2s = 0, s1t = 0, s2t = 0;
   bool bad = false;
 
   const int64_t lo = blockIdx.x * a.per_block;
@@ -202,8 +245,7 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
     // ---- resample of step t-1: cut-point lookup + joint gather
     int64_t anc = j;
     if (a.t > 1) {
-      const double u = unit_open(a.u3[j]);
-      anc = cutpoint_lookup<TQ>(a.q_prev, a.cut_prev, a.n, u);
+      anc = ancestor_of<TQ>(a.lk, a.u3[j]);
       if (a.idx_out) a.idx_out[j] = anc + 1;
     }
     const Rec r = a.rec_in[anc];
@@ -224,12 +266,12 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
     double s2 = a.sigma2_fixed, t2 = a.tau2_fixed;
     if (LS) {
       o.bs = r.bs + h;
-      const double g = a.feed_gs ? a.feed_gs[j] : gamma_draw(a.gs, unit_open(P.w[1]));
+      const double g = a.feed_gs ? a.feed_gs[j] : gamma_draw_slot(gs, slot_s, unit_open(P.w[1]));
       s2 = o.bs / g;
     }
     if (LT) {
       o.bt = r.bt + (0.5 * step) * step;
-      const double g = a.feed_gt ? a.feed_gt[j] : gamma_draw(a.gt, unit_open(P.w[2]));
+      const double g = a.feed_gt ? a.feed_gt[j] : gamma_draw_slot(gt, slot_t, unit_open(P.w[2]));
       t2 = o.bt / g;
     }
     o.tau2 = t2;
@@ -249,7 +291,7 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
       if (!(lw == lw) || lw == INFINITY) bad = true;
       if (lw > m) {
         const double sc = exp(m - lw);
-        s0 *= sc; sx *= sc; s1s *= sc; s2s *= sc; s1t *= sc; s2t *= sc;
+        s0 *= sc; sx *= sc; s2x *= sc; s1s *= sc; s2s *= sc; s1t *= sc; s2t *= sc;
         m = lw;
         e = 1.0;
       } else if (lw > -INFINITY) {
@@ -258,11 +300,13 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
         e = 0.0;
       }
     }
-    if (a.qx) a.qx[j] = xn;
-    if (a.qs) a.qs[j] = s2;
-    if (a.qt) a.qt[j] = t2;
+    if (a.kx) a.kx[j] = key_rd_(xn);
+    if (a.ks) a.ks[j] = key_rd_(s2);
+    if (a.kt) a.kt[j] = key_rd_(t2);
     s0 += e;
     sx = fma(e, xn, sx);
+    const double dxx = xn - cx;
+    s2x = fma(e * dxx, dxx, s2x);
     const double ds = s2 - cs, dt = t2 - ct;
     const double eds = e * ds, edt = e * dt;
     s1s += eds;
@@ -287,22 +331,24 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
   __syncthreads();
   const double mb = mblk;
   const double scl = (m == -INFINITY) ? 0.0 : exp(m - mb);
-  double v[7] = {s0 * scl, sx * scl, s1s * scl, s2s * scl, s1t * scl, s2t * scl, bad ? 1.0 : 0.0};
+  double v[8] = {s0 * scl, sx * scl, s2x * scl, s1s * scl, s2s * scl, s1t * scl, s2t * scl,
+                 bad ? 1.0 : 0.0};
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < 7; ++k) {
+  for (int k = 0; k < 8; ++k) {
     const double s = warp_sum(v[k]);
     if (lane == 0) red[warp][k] = s;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
-      for (int k = 0; k < 7; ++k) acc[k] += red[w][k];
+      for (int k = 0; k < 8; ++k) acc[k] += red[w][k];
     Partial p;
     p.m = mb;
-    p.s0 = acc[0]; p.sx = acc[1]; p.s1s = acc[2]; p.s2s = acc[3]; p.s1t = acc[4]; p.s2t = acc[5];
-    p.bad = acc[6];
+    p.s0 = acc[0]; p.sx = acc[1]; p.s2x = acc[2]; p.s1s = acc[3]; p.s2s = acc[4]; p.s1t = acc[5];
+    p.s2t = acc[6];
+    p.bad = acc[7];
     a.partials[blockIdx.x] = p;
     __threadfence();
     const unsigned int ticket = atomicAdd(&a.sc->counter, 1u);
@@ -332,46 +378,57 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
   }
   __syncthreads();
   M = mblk;
-  double acc[6] = {0, 0, 0, 0, 0, 0};
+  double acc[7] = {0, 0, 0, 0, 0, 0, 0};
   for (int b = threadIdx.x; b < G; b += blockDim.x) {
     const double mb2 = __ldcg(&a.partials[b].m);
     const double f = (mb2 == -INFINITY) ? 0.0 : exp(mb2 - M);
     acc[0] += f * __ldcg(&a.partials[b].s0);
     acc[1] += f * __ldcg(&a.partials[b].sx);
-    acc[2] += f * __ldcg(&a.partials[b].s1s);
-    acc[3] += f * __ldcg(&a.partials[b].s2s);
-    acc[4] += f * __ldcg(&a.partials[b].s1t);
-    acc[5] += f * __ldcg(&a.partials[b].s2t);
+    acc[2] += f * __ldcg(&a.partials[b].s2x);
+    acc[3] += f * __ldcg(&a.partials[b].s1s);
+    acc[4] += f * __ldcg(&a.partials[b].s2s);
+    acc[5] += f * __ldcg(&a.partials[b].s1t);
+    acc[6] += f * __ldcg(&a.partials[b].s2t);
   }
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < 6; ++k) {
+  for (int k = 0; k < 7; ++k) {
     const double s = warp_sum(acc[k]);
     if (lane == 0) red[warp][k] = s;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double S[6] = {0, 0, 0, 0, 0, 0};
+    double S[7] = {0, 0, 0, 0, 0, 0, 0};
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
-      for (int k = 0; k < 6; ++k) S[k] += red[w][k];
+      for (int k = 0; k < 7; ++k) S[k] += red[w][k];
     const int64_t i = a.t - 1;
     const double W = S[0];
-    a.out.fmean[i] = S[1] / W;
+    const double fm = S[1] / W;
+    a.out.fmean[i] = fm;
+    {
+      const double d = fm - cx;
+      const double var = S[2] / W - d * d;
+      if (a.qmom) { a.qmom[0] = fm; a.qmom[3] = sqrt(fmax(var, 0.0)); }
+      a.sc->cx = fm;
+    }
     if (LS) {
-      const double d = S[2] / W;
-      const double var = S[3] / W - d * d;
+      const double d = S[3] / W;
+      const double var = S[4] / W - d * d;
       a.out.s_mean[i] = cs + d;
       a.out.s_sd[i] = sqrt(fmax(var, 0.0));
       a.sc->cs = cs + d;
+      if (a.qmom) { a.qmom[1] = cs + d; a.qmom[4] = a.out.s_sd[i]; }
     }
     if (LT) {
-      const double d = S[4] / W;
-      const double var = S[5] / W - d * d;
+      const double d = S[5] / W;
+      const double var = S[6] / W - d * d;
       a.out.t_mean[i] = ct + d;
       a.out.t_sd[i] = sqrt(fmax(var, 0.0));
       a.sc->ct = ct + d;
+      if (a.qmom) { a.qmom[2] = ct + d; a.qmom[5] = a.out.t_sd[i]; }
     }
     a.sc->M = feedw ? 0.0 : M;
+    *a.Mout = feedw ? 0.0 : M;
     a.sc->W = W;
     a.sc->counter = 0;
     if (!feedw && !(M > -INFINITY && M < INFINITY))
@@ -388,8 +445,7 @@ struct MatArgs {
   int resample;            // 1: ancestors by lookup of u3 against q/cut
   const Rec* rec;
   const uint64_t* u3;
-  const TQ* q;
-  const int32_t* cut;
+  Lookup<TQ> lk;
   const double* s2_direct; // sigma2 per slot when no resample (init)
   GammaSrc gs;
   const double* feed_gs;   // oracle feed row t (indexed by ancestor)
@@ -412,7 +468,7 @@ __global__ void __launch_bounds__(256) materialize_kernel(MatArgs<TQ> a) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n;
        j += (int64_t)gridDim.x * blockDim.x) {
     int64_t anc = j;
-    if (a.resample) anc = cutpoint_lookup<TQ>(a.q, a.cut, a.n, unit_open(a.u3[j]));
+    if (a.resample) anc = ancestor_of<TQ>(a.lk, a.u3[j]);
     if (a.idx) a.idx[j] = anc + 1;
     const Rec r = a.rec[anc];
     if (a.x) a.x[j] = r.x;

@@ -81,6 +81,11 @@ class Engine:
         return {"total_ms": tot.value, "step_kernel_ms": step.value,
                 "step_kernel_launches": nsteps.value, "kernels": nk.value}
 
+    def quantile_stats(self):
+        s = (C.c_int64 * 4)()
+        _lib.check(self.lib.pf_engine_quantile_stats(self.h, s), self.lib)
+        return {"unresolved": s[0], "fallbacks": s[1], "max_candidates": s[2], "resolves": s[3]}
+
     def close(self):
         if self.h:
             self.lib.pf_engine_destroy(self.h)

@@ -1,4 +1,4 @@
-"""Short device run for ncu: PL at N=2^k, T steps (resident), no host outputs.
+"""Short device run for ncu / diagnostics: PL at N=2^k, T steps (resident).
 Usage: python scripts/prof_run.py [log2n] [T] [track_quantiles]"""
 import os
 import sys
@@ -13,6 +13,7 @@ _, y = P.simulate(P.TrendNoiseModel(), T, P.RngStream(0, P.rng.AUX_STREAM_BASE +
 b = P.Backend()
 P.run_particle_learning(P.Priors(), y, 1 << k, seed=0, backend=b, track_quantiles=tq)
 eng = next(iter(b._engines.values()))
+print("api run", eng.last_timing(), eng.quantile_stats())
 eng.run_resident(T)
-print(eng.last_timing())
+print("resident", eng.last_timing(), eng.quantile_stats())
 b.close()

@@ -242,3 +242,29 @@ def test_large_n_properties(gpu, k):
         s = a.param_posterior[nm]
         assert (np.diff(s.quantiles, axis=1) >= 0).all()
         assert ((s.quantiles[:, 0] <= s.mean) & (s.mean <= s.quantiles[:, 4])).all()
+
+
+@pytest.mark.parametrize("learn", [True, False])
+def test_oracle_mode_strata_path(gpu, learn):
+    # N >= 2^21 switches the resampling table to the integer strata records
+    # (csrc/cdf.cuh SRec/PRec); ancestors must still equal the reference's
+    # cutpoint_indices bit for bit.  Reference draws come from the oracle
+    # (scipy ndtri / gammaincinv, the reference's own dependencies).
+    n, t_len = 1 << 21, 3
+    _, y = R.simulate(1.0, 0.1, 0.0, t_len, 5)
+    rec = {}
+    if learn:
+        ref = R.run_loop(y, n, 7, keep_indices=True, record=rec)
+        feed = {k: np.stack([rec[k][t] for t in sorted(rec[k])]) for k in ("z", "g_sigma", "g_tau")}
+        out = P.run_particle_learning(P.Priors(), y, n, seed=7, keep_indices=True, noise=feed)
+    else:
+        ref = R.run_loop(y, n, 7, keep_indices=True, sigma2=1.0, tau2=0.1, record=rec)
+        feed = {"z": np.stack([rec["z"][t] for t in sorted(rec["z"])])}
+        out = P.run_particle_filter(P.TrendNoiseModel(), y, n, seed=7, keep_indices=True, noise=feed)
+    assert np.array_equal(out.resampled_indices, ref["indices"])
+    assert np.array_equal(out.filtered_quantiles, ref["filtered_quantiles"])
+    assert np.max(np.abs(out.filtered_mean - ref["filtered_mean"])) <= REL * np.max(np.abs(ref["filtered_mean"]))
+    if learn:
+        for nm in ("sigma2", "tau2"):
+            assert np.array_equal(out.param_posterior[nm].quantiles, ref[nm]["quantiles"])
+            assert _rel(out.param_posterior[nm].mean, ref[nm]["mean"]) <= REL
