@@ -219,11 +219,11 @@ cdf_top_kernel(const T* __restrict__ chunk_tot, int64_t G, T* __restrict__ node,
 // beyond the stratum), and the walk continues over per-particle (L, F)
 // pairs only when u lies past the first candidate.  Same answer as
 // cutpoint_indices (resampling.py:146-158), bit for bit.
-struct SRec {
+struct alignas(8) SRec {  // 8-byte aligned: one 64-bit load, one L2 request
   int32_t first;  // 0-based I_s
   uint32_t f;     // F of I_s if L_{I_s} == s, else 0xFFFFFFFF
 };
-struct PRec {
+struct alignas(8) PRec {
   int32_t L;      // ceil(N q_k) (0 for a zero-mass prefix)
   uint32_t f;
 };

@@ -265,6 +265,8 @@ struct pf_engine {
   DevBuf<double> mbuf;    // max log-weight per parity
   DevBuf<unsigned long long> qhist, qfhist;
   DevBuf<unsigned int> qunres;
+  DevBuf<uint32_t> qlidx;
+  DevBuf<double> qlw;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_b = nullptr, ev_e = nullptr;
   DevBuf<Partial> partials;
@@ -451,6 +453,10 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     CK(e->qhist.ensure((size_t)Q_MAXT * Q_SUB));
     CK(e->qfhist.ensure((size_t)Q_MAXT * Q_FB));
     CK(e->qunres.ensure(4));
+    CK(e->qlidx.ensure((size_t)Q_MAXT * Q_LIST));
+    CK(e->qlw.ensure((size_t)Q_MAXT * Q_LIST));
+    qa.lidx = e->qlidx.p;
+    qa.lw = e->qlw.p;
     CK(cudaMemcpyAsync(e->qtg.p, tgs.data(), ntg * sizeof(QTarget), cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(e->qsh.p, 0, 2 * sizeof(QShared), st));
     CK(cudaMemsetAsync(e->qhist.p, 0, (size_t)Q_MAXT * Q_SUB * 8, st));
@@ -690,13 +696,16 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       const int hgrid = std::max(1, std::min(64, (int)((n / 64 + 255) / 256)));
       static bool resolve_attr = false;
       if (!resolve_attr) {
-        CK(cudaFuncSetAttribute(q_resolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CK(cudaFuncSetAttribute(q_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 Q_RESOLVE_SMEM));
         resolve_attr = true;
       }
       for (int round = 0; round < 2; ++round) {
         q_hist_kernel<<<dim3(hgrid, ntg), 256, 0, ss>>>(qa, e->fail.p, round);
-        q_resolve_kernel<<<ntg, 1024, Q_RESOLVE_SMEM, ss>>>(qa, vs, ox, os, ot, t, e->fail.p, round);
+        q_locate_kernel<<<ntg, 1024, 0, ss>>>(qa, e->fail.p, round);
+        q_filter_kernel<<<dim3(hgrid, ntg), 256, 0, ss>>>(qa, e->fail.p);
+        q_finish_kernel<<<ntg, 1024, Q_RESOLVE_SMEM, ss>>>(qa, vs, ox, os, ot, t, e->fail.p);
+        g_launches.fetch_add(2);
         if (round == 0) {
           // misses: bounded re-window (attempt 0), whole side (attempt 1)
           for (int attempt = 0; attempt < 2; ++attempt) {
@@ -1065,6 +1074,8 @@ int pf_engine_destroy(pf_engine* e) {
   e->qhist.release();
   e->qfhist.release();
   e->qunres.release();
+  e->qlidx.release();
+  e->qlw.release();
   if (e->side) cudaStreamSynchronize(e->side);
   if (e->side) cudaStreamDestroy(e->side);
   if (e->ev_b) cudaEventDestroy(e->ev_b);

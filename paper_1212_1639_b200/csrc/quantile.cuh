@@ -32,10 +32,10 @@ constexpr int Q_MAXT = 13;       // targets: 3 state + 5 + 5 parameter probs
 constexpr int Q_SUB = 2048;      // sub-bins per window
 constexpr int Q_FB = 4096;       // fallback bins per missed interval
 constexpr int Q_LIST = 4096;     // exact-resolve list capacity (per target)
-constexpr int Q_RESOLVE_SMEM = (Q_SUB + 1) * 8 + Q_LIST * (8 + 8 + 4);
+constexpr int Q_RESOLVE_SMEM = Q_LIST * (8 + 8 + 4);
 
 enum : uint32_t { QS_OK = 0, QS_MISS_LO = 1, QS_MISS_HI = 2, QS_OVERFLOW = 3, QS_CROWD = 4,
-                  QS_REFILL = 5, QS_FB = 6, QS_RETRY = 7 };
+                  QS_REFILL = 5, QS_FB = 6, QS_RETRY = 7, QS_LOCATED = 8 };
 
 PF_HD uint32_t key_of_float(float f) {
   union { float f; uint32_t u; } c;
@@ -69,6 +69,9 @@ struct QTarget {
   uint32_t missed;   // the predicted window missed this step
   double wmass;      // candidate weight inside the window
   int side;          // fallback retry side (-1 below, +1 above)
+  int bstar;         // crossing sub-bin
+  double cum0;       // weight below sub-bin bstar-1
+  uint32_t nlist;    // candidates kept for the exact resolve
 };
 
 PF_HD double normal_pdf(double z) { return 0.3989422804014327 * exp(-0.5 * z * z); }
@@ -95,6 +98,8 @@ struct QArgs {
   unsigned long long* fhist;   // [ntarget][Q_FB]
   double fx_scale;             // fixed-point units per unit weight
   unsigned int* stats;         // [0] unresolved, [1] fallbacks, [2] max candidates, [3] resolves
+  uint32_t* lidx;              // [ntarget][Q_LIST] exact-resolve lists
+  double* lw;
 };
 
 // Window of target k for this step from mean/sd of its quantity.
@@ -149,8 +154,24 @@ struct QWin {
   int n;
 };
 
-PF_D void q_classify(const QArgs& qa, const QWin& win, uint32_t i, double w, double (&acc)[Q_MAXT],
-                     bool valid) {
+// CTA-level candidate staging (shared memory).
+constexpr int Q_AGG = 2048;
+struct QAgg {
+  QCand c[Q_AGG];
+  uint32_t pos[Q_AGG];
+  uint8_t tk[Q_AGG];
+  uint32_t cnt[Q_MAXT];
+  uint32_t base[Q_MAXT];
+  int fill;
+};
+
+PF_D void q_agg_init(QAgg& agg) {
+  if (threadIdx.x == 0) agg.fill = 0;
+  if (threadIdx.x < Q_MAXT) agg.cnt[threadIdx.x] = 0;
+}
+
+PF_D void q_classify(const QArgs& qa, const QWin& win, QAgg& agg, uint32_t i, double w,
+                     double (&acc)[Q_MAXT], bool valid) {
   const int lane = threadIdx.x & 31;
   const uint32_t k0 = (valid && qa.keys[0]) ? qa.keys[0][i] : 0u;
   const uint32_t k1 = (valid && qa.keys[1]) ? qa.keys[1][i] : 0u;
@@ -170,21 +191,58 @@ PF_D void q_classify(const QArgs& qa, const QWin& win, uint32_t i, double w, dou
     const int k = __ffs(any) - 1;
     any &= any - 1;
     const unsigned m = __ballot_sync(0xffffffffu, (inwin >> k) & 1u);
-    uint32_t base = 0;
     const int leader = __ffs(m) - 1;
-    if (lane == leader) base = atomicAdd(&qa.tg[k].count, (uint32_t)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, leader);
+    const uint32_t key = win.q[k] == 0 ? k0 : (win.q[k] == 1 ? k1 : k2);
+    // stage in the CTA buffer (shared atomics); spill straight to the global
+    // list (one global atomic per warp) only if the buffer is full
+    int slot = 0;
+    uint32_t kpos = 0;
+    if (lane == leader) {
+      slot = atomicAdd(&agg.fill, __popc(m));
+      if (slot + __popc(m) <= Q_AGG) kpos = atomicAdd(&agg.cnt[k], (uint32_t)__popc(m));
+      else kpos = 0x80000000u | atomicAdd(&qa.tg[k].count, (uint32_t)__popc(m));
+    }
+    slot = __shfl_sync(0xffffffffu, slot, leader);
+    kpos = __shfl_sync(0xffffffffu, kpos, leader);
     if ((inwin >> k) & 1u) {
-      const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
-      if (pos < qa.cap) {
-        QCand c;
-        c.key = win.q[k] == 0 ? k0 : (win.q[k] == 1 ? k1 : k2);
-        c.idx = i;
-        c.w = w;
-        qa.cand[(size_t)k * qa.cap + pos] = c;
+      const uint32_t rank = __popc(m & ((1u << lane) - 1u));
+      QCand c;
+      c.key = key;
+      c.idx = i;
+      c.w = w;
+      if (kpos & 0x80000000u) {
+        const uint32_t pos = (kpos & 0x7FFFFFFFu) + rank;
+        if (pos < qa.cap) qa.cand[(size_t)k * qa.cap + pos] = c;
+        if (slot + (int)rank < Q_AGG) agg.tk[slot + rank] = 0xFF;  // reserved, unused
+      } else {
+        agg.c[slot + rank] = c;
+        agg.tk[slot + rank] = (uint8_t)k;
+        agg.pos[slot + rank] = kpos + rank;
       }
     }
   }
+}
+
+// Flush the CTA's staged candidates: one global atomic per target reserves
+// space, then the whole CTA copies.  Called by all threads.
+PF_D void q_flush(const QArgs& qa, QAgg& agg) {
+  __syncthreads();
+  if (threadIdx.x < Q_MAXT) {
+    const uint32_t c = agg.cnt[threadIdx.x];
+    agg.base[threadIdx.x] = c ? atomicAdd(&qa.tg[threadIdx.x].count, c) : 0u;
+  }
+  __syncthreads();
+  const int nfill = min(agg.fill, Q_AGG);
+  for (int s = threadIdx.x; s < nfill; s += blockDim.x) {
+    const int k = agg.tk[s];
+    if (k == 0xFF) continue;
+    const uint32_t pos = agg.base[k] + agg.pos[s];
+    if (pos < qa.cap) qa.cand[(size_t)k * qa.cap + pos] = agg.c[s];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) agg.fill = 0;
+  if (threadIdx.x < Q_MAXT) agg.cnt[threadIdx.x] = 0;
+  __syncthreads();
 }
 
 // Block-reduce the below-window sums and W, combine CTAs in fixed order.
@@ -251,6 +309,8 @@ cdf_reduce_q_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ c
   __shared__ T wt[CDF_THREADS / 32];
   __shared__ T tt[64];
   __shared__ QWin win;
+  __shared__ QAgg agg;
+  q_agg_init(agg);
   q_make_windows(qa, win);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double M = src.mode == 0 ? *src.M : 0.0;
@@ -268,7 +328,7 @@ cdf_reduce_q_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ c
     for (int e = 0; e < CDF_V; ++e) {
       const double w = (double)v[e];
       wsum += w;
-      q_classify(qa, win, (uint32_t)(base + e), w, acc, true);
+      q_classify(qa, win, agg, (uint32_t)(base + e), w, acc, true);
     }
     thread_tree8<T>(v, l1, l2, g);
 #pragma unroll
@@ -288,6 +348,7 @@ cdf_reduce_q_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ c
       for (int i = 0; i < len / 2; ++i) tt[i] = tt[2 * i] + tt[2 * i + 1];
     chunk_tot[chunk] = tt[0];
   }
+  q_flush(qa, agg);
   q_reduce_partials(qa, win, acc, wsum);
 }
 
@@ -297,6 +358,8 @@ __global__ void __launch_bounds__(256)
 q_window_kernel(WSrc src, int64_t n, const int64_t* __restrict__ fail, QArgs qa) {
   if (fail && *fail) return;
   __shared__ QWin win;
+  __shared__ QAgg agg;
+  q_agg_init(agg);
   q_make_windows(qa, win);
   const double M = src.mode == 0 ? *src.M : 0.0;
   double acc[Q_MAXT];
@@ -310,8 +373,9 @@ q_window_kernel(WSrc src, int64_t n, const int64_t* __restrict__ fail, QArgs qa)
     const bool valid = i < n;
     const double w = valid ? (double)weight_of<T>(src.src[i], M, src.mode) : 0.0;
     wsum += w;
-    q_classify(qa, win, (uint32_t)(valid ? i : 0), w, acc, valid);
+    q_classify(qa, win, agg, (uint32_t)(valid ? i : 0), w, acc, valid);
   }
+  q_flush(qa, agg);
   q_reduce_partials(qa, win, acc, wsum);
 }
 
@@ -389,25 +453,19 @@ PF_D void bitonic_sort(double* v, uint32_t* id, double* w, int n2) {
     }
 }
 
-// R2: one CTA per target.  Locate the crossing sub-bin, order its candidates
-// exactly, write the quantile, update the predictor.  Misses set status.
+// R2a: one CTA per target.  Prefix the sub-bin histogram, classify the
+// window (hit / miss low / miss high / overflow), locate the crossing
+// sub-bin b* and the exact-enough weight below its left neighbour.
 __global__ void __launch_bounds__(1024)
-q_resolve_kernel(QArgs qa, QValueSrc vs, double* out_x, double* out_s, double* out_t, int64_t t_step,
-                 const int64_t* fail, int fallback_round) {
+q_locate_kernel(QArgs qa, const int64_t* fail, int fallback_round) {
   if (*fail) return;
   const int k = blockIdx.x;
   QTarget& tg = qa.tg[k];
   if (fallback_round && tg.status != QS_REFILL) return;
-  // dynamic smem: pre[Q_SUB+1] u64 | sv[Q_LIST] f64 | sw[Q_LIST] f64 | sid[Q_LIST] u32
-  extern __shared__ unsigned long long qsm[];
-  unsigned long long* pre = qsm;
-  double* sv = reinterpret_cast<double*>(qsm + Q_SUB + 1);
-  double* sw = sv + Q_LIST;
-  uint32_t* sid = reinterpret_cast<uint32_t*>(sw + Q_LIST);
-  __shared__ int bstar, nlist;
+  __shared__ unsigned long long pre[Q_SUB + 1];
+  __shared__ int bstar;
   __shared__ uint32_t status;
-  const double W = qa.sh->W;
-  const double T = tg.p * W;
+  const double T = tg.p * qa.sh->W;
   const double wb = tg.wbelow;
   const unsigned long long* H = qa.hist + (size_t)k * Q_SUB;
   for (int b = threadIdx.x; b < Q_SUB; b += blockDim.x) pre[b] = H[b];
@@ -422,37 +480,66 @@ q_resolve_kernel(QArgs qa, QValueSrc vs, double* out_x, double* out_s, double* o
     else if (!(T > wb)) status = QS_MISS_LO;
     else if (T > wb + (double)tot / qa.fx_scale) status = QS_MISS_HI;
     bstar = Q_SUB - 1;
-    nlist = 0;
   }
   __syncthreads();
-  // first sub-bin whose inclusive cumulative weight reaches T
   for (int j = threadIdx.x; j < Q_SUB; j += blockDim.x)
     if (wb + (double)pre[j + 1] / qa.fx_scale >= T && !(wb + (double)pre[j] / qa.fx_scale >= T))
       atomicMin(&bstar, j);
   __syncthreads();
-  if (status != QS_OK) {
-    if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) {
+    tg.wmass = (double)tot / qa.fx_scale;
+    tg.nlist = 0;
+    if (status != QS_OK) {
       tg.status = status;
-      tg.wmass = (double)tot / qa.fx_scale;
       qa.sh->any_miss = 1;
+    } else {
+      tg.status = QS_LOCATED;
+      tg.bstar = bstar;
+      tg.cum0 = wb + (double)pre[max(bstar - 1, 0)] / qa.fx_scale;
     }
-    return;
   }
-  const int b0 = max(bstar - 1, 0), b1 = min(bstar + 1, Q_SUB - 1);
-  const uint32_t n = tg.count;
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+}
+
+// R2b: grid pass over the candidate lists: keep the candidates of sub-bins
+// b*-1 .. b*+1 (a few hundred) for the exact resolve.
+__global__ void __launch_bounds__(256) q_filter_kernel(QArgs qa, const int64_t* fail) {
+  if (*fail) return;
+  const int k = blockIdx.y;
+  if (k >= qa.ntarget) return;
+  QTarget& t = qa.tg[k];
+  if (t.status != QS_LOCATED) return;
+  const uint32_t n = min(t.count, qa.cap);
+  const int b0 = max(t.bstar - 1, 0), b1 = min(t.bstar + 1, Q_SUB - 1);
+  const uint32_t lo = t.klo, hi = t.khi;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const QCand c = qa.cand[(size_t)k * qa.cap + i];
-    const int b = (int)sub_bin(c.key, tg.klo, tg.khi, Q_SUB);
+    const int b = (int)sub_bin(c.key, lo, hi, Q_SUB);
     if (b >= b0 && b <= b1) {
-      const int pos = atomicAdd(&nlist, 1);
+      const uint32_t pos = atomicAdd(&t.nlist, 1u);
       if (pos < Q_LIST) {
-        sid[pos] = c.idx;
-        sw[pos] = c.w;
+        qa.lidx[(size_t)k * Q_LIST + pos] = c.idx;
+        qa.lw[(size_t)k * Q_LIST + pos] = c.w;
       }
     }
   }
-  __syncthreads();
-  const int m = nlist;
+}
+
+// R2c: one CTA per target: exact values of the kept candidates, stable
+// (value, index) order, cumulative weight from cum0 -> the quantile; then
+// the window predictor update.
+__global__ void __launch_bounds__(1024)
+q_finish_kernel(QArgs qa, QValueSrc vs, double* out_x, double* out_s, double* out_t, int64_t t_step,
+                const int64_t* fail) {
+  if (*fail) return;
+  const int k = blockIdx.x;
+  QTarget& tg = qa.tg[k];
+  if (tg.status != QS_LOCATED) return;
+  // dynamic smem: sv[Q_LIST] f64 | sw[Q_LIST] f64 | sid[Q_LIST] u32
+  extern __shared__ unsigned long long qsm[];
+  double* sv = reinterpret_cast<double*>(qsm);
+  double* sw = sv + Q_LIST;
+  uint32_t* sid = reinterpret_cast<uint32_t*>(sw + Q_LIST);
+  const int m = (int)tg.nlist;
   if (m > Q_LIST) {
     if (threadIdx.x == 0) {
       tg.status = QS_CROWD;
@@ -463,13 +550,21 @@ q_resolve_kernel(QArgs qa, QValueSrc vs, double* out_x, double* out_s, double* o
   int n2 = 1;
   while (n2 < m) n2 <<= 1;
   for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-    if (i < m) sv[i] = quantity_value(vs, tg.q, sid[i]);
-    else { sv[i] = INFINITY; sid[i] = 0xFFFFFFFFu; sw[i] = 0.0; }
+    if (i < m) {
+      sid[i] = qa.lidx[(size_t)k * Q_LIST + i];
+      sw[i] = qa.lw[(size_t)k * Q_LIST + i];
+      sv[i] = quantity_value(vs, tg.q, sid[i]);
+    } else {
+      sv[i] = INFINITY;
+      sid[i] = 0xFFFFFFFFu;
+      sw[i] = 0.0;
+    }
   }
   __syncthreads();
   bitonic_sort(sv, sid, sw, n2);
   if (threadIdx.x == 0) {
-    double cum = wb + (double)pre[b0] / qa.fx_scale;
+    const double T = tg.p * qa.sh->W;
+    double cum = tg.cum0;
     double val = m > 0 ? sv[m - 1] : NAN;
     for (int i = 0; i < m; ++i) {
       cum += sw[i];
@@ -492,10 +587,10 @@ q_resolve_kernel(QArgs qa, QValueSrc vs, double* out_x, double* out_s, double* o
       tg.h = fmin(2.0, mass / phi);
       tg.zprev = z;
     }
-    if (fallback_round == 0) tg.wmass = (double)tot / qa.fx_scale;
     tg.status = QS_OK;
   }
 }
+
 
 // F0: interval for each target that missed.  Attempt 0 uses a secant
 // estimate from the missing mass, bounded so the histogram pass touches few
