@@ -497,4 +497,49 @@ PF_D int64_t ancestor_of(const Lookup<TQ>& L, uint64_t w3) {
   return cutpoint_lookup<TQ>(L.q, L.cut, L.n, unit_open(w3));
 }
 
+// SB lookups at once: all stratum-record loads are issued before any is
+// consumed (memory-level parallelism), then the rare walks.
+template <typename TQ, int SB>
+PF_D void ancestors_of(const Lookup<TQ>& L, const uint64_t (&w3)[SB], const bool (&ok)[SB],
+                       int64_t (&anc)[SB]) {
+  if (L.srec) {
+    uint32_t r[SB];
+    uint64_t s0[SB];
+    SRec R[SB];
+#pragma unroll
+    for (int b = 0; b < SB; ++b) {
+      const uint64_t K = ((w3[b] >> 12) << 1) | 1ull;
+      s0[b] = K >> L.B;
+      r[b] = (uint32_t)(K & ((1ull << L.B) - 1ull));
+    }
+#pragma unroll
+    for (int b = 0; b < SB; ++b) {
+      if (ok[b]) {
+        R[b] = L.srec[s0[b]];
+      } else {
+        R[b].first = 0;
+        R[b].f = 0xFFFFFFFFu;
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < SB; ++b) {
+      int64_t k = R[b].first;
+      if (r[b] > R[b].f) {
+        ++k;
+        const int32_t s = (int32_t)s0[b] + 1;
+        for (;;) {
+          const PRec p = L.pf[k];
+          if (p.L != s || r[b] <= p.f) break;
+          ++k;
+        }
+      }
+      if (ok[b]) anc[b] = k;
+    }
+    return;
+  }
+#pragma unroll
+  for (int b = 0; b < SB; ++b)
+    if (ok[b]) anc[b] = cutpoint_lookup<TQ>(L.q, L.cut, L.n, unit_open(w3[b]));
+}
+
 }  // namespace pf

@@ -449,7 +449,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     CK(e->qsh.ensure(2));
     CK(e->qcand.ensure((size_t)ntg * qcap));
     CK(e->qscratch.ensure((size_t)ntg * qcap));
-    CK(e->qpart.ensure((size_t)std::max<int64_t>(CDF_MAX_CHUNKS, sm_count() * 8) * (Q_MAXT + 1)));
+    CK(e->qpart.ensure((size_t)std::max<int64_t>(CDF_MAX_CHUNKS, sm_count() * 8) * (Q_SLOTS + 1)));
     CK(e->qhist.ensure((size_t)Q_MAXT * Q_SUB));
     CK(e->qfhist.ensure((size_t)Q_MAXT * Q_FB));
     CK(e->qunres.ensure(4));
@@ -558,7 +558,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   int step_grid = (int)((n + 255) / 256);
   if (step_grid > sms * 8) step_grid = sms * 8;
   int64_t per_block = (n + step_grid - 1) / step_grid;
-  per_block = (per_block + 255) / 256 * 256;
+  per_block = (per_block + 1023) / 1024 * 1024;  // STEP_SB x 256 slots per batch
   step_grid = (int)((n + per_block - 1) / per_block);
 
   // shared-memory copies of the step's gamma table(s)

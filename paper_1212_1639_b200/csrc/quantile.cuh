@@ -148,10 +148,15 @@ PF_D double quantity_value(const QValueSrc& s, int q, uint32_t idx) {
 // --------------------------------------------- classify (in CDF reduce) ---
 // Called by cdf_reduce for every element; accumulates below-window weight
 // into acc[k] and appends window candidates (warp-aggregated).
+// Windows of a step per quantity q; classification slot s = q * Q_PER + k
+// holds target base[q] + k.  Static slot indices keep the bounds and the
+// below-window sums in registers.
+constexpr int Q_PER = 5;                  // max targets per quantity
+constexpr int Q_SLOTS = Q_MAXQ * Q_PER;   // 15
 struct QWin {
-  uint32_t lo[Q_MAXT], hi[Q_MAXT];
-  int q[Q_MAXT];
-  int n;
+  uint32_t lo[Q_SLOTS], hi[Q_SLOTS];
+  int nq[Q_MAXQ];    // targets of quantity q
+  int base[Q_MAXQ];  // index of its first target in qa.tg
 };
 
 // CTA-level candidate staging (shared memory).
@@ -171,52 +176,55 @@ PF_D void q_agg_init(QAgg& agg) {
 }
 
 PF_D void q_classify(const QArgs& qa, const QWin& win, QAgg& agg, uint32_t i, double w,
-                     double (&acc)[Q_MAXT], bool valid) {
+                     double (&acc)[Q_SLOTS], bool valid) {
   const int lane = threadIdx.x & 31;
-  const uint32_t k0 = (valid && qa.keys[0]) ? qa.keys[0][i] : 0u;
-  const uint32_t k1 = (valid && qa.keys[1]) ? qa.keys[1][i] : 0u;
-  const uint32_t k2 = (valid && qa.keys[2]) ? qa.keys[2][i] : 0u;
+  uint32_t key[Q_MAXQ];
   uint32_t inwin = 0;
 #pragma unroll
-  for (int k = 0; k < Q_MAXT; ++k) {  // unrolled: acc[] stays in registers
-    if (k < win.n) {
-      const int q = win.q[k];
-      const uint32_t key = q == 0 ? k0 : (q == 1 ? k1 : k2);
-      if (valid && key < win.lo[k]) acc[k] += w;
-      else if (valid && key <= win.hi[k]) inwin |= 1u << k;
+  for (int q = 0; q < Q_MAXQ; ++q) {
+    key[q] = (valid && win.nq[q]) ? qa.keys[q][i] : 0u;
+#pragma unroll
+    for (int k = 0; k < Q_PER; ++k) {
+      const int s = q * Q_PER + k;
+      if (k < win.nq[q] && valid) {
+        if (key[q] < win.lo[s]) acc[s] += w;
+        else if (key[q] <= win.hi[s]) inwin |= 1u << s;
+      }
     }
   }
   uint32_t any = __reduce_or_sync(0xffffffffu, inwin);
   while (any) {
-    const int k = __ffs(any) - 1;
+    const int s = __ffs(any) - 1;
     any &= any - 1;
-    const unsigned m = __ballot_sync(0xffffffffu, (inwin >> k) & 1u);
+    const int q = s / Q_PER;
+    const int qb = q == 0 ? win.base[0] : (q == 1 ? win.base[1] : win.base[2]);  // static indices
+    const int t = qb + (s - q * Q_PER);
+    const unsigned m = __ballot_sync(0xffffffffu, (inwin >> s) & 1u);
     const int leader = __ffs(m) - 1;
-    const uint32_t key = win.q[k] == 0 ? k0 : (win.q[k] == 1 ? k1 : k2);
     // stage in the CTA buffer (shared atomics); spill straight to the global
     // list (one global atomic per warp) only if the buffer is full
     int slot = 0;
     uint32_t kpos = 0;
     if (lane == leader) {
       slot = atomicAdd(&agg.fill, __popc(m));
-      if (slot + __popc(m) <= Q_AGG) kpos = atomicAdd(&agg.cnt[k], (uint32_t)__popc(m));
-      else kpos = 0x80000000u | atomicAdd(&qa.tg[k].count, (uint32_t)__popc(m));
+      if (slot + __popc(m) <= Q_AGG) kpos = atomicAdd(&agg.cnt[t], (uint32_t)__popc(m));
+      else kpos = 0x80000000u | atomicAdd(&qa.tg[t].count, (uint32_t)__popc(m));
     }
     slot = __shfl_sync(0xffffffffu, slot, leader);
     kpos = __shfl_sync(0xffffffffu, kpos, leader);
-    if ((inwin >> k) & 1u) {
+    if ((inwin >> s) & 1u) {
       const uint32_t rank = __popc(m & ((1u << lane) - 1u));
       QCand c;
-      c.key = key;
+      c.key = q == 0 ? key[0] : (q == 1 ? key[1] : key[2]);
       c.idx = i;
       c.w = w;
       if (kpos & 0x80000000u) {
         const uint32_t pos = (kpos & 0x7FFFFFFFu) + rank;
-        if (pos < qa.cap) qa.cand[(size_t)k * qa.cap + pos] = c;
+        if (pos < qa.cap) qa.cand[(size_t)t * qa.cap + pos] = c;
         if (slot + (int)rank < Q_AGG) agg.tk[slot + rank] = 0xFF;  // reserved, unused
       } else {
         agg.c[slot + rank] = c;
-        agg.tk[slot + rank] = (uint8_t)k;
+        agg.tk[slot + rank] = (uint8_t)t;
         agg.pos[slot + rank] = kpos + rank;
       }
     }
@@ -246,24 +254,21 @@ PF_D void q_flush(const QArgs& qa, QAgg& agg) {
 }
 
 // Block-reduce the below-window sums and W, combine CTAs in fixed order.
-PF_D void q_reduce_partials(const QArgs& qa, const QWin& win, double (&acc)[Q_MAXT], double wsum) {
-  __shared__ double red[8][Q_MAXT + 1];
+PF_D void q_reduce_partials(const QArgs& qa, const QWin& win, double (&acc)[Q_SLOTS], double wsum) {
+  __shared__ double red[8][Q_SLOTS + 1];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nv = win.n + 1;
 #pragma unroll
-  for (int k = 0; k <= Q_MAXT; ++k) {  // unrolled: static indices keep acc[] in registers
-    if (k < nv) {
-      double v = k < win.n ? acc[k < Q_MAXT ? k : 0] : wsum;
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) red[warp][k] = v;
-    }
+  for (int s = 0; s <= Q_SLOTS; ++s) {
+    double v = s < Q_SLOTS ? acc[s < Q_SLOTS ? s : 0] : wsum;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][s] = v;
   }
   __syncthreads();
-  if (threadIdx.x < nv) {
+  if (threadIdx.x <= Q_SLOTS) {
     double s = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w][threadIdx.x];
-    qa.part[(size_t)blockIdx.x * (Q_MAXT + 1) + threadIdx.x] = s;
+    qa.part[(size_t)blockIdx.x * (Q_SLOTS + 1) + threadIdx.x] = s;
   }
   __threadfence();
   __syncthreads();
@@ -271,32 +276,50 @@ PF_D void q_reduce_partials(const QArgs& qa, const QWin& win, double (&acc)[Q_MA
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (threadIdx.x < nv) {
+  if (threadIdx.x <= Q_SLOTS) {
     double s = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(&qa.part[(size_t)b * (Q_MAXT + 1) + threadIdx.x]);
-    if (threadIdx.x < win.n) {
-      qa.tg[threadIdx.x].wbelow = s;
-      qa.tg[threadIdx.x].klo = win.lo[threadIdx.x];
-      qa.tg[threadIdx.x].khi = win.hi[threadIdx.x];
-    } else {
+    for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(&qa.part[(size_t)b * (Q_SLOTS + 1) + threadIdx.x]);
+    if (threadIdx.x == Q_SLOTS) {
       qa.sh->W = s;
+    } else {
+      const int q = threadIdx.x / Q_PER, k = threadIdx.x - q * Q_PER;
+      if (k < win.nq[q]) {
+        QTarget& t = qa.tg[win.base[q] + k];
+        t.wbelow = s;
+        t.klo = win.lo[threadIdx.x];
+        t.khi = win.hi[threadIdx.x];
+      }
     }
   }
   if (threadIdx.x == 0) qa.sh->counter = 0;
 }
 
 // Windows of this step (identical in every CTA: same inputs, same code).
+// Targets are grouped by quantity in qa.tg (x, sigma2, tau2 order).
 PF_D void q_make_windows(const QArgs& qa, QWin& win) {
   if (threadIdx.x == 0) {
-    win.n = qa.ntarget;
-    for (int k = 0; k < qa.ntarget; ++k) {
-      const QTarget& t = qa.tg[k];
-      win.q[k] = t.q;
-      window_of(t, qa.sh->mean[t.q], qa.sh->sd[t.q], &win.lo[k], &win.hi[k]);
+    for (int q = 0; q < Q_MAXQ; ++q) {
+      win.nq[q] = 0;
+      win.base[q] = 0;
+    }
+    for (int s = 0; s < Q_SLOTS; ++s) {
+      win.lo[s] = 0xFFFFFFFFu;
+      win.hi[s] = 0u;
+    }
+    for (int t = qa.ntarget - 1; t >= 0; --t) {
+      const int q = qa.tg[t].q;
+      win.base[q] = t;
+      ++win.nq[q];
+    }
+    for (int t = 0; t < qa.ntarget; ++t) {
+      const QTarget& tg = qa.tg[t];
+      const int s = tg.q * Q_PER + (t - win.base[tg.q]);
+      window_of(tg, qa.sh->mean[tg.q], qa.sh->sd[tg.q], &win.lo[s], &win.hi[s]);
     }
   }
   __syncthreads();
 }
+
 
 // K2 with the quantile window pass fused in: the tile's exact subtree sum
 // (as cdf_reduce_kernel) plus, for every element, the below-window weight /
@@ -315,9 +338,10 @@ cdf_reduce_q_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ c
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double M = src.mode == 0 ? *src.M : 0.0;
   const int64_t chunk = blockIdx.x;
-  double acc[Q_MAXT];
+  const QWin wr = win;  // register copy
+  double acc[Q_SLOTS];
 #pragma unroll
-  for (int k = 0; k < Q_MAXT; ++k) acc[k] = 0.0;
+  for (int k = 0; k < Q_SLOTS; ++k) acc[k] = 0.0;
   double wsum = 0.0;
   for (int r = 0; r < R; ++r) {
     const int64_t tile = chunk * R + r;
@@ -328,7 +352,7 @@ cdf_reduce_q_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ c
     for (int e = 0; e < CDF_V; ++e) {
       const double w = (double)v[e];
       wsum += w;
-      q_classify(qa, win, agg, (uint32_t)(base + e), w, acc, true);
+      q_classify(qa, wr, agg, (uint32_t)(base + e), w, acc, true);
     }
     thread_tree8<T>(v, l1, l2, g);
 #pragma unroll
@@ -349,7 +373,7 @@ cdf_reduce_q_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ c
     chunk_tot[chunk] = tt[0];
   }
   q_flush(qa, agg);
-  q_reduce_partials(qa, win, acc, wsum);
+  q_reduce_partials(qa, win, acc, wsum);  // shared copy: dynamic indices there
 }
 
 // Window pass on its own (n below one CDF tile, where K2 is not used).
@@ -362,9 +386,10 @@ q_window_kernel(WSrc src, int64_t n, const int64_t* __restrict__ fail, QArgs qa)
   q_agg_init(agg);
   q_make_windows(qa, win);
   const double M = src.mode == 0 ? *src.M : 0.0;
-  double acc[Q_MAXT];
+  const QWin wr = win;  // register copy
+  double acc[Q_SLOTS];
 #pragma unroll
-  for (int k = 0; k < Q_MAXT; ++k) acc[k] = 0.0;
+  for (int k = 0; k < Q_SLOTS; ++k) acc[k] = 0.0;
   double wsum = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t iters = (n + stride - 1) / stride;
@@ -373,10 +398,10 @@ q_window_kernel(WSrc src, int64_t n, const int64_t* __restrict__ fail, QArgs qa)
     const bool valid = i < n;
     const double w = valid ? (double)weight_of<T>(src.src[i], M, src.mode) : 0.0;
     wsum += w;
-    q_classify(qa, win, agg, (uint32_t)(valid ? i : 0), w, acc, valid);
+    q_classify(qa, wr, agg, (uint32_t)(valid ? i : 0), w, acc, valid);
   }
   q_flush(qa, agg);
-  q_reduce_partials(qa, win, acc, wsum);
+  q_reduce_partials(qa, win, acc, wsum);  // shared copy: dynamic indices there
 }
 
 // ------------------------------------------------------- resolve (side) ---

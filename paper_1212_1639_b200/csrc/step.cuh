@@ -23,6 +23,7 @@
 namespace pf {
 
 constexpr double LOG_TWO_PI = 1.8378770664093453;  // math.log(2*math.pi), models.py:20
+constexpr int STEP_SB = 4;  // slots per thread whose gathers are in flight together
 
 // Order-preserving 32-bit image of a double (float32 rounded down, sign
 // folded): the quantile keys of quantile.cuh.
@@ -239,16 +240,43 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
   double s0 = 0, sx = 0, s2x = 0, s1s = 0, s2s = 0, s1t = 0, s2t = 0;
   bool bad = false;
 
+  // Slots are taken STEP_SB per thread at a time: the resampling lookups
+  // and the record gathers of all of them are issued before any compute, so
+  // every warp keeps STEP_SB independent random-access chains in flight
+  // (the gathers are bound by random DRAM accesses, not bytes).  The
+  // gathered records wait in shared memory (per-thread slots, no sync).
+  __shared__ Rec stage[STEP_SB][256];
   const int64_t lo = blockIdx.x * a.per_block;
   const int64_t hi = lo + a.per_block < a.n ? lo + a.per_block : a.n;
-  for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
-    // ---- resample of step t-1: cut-point lookup + joint gather
-    int64_t anc = j;
-    if (a.t > 1) {
-      anc = ancestor_of<TQ>(a.lk, a.u3[j]);
-      if (a.idx_out) a.idx_out[j] = anc + 1;
+  for (int64_t jb = lo; jb < hi; jb += STEP_SB * (int64_t)blockDim.x) {
+    int64_t jj[STEP_SB], anc[STEP_SB];
+    bool ok[STEP_SB];
+#pragma unroll
+    for (int b = 0; b < STEP_SB; ++b) {
+      jj[b] = jb + b * (int64_t)blockDim.x + threadIdx.x;
+      ok[b] = jj[b] < hi;
+      anc[b] = jj[b];
     }
-    const Rec r = a.rec_in[anc];
+    // ---- resample of step t-1: cut-point lookups + joint gathers
+    if (a.t > 1) {
+      uint64_t w3[STEP_SB];
+#pragma unroll
+      for (int b = 0; b < STEP_SB; ++b) w3[b] = ok[b] ? a.u3[jj[b]] : 0ull;
+      ancestors_of<TQ, STEP_SB>(a.lk, w3, ok, anc);
+      if (a.idx_out) {
+#pragma unroll
+        for (int b = 0; b < STEP_SB; ++b)
+          if (ok[b]) a.idx_out[jj[b]] = anc[b] + 1;
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < STEP_SB; ++b)
+      if (ok[b]) stage[b][threadIdx.x] = a.rec_in[anc[b]];
+#pragma unroll 1
+  for (int b = 0; b < STEP_SB; ++b) {
+    const int64_t j = jb + b * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= hi) continue;
+    const Rec r = stage[b][threadIdx.x];
     // ---- propagate with Philox block t of stream j
     const Philox4 P = philox_block(a.seed, (uint64_t)j, (uint64_t)a.t);
     a.u3[j] = P.w[3];
@@ -313,6 +341,7 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
     s2s = fma(eds, ds, s2s);
     s1t += edt;
     s2t = fma(edt, dt, s2t);
+  }
   }
 
   // ---- CTA reduction with rescaling to the CTA max
