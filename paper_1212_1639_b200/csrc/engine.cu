@@ -9,12 +9,14 @@
 // and checks the device status word once, after the loop.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cuda_profiler_api.h>
 
 #include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -597,7 +599,19 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   }
   const int fb_grid = grid_for(n, 256, sms * 4);
 
+  // Diagnostics: PF_PROFILE_FROM_STEP=t brackets steps t..T with
+  // cudaProfilerStart/Stop (ncu --profile-from-start off) so a launch list
+  // can be taken over steady-state steps only.
+  static const int64_t prof_from = [] {
+    const char* v = getenv("PF_PROFILE_FROM_STEP");
+    return v ? (int64_t)atoll(v) : (int64_t)0;
+  }();
+  bool profiling = false;
   for (int64_t t = 1; t <= T; ++t) {
+    if (prof_from > 0 && t == prof_from && rs.resident) {
+      cudaProfilerStart();
+      profiling = true;
+    }
     const int par = (int)(t & 1);
     double* lwp = e->lw.p + (size_t)par * n;
     wsrc.src = lwp;
@@ -764,6 +778,12 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
         if (dst[k]) CK(cudaMemcpyAsync(dst[k] + off, src[k], n * sizeof(double), cudaMemcpyDeviceToHost, st));
       mark(PH_STORE);
     }
+  }
+
+  if (profiling) {
+    CK(cudaStreamSynchronize(st));
+    CK(cudaStreamSynchronize(e->side));
+    cudaProfilerStop();
   }
 
   // ---- final resample (keep_indices row T, keep_final)

@@ -1,5 +1,11 @@
-"""Short device run for ncu / diagnostics: PL at N=2^k, T steps (resident).
-Usage: python scripts/prof_run.py [log2n] [T] [track_quantiles]"""
+"""Short device run for ncu / diagnostics: PL at N=2^k, T steps.
+
+Usage: python scripts/prof_run.py [log2n] [T] [track_quantiles]
+
+One API run of T steps (engine, gamma tables), then one resident run.  With
+PF_PROFILE_FROM_STEP=t set, the resident run brackets steps t..T with
+cudaProfilerStart/Stop (ncu --profile-from-start off: steady-state steps).
+"""
 import os
 import sys
 
