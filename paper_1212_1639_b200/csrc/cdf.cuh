@@ -209,25 +209,46 @@ cdf_top_kernel(const T* __restrict__ chunk_tot, int64_t G, T* __restrict__ node,
 }
 
 // ------------------------------------------------ stratum lookup tables ---
-// For N = 2^n with n >= 21 the cut-point lookup runs on integers.  A uniform
-// u = K 2^-53 (K odd, 53 bits: unit_open) falls in stratum s = ceil(N u) =
-// (K >> B) + 1 with B = 53 - n, at offset r = K & (2^B - 1).  A particle k
-// whose CDF value lies in the same stratum (L_k = ceil(N q_k) = s) has
-// F_k = floor(q_k 2^53 - (s-1) 2^B) < 2^32, and u > q_k  <=>  r > F_k
-// exactly (r is an integer).  So the table per stratum is the cut point
-// I_s plus F of that first candidate (a sentinel when its CDF value lies
-// beyond the stratum), and the walk continues over per-particle (L, F)
-// pairs only when u lies past the first candidate.  Same answer as
-// cutpoint_indices (resampling.py:146-158), bit for bit.
-struct alignas(8) SRec {  // 8-byte aligned: one 64-bit load, one L2 request
-  int32_t first;  // 0-based I_s
-  uint32_t f;     // F of I_s if L_{I_s} == s, else 0xFFFFFFFF
-};
-struct alignas(8) PRec {
-  int32_t L;      // ceil(N q_k) (0 for a zero-mass prefix)
-  uint32_t f;
+// For N = 2^n with n >= 21 the cut-point lookup runs on integers against a
+// compact, L2-resident rank structure instead of q / the cut table.
+//
+// A uniform u = K 2^-53 (K odd, 53 bits: unit_open) falls in stratum
+// s = ceil(N u) = (K >> B) + 1, B = 53 - n, at offset r = K & (2^B - 1).  The
+// particles whose CDF value lies in stratum s (L_k = ceil(N q_k) = s) are
+// the consecutive run [I_s, I_{s+1}), I_s = first k with L_k >= s (the
+// reference's cut point, resampling.py:124-131).  For such k,
+//   u > q_k  <=>  r > F_k,   F_k = floor(q_k 2^53) - (s-1) 2^B  (exact),
+// and F is nondecreasing along the run, so cutpoint_indices (resampling.py:
+// 146-158: start at I_s, advance while u > q(k)) returns
+//   I_s + #{ k in [I_s, I_{s+1}) : r > F_k }.
+// Tables (rebuilt every step by K4 + group_build_kernel):
+//   cut  int32 [N+1]   I_s (0-based), cut[N] = N       (fallback, group build)
+//   grp  16 B per 16 strata: base = I of the group's first stratum and a
+//        96-bit unary string -- per stratum c_s ones then a zero -- so
+//        I_s and c_s come from two bit selects (overflow bit 31 of base when
+//        16 + #candidates > 96: lookups then read cut[] directly)
+//   fq   uint8 [N]     F_k >> (B-8) clamped to 255 (monotone quantisation)
+//   f32  uint32 [N]    F_k clamped to 2^32-1 (exact, read only when fq ties)
+// grp + fq are 1.06 B per particle (18 MB at 2^24) and stay in L2, so a
+// lookup costs L2 hits only; the ancestor's record gather is the one random
+// DRAM access per slot (a random read moves a 128 B DRAM atom on B200,
+// measured: scripts/micro/gather.cu).  Same answer as the reference, bit
+// for bit.
+struct alignas(16) Grp {
+  uint32_t base;  // bit 31: overflow
+  uint32_t hi;    // unary bits 64..95
+  uint64_t lo;    // unary bits 0..63
 };
 constexpr int STRATA_MIN_LOG2N = 21;
+constexpr int GRP_STRATA = 16;
+constexpr uint32_t GRP_OVERFLOW = 0x80000000u;
+
+struct RankOut {  // K4 outputs on the strata path
+  int32_t* cut;
+  uint8_t* fq;
+  uint32_t* f32;
+  int B;
+};
 
 template <typename T>
 PF_D uint32_t strata_f(T q, int64_t L, int B) {
@@ -236,6 +257,60 @@ PF_D uint32_t strata_f(T q, int64_t L, int B) {
   const double sub = (double)(L - 1) * ldexp(1.0, B);       // exact
   const double d = floor(x - sub);                          // exact (Sterbenz)
   return d >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)d;
+}
+
+// Position of the k-th (0-based) set bit of x (k < popc(x)).
+PF_HD int select32(uint32_t x, int k) {
+  int pos = 0;
+  int c = pf_popc(x & 0xFFFFu);
+  if (k >= c) { k -= c; x >>= 16; pos += 16; }
+  c = pf_popc(x & 0xFFu);
+  if (k >= c) { k -= c; x >>= 8; pos += 8; }
+  c = pf_popc(x & 0xFu);
+  if (k >= c) { k -= c; x >>= 4; pos += 4; }
+  c = pf_popc(x & 0x3u);
+  if (k >= c) { k -= c; x >>= 2; pos += 2; }
+  if (k >= (int)(x & 1u)) pos += 1;
+  return pos;
+}
+
+// Position of the k-th zero of the 96-bit unary string.
+PF_HD int grp_zero(const Grp& g, int k) {
+  const uint32_t z0 = ~(uint32_t)g.lo, z1 = ~(uint32_t)(g.lo >> 32), z2 = ~g.hi;
+  const int c0 = pf_popc(z0);
+  if (k < c0) return select32(z0, k);
+  k -= c0;
+  const int c1 = pf_popc(z1);
+  if (k < c1) return 32 + select32(z1, k);
+  return 64 + select32(z2, k - c1);
+}
+
+// One thread per group of 16 strata: unary string from the cut table.
+__global__ void __launch_bounds__(256)
+group_build_kernel(const int32_t* __restrict__ cut, int64_t ngroups, Grp* __restrict__ grp,
+                   const int64_t* __restrict__ fail) {
+  if (fail && *fail) return;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t* c = cut + g * GRP_STRATA;
+    const uint32_t base = (uint32_t)c[0];
+    uint64_t lo = ~0ull;
+    uint32_t hi = ~0u;
+    bool over = false;
+    for (int i = 0; i < GRP_STRATA; ++i) {
+      const uint32_t z = (uint32_t)(c[i + 1] - (int32_t)base) + (uint32_t)i;  // i-th zero
+      if (z >= 96u) {
+        over = true;
+        break;
+      }
+      if (z < 64u) lo &= ~(1ull << z); else hi &= ~(1u << (z - 64u));
+    }
+    Grp r;
+    r.base = base | (over ? GRP_OVERFLOW : 0u);
+    r.hi = hi;
+    r.lo = lo;
+    grp[g] = r;
+  }
 }
 
 // ------------------------------------------------------------------ K4 ---
@@ -248,8 +323,7 @@ cdf_expand_kernel(WSrc src, int64_t n, int R, const T* __restrict__ tile_tot,
                   const T* __restrict__ node, const T* __restrict__ carry,
                   const T* __restrict__ total_p, T* __restrict__ q_out,
                   int32_t* __restrict__ cut_out, const int64_t* __restrict__ fail,
-                  SRec* __restrict__ srec_out = nullptr, PRec* __restrict__ pf_out = nullptr,
-                  int B = 0) {
+                  RankOut ro = RankOut()) {
   if (fail && *fail) return;
   __shared__ T wt[CDF_THREADS / 32];
   __shared__ T wmax[CDF_THREADS / 32];
@@ -361,30 +435,30 @@ cdf_expand_kernel(WSrc src, int64_t n, int R, const T* __restrict__ tile_tot,
     // finalize and scatter the cut table
     T qv[CDF_V];
     int64_t Lprev = (int64_t)ceil(clip01(pre) * nf);
+    uint64_t fqw = 0;
+    uint32_t fx[CDF_V];
 #pragma unroll
     for (int i = 0; i < CDF_V; ++i) {
       T qi = clip01(fmax(pre, run[i]));
       if (base + i == n - 1) qi = (T)1;
       qv[i] = qi;
       const int64_t L = (int64_t)ceil(qi * nf);
+      int32_t* ct = STRATA ? ro.cut : cut_out;
+      for (int64_t kk = Lprev; kk < L; ++kk) ct[kk] = (int32_t)(base + i);
       if (STRATA) {
-        const uint32_t f = strata_f<T>(qi, L, B);
-        PRec pr;
-        pr.L = (int32_t)L;
-        pr.f = f;
-        pf_out[base + i] = pr;
-        for (int64_t kk = Lprev; kk < L; ++kk) {
-          SRec sr;
-          sr.first = (int32_t)(base + i);
-          sr.f = (kk == L - 1) ? f : 0xFFFFFFFFu;
-          srec_out[kk] = sr;
-        }
-      } else {
-        for (int64_t kk = Lprev; kk < L; ++kk) cut_out[kk] = (int32_t)(base + i);
+        const uint32_t f = strata_f<T>(qi, L, ro.B);
+        fx[i] = f;
+        const uint32_t h = f >> (ro.B - 8);
+        fqw |= (uint64_t)(h > 255u ? 255u : h) << (8 * i);
       }
       Lprev = L > Lprev ? L : Lprev;
     }
-    if (!STRATA) {
+    if (STRATA) {
+      *reinterpret_cast<uint64_t*>(ro.fq + base) = fqw;
+      uint4* fp = reinterpret_cast<uint4*>(ro.f32 + base);
+      fp[0] = make_uint4(fx[0], fx[1], fx[2], fx[3]);
+      fp[1] = make_uint4(fx[4], fx[5], fx[6], fx[7]);
+    } else {
 #pragma unroll
       for (int i = 0; i < CDF_V; ++i) q_out[base + i] = qv[i];
     }
@@ -462,77 +536,149 @@ PF_D int64_t cutpoint_lookup(const T* __restrict__ q, const int32_t* __restrict_
   return k;
 }
 
-// The resampling table of one step: (q, cut) for small n, strata tables
-// for n >= 2^21 (see SRec).  ancestor_of() takes the raw Philox word whose
-// unit_open() is the resampling uniform.
+// The resampling table of one step: (q, cut) for small n, the rank
+// structure for n >= 2^21 (see Grp).  ancestor_of() takes the raw Philox
+// word whose unit_open() is the resampling uniform.
 template <typename TQ>
 struct Lookup {
   const TQ* q;
   const int32_t* cut;
-  const SRec* srec;  // non-null: strata path
-  const PRec* pf;
+  const Grp* grp;       // non-null: strata path
+  const uint8_t* fq;
+  const uint32_t* f32;
   int B;
   int64_t n;
 };
 
+// L2 eviction-priority hints: the rank tables are re-read by every slot of
+// the step (keep them), the ancestor records are touched ~once (stream them).
+PF_D uint64_t l2_policy_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+PF_D Grp ld_grp(const Grp* p, uint64_t pol) {
+  uint32_t a, b, c, d;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(p), "l"(pol));
+  Grp g;
+  g.base = a;
+  g.hi = b;
+  g.lo = (uint64_t)c | ((uint64_t)d << 32);
+  return g;
+}
+PF_D uint64_t ld_fq8(const uint8_t* p, uint64_t pol) {  // 8-byte aligned
+  uint64_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+}
+PF_D uint32_t ld_fq(const uint8_t* p, uint64_t pol) {
+  uint16_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+  return (uint32_t)v;
+}
+
+// Run start I_s and length c_s of stratum s0 (0-based).
+template <typename TQ>
+PF_D void stratum_run(const Lookup<TQ>& L, const Grp& g, uint64_t s0, int64_t& first, int& cnt) {
+  if (g.base & GRP_OVERFLOW) {
+    first = L.cut[s0];
+    cnt = (int)(L.cut[s0 + 1] - first);
+    return;
+  }
+  const int i = (int)(s0 & (GRP_STRATA - 1));
+  const int pz = grp_zero(g, i);
+  const int st = i ? grp_zero(g, i - 1) + 1 : 0;
+  first = (int64_t)g.base + st - i;
+  cnt = pz - st;
+}
+
+// #{k in [first, first+cnt) : r > F_k}, F nondecreasing along the run.
+template <typename TQ>
+PF_D int64_t run_count(const Lookup<TQ>& L, int64_t first, int cnt, uint32_t r, uint64_t pol) {
+  const uint32_t rh = r >> (L.B - 8);
+  int64_t k = first;
+  for (int m = 0; m < cnt; ++m, ++k) {
+    const uint32_t h = ld_fq(L.fq + k, pol);
+    if (rh < h) break;
+    if (rh == h && r <= __ldg(L.f32 + k)) break;
+  }
+  return k;
+}
+
+// Same count from the two aligned 8-byte words of fq covering bytes
+// first .. first+7 (fq is padded by 16 bytes): the bytes below r's are a
+// prefix of the run (fq is nondecreasing along it), counted with one SIMD
+// byte compare; an equal byte, or a run longer than 8, takes run_count.
+template <typename TQ>
+PF_D int64_t run_count_win(const Lookup<TQ>& L, int64_t first, int cnt, uint32_t r, uint64_t w0, uint64_t w1,
+                           uint64_t pol) {
+  if (cnt == 0) return first;
+  const uint32_t rh = r >> (L.B - 8);
+  const int sh = (int)(first & 7) * 8;
+  const uint64_t win = sh ? ((w0 >> sh) | (w1 << (64 - sh))) : w0;
+  const int m = cnt < 8 ? cnt : 8;
+  const uint32_t rb = rh * 0x01010101u;
+  const uint64_t cm = (uint64_t)__vcmpltu4((uint32_t)win, rb) |
+                      ((uint64_t)__vcmpltu4((uint32_t)(win >> 32), rb) << 32);
+  const uint64_t mask = m == 8 ? ~0ull : ((1ull << (8 * m)) - 1ull);
+  const int k = __popcll(cm & mask) >> 3;
+  if (k < m) {
+    if (((win >> (8 * k)) & 0xFFu) != rh) return first + k;
+  } else if (cnt <= 8) {
+    return first + cnt;
+  }
+  return run_count(L, first + k, cnt - k, r, pol);
+}
+
 template <typename TQ>
 PF_D int64_t ancestor_of(const Lookup<TQ>& L, uint64_t w3) {
-  if (L.srec) {
+  if (L.grp) {
+    const uint64_t pol = l2_policy_last();
     const uint64_t K = ((w3 >> 12) << 1) | 1ull;  // u = K 2^-53
     const uint64_t s0 = K >> L.B;                 // stratum - 1
     const uint32_t r = (uint32_t)(K & ((1ull << L.B) - 1ull));
-    const SRec R = L.srec[s0];
-    int64_t k = R.first;
-    if (r > R.f) {
-      ++k;
-      const int32_t s = (int32_t)s0 + 1;
-      for (;;) {
-        const PRec p = L.pf[k];
-        if (p.L != s || r <= p.f) break;
-        ++k;
-      }
-    }
-    return k;
+    const Grp g = ld_grp(L.grp + (s0 / GRP_STRATA), pol);
+    int64_t first;
+    int cnt;
+    stratum_run(L, g, s0, first, cnt);
+    return run_count(L, first, cnt, r, pol);
   }
   return cutpoint_lookup<TQ>(L.q, L.cut, L.n, unit_open(w3));
 }
 
-// SB lookups at once: all stratum-record loads are issued before any is
-// consumed (memory-level parallelism), then the rare walks.
+// SB lookups at once: two rounds of independent L2 loads (all groups, then
+// all fq windows), then the rare exact / long-run walks.
 template <typename TQ, int SB>
 PF_D void ancestors_of(const Lookup<TQ>& L, const uint64_t (&w3)[SB], const bool (&ok)[SB],
                        int64_t (&anc)[SB]) {
-  if (L.srec) {
+  if (L.grp) {
+    const uint64_t pol = l2_policy_last();
     uint32_t r[SB];
     uint64_t s0[SB];
-    SRec R[SB];
+    Grp G[SB];
 #pragma unroll
     for (int b = 0; b < SB; ++b) {
       const uint64_t K = ((w3[b] >> 12) << 1) | 1ull;
-      s0[b] = K >> L.B;
+      s0[b] = ok[b] ? (K >> L.B) : 0;
       r[b] = (uint32_t)(K & ((1ull << L.B) - 1ull));
     }
 #pragma unroll
+    for (int b = 0; b < SB; ++b) G[b] = ld_grp(L.grp + (s0[b] / GRP_STRATA), pol);
+    int64_t first[SB];
+    int cnt[SB];
+#pragma unroll
+    for (int b = 0; b < SB; ++b) stratum_run(L, G[b], s0[b], first[b], cnt[b]);
+    uint64_t w0[SB], w1[SB];
+#pragma unroll
     for (int b = 0; b < SB; ++b) {
-      if (ok[b]) {
-        R[b] = L.srec[s0[b]];
-      } else {
-        R[b].first = 0;
-        R[b].f = 0xFFFFFFFFu;
-      }
+      const uint8_t* p = L.fq + (first[b] & ~7ll);
+      w0[b] = ld_fq8(p, pol);
+      w1[b] = ld_fq8(p + 8, pol);
     }
 #pragma unroll
     for (int b = 0; b < SB; ++b) {
-      int64_t k = R[b].first;
-      if (r[b] > R[b].f) {
-        ++k;
-        const int32_t s = (int32_t)s0[b] + 1;
-        for (;;) {
-          const PRec p = L.pf[k];
-          if (p.L != s || r[b] <= p.f) break;
-          ++k;
-        }
-      }
+      const int64_t k = run_count_win(L, first[b], cnt[b], r[b], w0[b], w1[b], pol);
       if (ok[b]) anc[b] = k;
     }
     return;

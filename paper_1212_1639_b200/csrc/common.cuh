@@ -27,6 +27,13 @@ enum Code : int32_t {
   NOT_IMPLEMENTED = 7,
 };
 
+PF_HD int pf_popc(uint32_t x) {
+#ifdef __CUDA_ARCH__
+  return __popc(x);
+#else
+  return __builtin_popcount(x);
+#endif
+}
 PF_HD bool is_pow2(int64_t n) { return n >= 1 && (n & (n - 1)) == 0; }
 PF_HD int ilog2(int64_t n) {
   int k = 0;

@@ -185,9 +185,9 @@ struct CdfBufs {
 };
 
 struct StrataOut {
-  SRec* srec = nullptr;
-  PRec* pf = nullptr;
-  int B = 0;
+  RankOut ro{nullptr, nullptr, nullptr, 0};
+  Grp* grp = nullptr;
+  bool on = false;
 };
 
 template <typename T>
@@ -229,10 +229,13 @@ int launch_cdf_tail(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t
   }
   cdf_top_kernel<T><<<1, 1024, smem, st>>>(ct, p.chunks, nd, cr, total, fail, step);
   LAUNCHED();
-  if (so.srec)
+  if (so.on) {
     cdf_expand_kernel<T, true><<<(int)p.chunks, CDF_THREADS, 0, st>>>(src, n, p.R, tt, nd, cr, total, q, cut,
-                                                                    fail, so.srec, so.pf, so.B);
-  else
+                                                                    fail, so.ro);
+    LAUNCHED();
+    const int64_t ng = n / GRP_STRATA;
+    group_build_kernel<<<grid_for(ng, 256, 148 * 8), 256, 0, st>>>(so.ro.cut, ng, so.grp, fail);
+  } else
     cdf_expand_kernel<T, false><<<(int)p.chunks, CDF_THREADS, 0, st>>>(src, n, p.R, tt, nd, cr, total, q, cut,
                                                                      fail);
   LAUNCHED();
@@ -253,8 +256,9 @@ struct pf_engine {
   DevBuf<uint64_t> u3;
   DevBuf<unsigned char> q;
   DevBuf<int32_t> cut;
-  DevBuf<SRec> srec;      // strata tables (n >= 2^21) replace q / cut
-  DevBuf<PRec> pfr;
+  DevBuf<Grp> grp;        // rank tables (n >= 2^21) replace q (cut is kept)
+  DevBuf<uint8_t> fq;
+  DevBuf<uint32_t> f32;
   bool strata = false;
   DevBuf<int64_t> idx;
   DevBuf<uint32_t> keys;  // quantile keys [2 parities][3 quantities][n]
@@ -557,24 +561,28 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   mark(PH_INIT);
 
   const int sms = sm_count();
-  int step_grid = (int)((n + 255) / 256);
-  if (step_grid > sms * 8) step_grid = sms * 8;
-  int64_t per_block = (n + step_grid - 1) / step_grid;
-  per_block = (per_block + 1023) / 1024 * 1024;  // STEP_SB x 256 slots per batch
-  step_grid = (int)((n + per_block - 1) / per_block);
-
-  // shared-memory copies of the step's gamma table(s)
+  // shared-memory copies of the step's gamma table(s), then the double-
+  // buffered record stage of the cp.async gather pipeline
   const bool share_tab = LS && LT && e->tab_s == e->tab_t && c.gamma_method == 0;
-  const size_t step_smem = c.gamma_method == 0
-      ? (size_t)((LS ? 1 : 0) + (LT && !share_tab ? 1 : 0)) * GT_TABLE_DOUBLES * sizeof(double) : 0;
+  const int ntab = c.gamma_method == 0 ? (LS ? 1 : 0) + (LT && !share_tab ? 1 : 0) : 0;
+  const size_t stage_off = (size_t)ntab * GT_TABLE_DOUBLES;
+  const size_t step_smem = stage_off * sizeof(double) + (size_t)2 * STEP_SB * 256 * sizeof(Rec);
+  static int step_occ[8] = {0};
   {
     static bool attr[8] = {false};
     if (!attr[MODE]) {
       CK(cudaFuncSetAttribute(step_kernel<MODE, TQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              2 * GT_TABLE_DOUBLES * (int)sizeof(double)));
+                              (int)(2 * GT_TABLE_DOUBLES * sizeof(double) + 2 * STEP_SB * 256 * sizeof(Rec))));
       attr[MODE] = true;
     }
   }
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, step_kernel<MODE, TQ>, 256, step_smem));
+  (void)step_occ;
+  if (occ < 1) occ = 1;
+  // persistent grid: one wave of resident CTAs, batches dealt round robin
+  const int64_t nbatches = (n + STEP_SB * 256 - 1) / (STEP_SB * 256);
+  const int step_grid = (int)std::min<int64_t>(nbatches, (int64_t)sms * occ);
 
   int cur = 0;
   WSrc wsrc;
@@ -586,16 +594,21 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   Lookup<TQ> lk;
   lk.q = qv;
   lk.cut = e->cut.p;
-  lk.srec = nullptr;
-  lk.pf = nullptr;
+  lk.grp = nullptr;
+  lk.fq = nullptr;
+  lk.f32 = nullptr;
   lk.B = 53 - ilog2(n);
   lk.n = n;
   if (e->strata) {
-    so.srec = e->srec.p;
-    so.pf = e->pfr.p;
-    so.B = lk.B;
-    lk.srec = e->srec.p;
-    lk.pf = e->pfr.p;
+    so.on = true;
+    so.ro.cut = e->cut.p;
+    so.ro.fq = e->fq.p;
+    so.ro.f32 = e->f32.p;
+    so.ro.B = lk.B;
+    so.grp = e->grp.p;
+    lk.grp = e->grp.p;
+    lk.fq = e->fq.p;
+    lk.f32 = e->f32.p;
   }
   const int fb_grid = grid_for(n, 256, sms * 4);
 
@@ -653,7 +666,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     a.out.t_mean = e->o_tm.p;
     a.out.t_sd = e->o_tsd.p;
     a.fail = e->fail.p;
-    a.per_block = per_block;
+    a.stage_off = (int64_t)stage_off;
     if (rs.resident) {
       cudaEvent_t b0, b1;
       cudaEventCreate(&b0);
@@ -1001,7 +1014,11 @@ int pf_engine_create(const pf_config* cfg, pf_engine** out) {
     return bail(err);
   e->strata = ilog2(n) >= STRATA_MIN_LOG2N;
   if (e->strata) {
-    if ((err = e->srec.ensure(n)) || (err = e->pfr.ensure(n))) return bail(err);
+    if ((err = e->grp.ensure(n / GRP_STRATA)) || (err = e->fq.ensure(n + 16)) || (err = e->f32.ensure(n)) ||
+        (err = e->cut.ensure(n + 1)))
+      return bail(err);
+    const int32_t nn = (int32_t)n;  // cut[N] = N: end of the last stratum's run
+    if ((err = cudaMemcpy(e->cut.p + n, &nn, sizeof(nn), cudaMemcpyHostToDevice))) return bail(err);
   } else {
     if ((err = e->q.ensure(n * (e->single ? 4 : 8))) || (err = e->cut.ensure(n))) return bail(err);
   }
@@ -1073,8 +1090,9 @@ int pf_engine_destroy(pf_engine* e) {
   e->u3.release();
   e->q.release();
   e->cut.release();
-  e->srec.release();
-  e->pfr.release();
+  e->grp.release();
+  e->fq.release();
+  e->f32.release();
   e->idx.release();
   e->partials.release();
   e->sc.release();

@@ -197,7 +197,7 @@ struct StepArgs {
   Scalars* sc;
   StepOut out;
   int64_t* fail;
-  int64_t per_block;     // particles per CTA (multiple of blockDim)
+  int64_t stage_off;     // offset (doubles) of the record stage in dynamic smem
 };
 
 PF_D double warp_sum(double v) {
@@ -240,28 +240,31 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
   double s0 = 0, sx = 0, s2x = 0, s1s = 0, s2s = 0, s1t = 0, s2t = 0;
   bool bad = false;
 
-  // Slots are taken STEP_SB per thread at a time: the resampling lookups
-  // and the record gathers of all of them are issued before any compute, so
-  // every warp keeps STEP_SB independent random-access chains in flight
-  // (the gathers are bound by random DRAM accesses, not bytes).  The
-  // gathered records wait in shared memory (per-thread slots, no sync).
-  __shared__ Rec stage[STEP_SB][256];
-  const int64_t lo = blockIdx.x * a.per_block;
-  const int64_t hi = lo + a.per_block < a.n ? lo + a.per_block : a.n;
-  for (int64_t jb = lo; jb < hi; jb += STEP_SB * (int64_t)blockDim.x) {
+  // Software pipeline over batches of STEP_SB x 256 slots (batches are
+  // dealt to CTAs round robin).  Iteration i: resolve the ancestors of
+  // batch i+1 (cut-point lookups: L2-resident tables) and start their
+  // 32-byte record gathers with cp.async into the other half of a double
+  // buffer; then wait for batch i's gathers (issued one iteration earlier)
+  // and run its compute -- Philox, ndtri, the two inverse-gamma draws,
+  // propagation, log-weight, moments -- while batch i+1's random DRAM reads
+  // are in flight.  Each thread only reads back its own staged records.
+  Rec* stage = reinterpret_cast<Rec*>(pf_gtab + a.stage_off);  // [2][STEP_SB][blockDim]
+  const int nth = blockDim.x;
+  const int64_t batch = (int64_t)STEP_SB * nth;
+  const int64_t nbatches = (a.n + batch - 1) / batch;
+  auto issue = [&](int64_t bi, int buf) {
     int64_t jj[STEP_SB], anc[STEP_SB];
     bool ok[STEP_SB];
 #pragma unroll
     for (int b = 0; b < STEP_SB; ++b) {
-      jj[b] = jb + b * (int64_t)blockDim.x + threadIdx.x;
-      ok[b] = jj[b] < hi;
+      jj[b] = bi * batch + b * (int64_t)nth + threadIdx.x;
+      ok[b] = jj[b] < a.n;
       anc[b] = jj[b];
     }
-    // ---- resample of step t-1: cut-point lookups + joint gathers
     if (a.t > 1) {
       uint64_t w3[STEP_SB];
 #pragma unroll
-      for (int b = 0; b < STEP_SB; ++b) w3[b] = ok[b] ? a.u3[jj[b]] : 0ull;
+      for (int b = 0; b < STEP_SB; ++b) w3[b] = ok[b] ? __ldcs(a.u3 + jj[b]) : 0ull;
       ancestors_of<TQ, STEP_SB>(a.lk, w3, ok, anc);
       if (a.idx_out) {
 #pragma unroll
@@ -270,13 +273,27 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
       }
     }
 #pragma unroll
-    for (int b = 0; b < STEP_SB; ++b)
-      if (ok[b]) stage[b][threadIdx.x] = a.rec_in[anc[b]];
+    for (int b = 0; b < STEP_SB; ++b) {
+      if (!ok[b]) continue;
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(stage + ((size_t)buf * STEP_SB + b) * nth + threadIdx.x);
+      const Rec* src = a.rec_in + anc[b];
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16), "l"(reinterpret_cast<const char*>(src) + 16));
+    }
+    asm volatile("cp.async.commit_group;");
+  };
+  int cur = 0;
+  int64_t bi = blockIdx.x;
+  if (bi < nbatches) issue(bi, 0);
+  for (; bi < nbatches; bi += gridDim.x) {
+    if (bi + gridDim.x < nbatches) issue(bi + gridDim.x, cur ^ 1);
+    else asm volatile("cp.async.commit_group;");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
 #pragma unroll 1
   for (int b = 0; b < STEP_SB; ++b) {
-    const int64_t j = jb + b * (int64_t)blockDim.x + threadIdx.x;
-    if (j >= hi) continue;
-    const Rec r = stage[b][threadIdx.x];
+    const int64_t j = bi * batch + b * (int64_t)nth + threadIdx.x;
+    if (j >= a.n) continue;
+    const Rec r = stage[((size_t)cur * STEP_SB + b) * nth + threadIdx.x];
     // ---- propagate with Philox block t of stream j
     const Philox4 P = philox_block(a.seed, (uint64_t)j, (uint64_t)a.t);
     a.u3[j] = P.w[3];
@@ -342,7 +359,9 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
     s1t += edt;
     s2t = fma(edt, dt, s2t);
   }
+    cur ^= 1;
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
 
   // ---- CTA reduction with rescaling to the CTA max
   __shared__ double red[8][8];

@@ -71,6 +71,58 @@ __global__ void __launch_bounds__(256) dep_pair(const uint32_t* __restrict__ idx
   out[tid] = (double)acc;
 }
 
+
+// 32-byte random reads with an explicit PTX load flavour (cache operator /
+// L1 policy): 0 = ld.global (default), 1 = ld.global.cg (L2 only),
+// 2 = ld.global.cs (streaming), 3 = ld.global.L1::no_allocate,
+// 4 = ld.global.nc (texture path), 5 = ld.global.lu, 6 = ld.global.cv
+template <int FLAVOUR, int ILP>
+__global__ void __launch_bounds__(256) rand32_flavour(const uint4* __restrict__ tab, uint64_t n32, double* out,
+                                                      int rounds) {
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t acc = 0;
+  for (int it = 0; it < rounds; ++it) {
+    uint32_t v[ILP][8];
+#pragma unroll
+    for (int k = 0; k < ILP; ++k) {
+      const uint64_t e = mix(tid * 0x9E3779B97F4A7C15ull + it * ILP + k) % n32;
+      const uint4* p = tab + 2 * e;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t* d = &v[k][4 * h];
+        const uint4* q = p + h;
+        if (FLAVOUR == 0)
+          asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]) : "l"(q));
+        else if (FLAVOUR == 1)
+          asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]) : "l"(q));
+        else if (FLAVOUR == 2)
+          asm volatile("ld.global.cs.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]) : "l"(q));
+        else if (FLAVOUR == 3)
+          asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]) : "l"(q));
+        else if (FLAVOUR == 4)
+          asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]) : "l"(q));
+        else if (FLAVOUR == 5)
+          asm volatile("ld.global.lu.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]) : "l"(q));
+        else
+          asm volatile("ld.global.cv.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]) : "l"(q));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < ILP; ++k) acc += v[k][0] ^ v[k][7];
+  }
+  out[tid] = (double)acc;
+}
+
+// Random 32-byte writes (scatter), for the write-side cost.
+__global__ void __launch_bounds__(256) rand32_write(uint4* tab, uint64_t n32, int rounds) {
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  for (int it = 0; it < rounds * 4; ++it) {
+    const uint64_t e = mix(tid * 0x9E3779B97F4A7C15ull + it) % n32;
+    tab[2 * e] = make_uint4((uint32_t)tid, it, 1, 2);
+    tab[2 * e + 1] = make_uint4(3, 4, 5, 6);
+  }
+}
+
 __global__ void fill(uint32_t* p, uint64_t n) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     p[i] = (uint32_t)mix(i);
@@ -121,6 +173,12 @@ int main(int argc, char** argv) {
          [&] { dep_pair<4><<<blocks, threads>>>((const uint32_t*)tab, tab, n, out, rounds); });
   timeit("dep_pair 8B->32B ilp8", th * 8, 40,
          [&] { dep_pair<8><<<blocks, threads>>>((const uint32_t*)tab, tab, n, out, rounds); });
+  const uint64_t n32 = bytes / 32;
+#define FL(F)                                                                                      \
+  timeit("rand32 flavour " #F " ilp8", th * 8, 32,                                                \
+         [&] { rand32_flavour<F, 8><<<blocks, threads>>>(tab, n32, out, rounds); })
+  FL(0); FL(1); FL(2); FL(3); FL(4); FL(5); FL(6);
+  timeit("rand32 write", th * 4, 32, [&] { rand32_write<<<blocks, threads>>>(tab, n32, rounds); });
   cudaError_t e = cudaDeviceSynchronize();
   printf("status %s\n", cudaGetErrorString(e));
   return 0;
