@@ -5,7 +5,7 @@ ARCH ?= -gencode arch=compute_100a,code=sm_100a
 NVFLAGS = -O3 -std=c++17 $(ARCH) -lineinfo -fmad=false -Xcompiler -fPIC -Xptxas -v \
           --expt-relaxed-constexpr
 SRC = paper_1212_1639_b200/csrc/engine.cu
-HDR = $(wildcard paper_1212_1639_b200/csrc/*.cuh) include/parsmc_b200.h
+HDR = $(wildcard paper_1212_1639_b200/csrc/*.cuh) $(wildcard paper_1212_1639_b200/csrc/*.inc) include/parsmc_b200.h
 LIB = paper_1212_1639_b200/libparsmc_b200.so
 
 all: $(LIB)

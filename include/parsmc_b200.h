@@ -160,6 +160,9 @@ int pf_uniforms_at(uint64_t seed, const uint64_t* stream_ids,
                    const uint64_t* counters, int64_t n, double* u_out);
 /* scipy.special.ndtri as used at rng.py:223-224. */
 int pf_ndtri(const double* u, int64_t n, double* out);
+/* The hot-path normal draw: the piecewise u-space table of ndtri that the
+ * draws kernel evaluates (replaces the same ndtri call, rng.py:223-224). */
+int pf_ndtri_table(const double* u, int64_t n, double* out);
 /* scipy.special.gammaincinv(a, u) as used at rng.py:226-229.  method 0 uses
  * the per-step table (hot path), 1 the accurate Halley solver. */
 int pf_gammaincinv(double a, const double* u, int64_t n, int32_t method, double* out);

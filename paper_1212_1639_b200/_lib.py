@@ -93,6 +93,7 @@ SIGNATURES = {
     "pf_philox4x64": (C.c_int, [_u64p, _u64p, C.c_int64, _u64p]),
     "pf_uniforms_at": (C.c_int, [C.c_uint64, _u64p, _u64p, C.c_int64, _dp]),
     "pf_ndtri": (C.c_int, [_dp, C.c_int64, _dp]),
+    "pf_ndtri_table": (C.c_int, [_dp, C.c_int64, _dp]),
     "pf_gammaincinv": (C.c_int, [C.c_double, _dp, C.c_int64, C.c_int32, _dp]),
     "pf_tree_cdf": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, _dp]),
     "pf_adder_tree": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),

@@ -223,24 +223,24 @@ cdf_top_kernel(const T* __restrict__ chunk_tot, int64_t G, T* __restrict__ node,
 //   I_s + #{ k in [I_s, I_{s+1}) : r > F_k }.
 // Tables (rebuilt every step by K4 + group_build_kernel):
 //   cut  int32 [N+1]   I_s (0-based), cut[N] = N       (fallback, group build)
-//   grp  16 B per 16 strata: base = I of the group's first stratum and a
-//        96-bit unary string -- per stratum c_s ones then a zero -- so
-//        I_s and c_s come from two bit selects (overflow bit 31 of base when
-//        16 + #candidates > 96: lookups then read cut[] directly)
+//   grp  16 B per 8 strata: base = I of the group's first stratum and the 8
+//        cumulative run ends (bytes, relative to base), so I_s and c_s are two
+//        byte extracts (overflow bit 31 of base when the group's 8 runs hold
+//        more than 255 particles: lookups then read cut[] directly)
 //   fq   uint8 [N]     F_k >> (B-8) clamped to 255 (monotone quantisation)
 //   f32  uint32 [N]    F_k clamped to 2^32-1 (exact, read only when fq ties)
-// grp + fq are 1.06 B per particle (18 MB at 2^24) and stay in L2, so a
-// lookup costs L2 hits only; the ancestor's record gather is the one random
-// DRAM access per slot (a random read moves a 128 B DRAM atom on B200,
-// measured: scripts/micro/gather.cu).  Same answer as the reference, bit
-// for bit.
+// grp + fq are 3 B per particle (48 MB at 2^24) and are read with an L2
+// evict_last policy, so a lookup is L2 hits; the ancestor's record gather is
+// the one random DRAM access per slot (a random read moves a 128 B DRAM atom
+// on B200, measured: scripts/micro/gather.cu).  Same answer as the
+// reference, bit for bit.
 struct alignas(16) Grp {
   uint32_t base;  // bit 31: overflow
-  uint32_t hi;    // unary bits 64..95
-  uint64_t lo;    // unary bits 0..63
+  uint32_t pad;
+  uint64_t cum;   // byte i: I_{first stratum + i + 1} - base
 };
 constexpr int STRATA_MIN_LOG2N = 21;
-constexpr int GRP_STRATA = 16;
+constexpr int GRP_STRATA = 8;
 constexpr uint32_t GRP_OVERFLOW = 0x80000000u;
 
 struct RankOut {  // K4 outputs on the strata path
@@ -259,33 +259,7 @@ PF_D uint32_t strata_f(T q, int64_t L, int B) {
   return d >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)d;
 }
 
-// Position of the k-th (0-based) set bit of x (k < popc(x)).
-PF_HD int select32(uint32_t x, int k) {
-  int pos = 0;
-  int c = pf_popc(x & 0xFFFFu);
-  if (k >= c) { k -= c; x >>= 16; pos += 16; }
-  c = pf_popc(x & 0xFFu);
-  if (k >= c) { k -= c; x >>= 8; pos += 8; }
-  c = pf_popc(x & 0xFu);
-  if (k >= c) { k -= c; x >>= 4; pos += 4; }
-  c = pf_popc(x & 0x3u);
-  if (k >= c) { k -= c; x >>= 2; pos += 2; }
-  if (k >= (int)(x & 1u)) pos += 1;
-  return pos;
-}
-
-// Position of the k-th zero of the 96-bit unary string.
-PF_HD int grp_zero(const Grp& g, int k) {
-  const uint32_t z0 = ~(uint32_t)g.lo, z1 = ~(uint32_t)(g.lo >> 32), z2 = ~g.hi;
-  const int c0 = pf_popc(z0);
-  if (k < c0) return select32(z0, k);
-  k -= c0;
-  const int c1 = pf_popc(z1);
-  if (k < c1) return 32 + select32(z1, k);
-  return 64 + select32(z2, k - c1);
-}
-
-// One thread per group of 16 strata: unary string from the cut table.
+// One thread per group of 8 strata: cumulative run ends from the cut table.
 __global__ void __launch_bounds__(256)
 group_build_kernel(const int32_t* __restrict__ cut, int64_t ngroups, Grp* __restrict__ grp,
                    const int64_t* __restrict__ fail) {
@@ -294,21 +268,18 @@ group_build_kernel(const int32_t* __restrict__ cut, int64_t ngroups, Grp* __rest
        g += (int64_t)gridDim.x * blockDim.x) {
     const int32_t* c = cut + g * GRP_STRATA;
     const uint32_t base = (uint32_t)c[0];
-    uint64_t lo = ~0ull;
-    uint32_t hi = ~0u;
+    uint64_t cum = 0;
     bool over = false;
+#pragma unroll
     for (int i = 0; i < GRP_STRATA; ++i) {
-      const uint32_t z = (uint32_t)(c[i + 1] - (int32_t)base) + (uint32_t)i;  // i-th zero
-      if (z >= 96u) {
-        over = true;
-        break;
-      }
-      if (z < 64u) lo &= ~(1ull << z); else hi &= ~(1u << (z - 64u));
+      const uint32_t e = (uint32_t)(c[i + 1] - (int32_t)base);
+      over |= e > 255u;
+      cum |= (uint64_t)(e & 255u) << (8 * i);
     }
     Grp r;
     r.base = base | (over ? GRP_OVERFLOW : 0u);
-    r.hi = hi;
-    r.lo = lo;
+    r.pad = 0;
+    r.cum = cum;
     grp[g] = r;
   }
 }
@@ -563,8 +534,8 @@ PF_D Grp ld_grp(const Grp* p, uint64_t pol) {
                : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(p), "l"(pol));
   Grp g;
   g.base = a;
-  g.hi = b;
-  g.lo = (uint64_t)c | ((uint64_t)d << 32);
+  g.pad = b;
+  g.cum = (uint64_t)c | ((uint64_t)d << 32);
   return g;
 }
 PF_D uint64_t ld_fq8(const uint8_t* p, uint64_t pol) {  // 8-byte aligned
@@ -586,11 +557,11 @@ PF_D void stratum_run(const Lookup<TQ>& L, const Grp& g, uint64_t s0, int64_t& f
     cnt = (int)(L.cut[s0 + 1] - first);
     return;
   }
-  const int i = (int)(s0 & (GRP_STRATA - 1));
-  const int pz = grp_zero(g, i);
-  const int st = i ? grp_zero(g, i - 1) + 1 : 0;
-  first = (int64_t)g.base + st - i;
-  cnt = pz - st;
+  const int sh = 8 * (int)(s0 & (GRP_STRATA - 1));
+  const uint32_t end = (uint32_t)(g.cum >> sh) & 255u;
+  const uint32_t beg = sh ? (uint32_t)(g.cum >> (sh - 8)) & 255u : 0u;
+  first = (int64_t)g.base + beg;
+  cnt = (int)(end - beg);
 }
 
 // #{k in [first, first+cnt) : r > F_k}, F nondecreasing along the run.

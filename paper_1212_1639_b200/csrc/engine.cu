@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "../../include/parsmc_b200.h"
+#include "ndtri_table.inc"
 #include "quantile.cuh"
 
 using namespace pf;
@@ -169,6 +170,43 @@ int weighted_quantiles_dev(QuantileScratch& s, const double* vals, WSrc w, int64
   return PF_OK;
 }
 
+// K2 with the region-form quantile windows, dispatched on the quantity mask.
+// Classification only (side stream): persistent over the n / 2048 tiles.
+template <typename TQ, int QM>
+int launch_reduce_qr_m(int grid, WSrc src, int R, TQ* tt, TQ* ct, int64_t* fail, const QArgs& qa,
+                       cudaStream_t st) {
+  constexpr int NQ = (QM & 1) + ((QM >> 1) & 1) + ((QM >> 2) & 1);
+  const size_t smem = (size_t)NQ * (2 * Q_PER + 1) * CDF_THREADS * sizeof(double);
+  static int occ = 0;
+  if (!occ) {
+    CK(cudaFuncSetAttribute(cdf_reduce_qr_kernel<TQ, QM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cdf_reduce_qr_kernel<TQ, QM, false>, CDF_THREADS,
+                                                     smem));
+    if (occ < 1) occ = 1;
+  }
+  (void)grid;
+  const int g = (int)std::min<int64_t>((int64_t)R, (int64_t)sm_count() * occ);
+  cdf_reduce_qr_kernel<TQ, QM, false><<<g, CDF_THREADS, smem, st>>>(src, R, tt, ct, fail, qa);
+  LAUNCHED();
+  return PF_OK;
+}
+
+template <typename TQ>
+int launch_reduce_qr(int qm, int grid, WSrc src, int R, TQ* tt, TQ* ct, int64_t* fail, const QArgs& qa,
+                     cudaStream_t st) {
+  switch (qm) {
+    case 1: return launch_reduce_qr_m<TQ, 1>(grid, src, R, tt, ct, fail, qa, st);
+    case 2: return launch_reduce_qr_m<TQ, 2>(grid, src, R, tt, ct, fail, qa, st);
+    case 3: return launch_reduce_qr_m<TQ, 3>(grid, src, R, tt, ct, fail, qa, st);
+    case 4: return launch_reduce_qr_m<TQ, 4>(grid, src, R, tt, ct, fail, qa, st);
+    case 5: return launch_reduce_qr_m<TQ, 5>(grid, src, R, tt, ct, fail, qa, st);
+    case 6: return launch_reduce_qr_m<TQ, 6>(grid, src, R, tt, ct, fail, qa, st);
+    case 7: return launch_reduce_qr_m<TQ, 7>(grid, src, R, tt, ct, fail, qa, st);
+  }
+  return set_err(PF_ERR_VALUE, "quantile mask");
+}
+
 // ---------------------------------------------------------------- CDF ---
 struct CdfBufs {
   CdfPlan plan;
@@ -253,11 +291,18 @@ struct pf_engine {
   bool single = false;
   DevBuf<Rec> rec[2];
   DevBuf<double> lw;      // log-weights, double-buffered by step parity: [2][n]
-  DevBuf<uint64_t> u3;
+  // draws of step t (draws_kernel), double-buffered by step parity: [2][n]
+  DevBuf<double> dz, dgs, dgt;
+  DevBuf<uint64_t> du3;
+  cudaStream_t dstream = nullptr;  // draws run here, overlapping the CDF kernels
+  cudaEvent_t ev_draw = nullptr, ev_step = nullptr;
+  const double* ntab = nullptr;    // cached normal-quantile table (not owned)
   DevBuf<unsigned char> q;
   DevBuf<int32_t> cut;
-  DevBuf<Grp> grp;        // rank tables (n >= 2^21) replace q (cut is kept)
-  DevBuf<uint8_t> fq;
+  DevBuf<unsigned char> rank;  // rank tables (n >= 2^21): [grp | fq], one L2-persisting window
+  Grp* grp_p = nullptr;
+  uint8_t* fq_p = nullptr;
+  size_t rank_bytes = 0;
   DevBuf<uint32_t> f32;
   bool strata = false;
   DevBuf<int64_t> idx;
@@ -275,6 +320,7 @@ struct pf_engine {
   DevBuf<double> qlw;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_b = nullptr, ev_e = nullptr;
+  cudaEvent_t ev_q[2] = {nullptr, nullptr};  // side stream done with step t (by parity)
   DevBuf<Partial> partials;
   DevBuf<Scalars> sc;
   DevBuf<int64_t> fail;
@@ -352,10 +398,41 @@ int cached_table(int device, double a0, int64_t T, cudaStream_t st, const TableE
   return PF_OK;
 }
 
+// Process-wide normal-quantile table per device (shape independent; the
+// coefficients are generated at 50 digits by scripts/gen_ndtri_table.py).
+struct NtabEntry {
+  int device;
+  double* tab;
+};
+std::vector<NtabEntry> g_ntabs;
+
+int cached_ntab(int device, cudaStream_t st, const double** out) {
+  std::lock_guard<std::mutex> lk(g_tables_mu);
+  for (auto& te : g_ntabs)
+    if (te.device == device) {
+      *out = te.tab;
+      return PF_OK;
+    }
+  NtabEntry te;
+  te.device = device;
+  static_assert(sizeof(NT_COEF) == NT_TABLE_DOUBLES * sizeof(double), "ndtri table size");
+  CK(cudaMalloc((void**)&te.tab, sizeof(NT_COEF)));
+  CK(cudaMemcpyAsync(te.tab, NT_COEF, sizeof(NT_COEF), cudaMemcpyHostToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  g_ntabs.push_back(te);
+  *out = te.tab;
+  return PF_OK;
+}
+
 int build_tables(pf_engine* e, int64_t T) {
   e->tab_s = e->tab_t = nullptr;
   e->sh_s = e->sh_t = nullptr;
+  e->ntab = nullptr;
   if (e->cfg.gamma_method != 0) return PF_OK;
+  {
+    int rc = cached_ntab(e->cfg.device, e->st, &e->ntab);
+    if (rc != PF_OK) return rc;
+  }
   const bool ls = e->cfg.learn && e->cfg.learn_sigma2, lt = e->cfg.learn && e->cfg.learn_tau2;
   const TableEntry* te;
   int rc;
@@ -561,28 +638,49 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   mark(PH_INIT);
 
   const int sms = sm_count();
-  // shared-memory copies of the step's gamma table(s), then the double-
-  // buffered record stage of the cp.async gather pipeline
+  // K1a draws_kernel: tables in shared memory; K1b step_kernel: the double-
+  // buffered cp.async stage (records + draws)
   const bool share_tab = LS && LT && e->tab_s == e->tab_t && c.gamma_method == 0;
-  const int ntab = c.gamma_method == 0 ? (LS ? 1 : 0) + (LT && !share_tab ? 1 : 0) : 0;
-  const size_t stage_off = (size_t)ntab * GT_TABLE_DOUBLES;
-  const size_t step_smem = stage_off * sizeof(double) + (size_t)2 * STEP_SB * 256 * sizeof(Rec);
-  static int step_occ[8] = {0};
+  const int ngt = c.gamma_method == 0 ? (LS ? 1 : 0) + (LT && !share_tab ? 1 : 0) : 0;
+  const size_t draw_smem = ((size_t)ngt * GT_TABLE_DOUBLES + (e->ntab ? NT_TABLE_DOUBLES : 0)) * sizeof(double);
+  const size_t step_smem = (size_t)2 * STEP_SB * 256 * (sizeof(Rec) + 3 * sizeof(double));
   {
     static bool attr[8] = {false};
     if (!attr[MODE]) {
+      CK(cudaFuncSetAttribute(draws_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)((2 * GT_TABLE_DOUBLES + NT_TABLE_DOUBLES) * sizeof(double))));
       CK(cudaFuncSetAttribute(step_kernel<MODE, TQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(2 * GT_TABLE_DOUBLES * sizeof(double) + 2 * STEP_SB * 256 * sizeof(Rec))));
+                              (int)step_smem));
       attr[MODE] = true;
     }
   }
-  int occ = 0;
+  int occ = 0, docc = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, step_kernel<MODE, TQ>, 256, step_smem));
-  (void)step_occ;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&docc, draws_kernel<MODE>, 256, draw_smem));
   if (occ < 1) occ = 1;
-  // persistent grid: one wave of resident CTAs, batches dealt round robin
+  if (docc < 1) docc = 1;
+  // persistent grids: one wave of resident CTAs
   const int64_t nbatches = (n + STEP_SB * 256 - 1) / (STEP_SB * 256);
   const int step_grid = (int)std::min<int64_t>(nbatches, (int64_t)sms * occ);
+  const int draw_grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sms * docc);
+  auto launch_draws = [&](int64_t t, cudaStream_t s_) {
+    DrawArgs d;
+    d.n = n;
+    d.t = t;
+    d.seed = c.seed;
+    d.gs = gamma_src(e, true, t);
+    d.gt = gamma_src(e, false, t);
+    d.ntab = e->ntab;
+    const size_t off = (size_t)(t & 1) * n;
+    d.z = e->dz.p + off;
+    d.g_s = e->dgs.p + off;
+    d.g_t = e->dgt.p + off;
+    d.u3 = e->du3.p + off;
+    d.fail = e->fail.p;
+    draws_kernel<MODE><<<draw_grid, 256, draw_smem, s_>>>(d);
+    LAUNCHED();
+  };
+  if (T >= 1) launch_draws(1, st);
 
   int cur = 0;
   WSrc wsrc;
@@ -602,12 +700,12 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   if (e->strata) {
     so.on = true;
     so.ro.cut = e->cut.p;
-    so.ro.fq = e->fq.p;
+    so.ro.fq = e->fq_p;
     so.ro.f32 = e->f32.p;
     so.ro.B = lk.B;
-    so.grp = e->grp.p;
-    lk.grp = e->grp.p;
-    lk.fq = e->fq.p;
+    so.grp = e->grp_p;
+    lk.grp = e->grp_p;
+    lk.fq = e->fq_p;
     lk.f32 = e->f32.p;
   }
   const int fb_grid = grid_for(n, 256, sms * 4);
@@ -641,19 +739,23 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     a.tau2_fixed = c.tau2_fixed;
     a.sqrt_tau2_fixed = c.sqrt_tau2_fixed;
     a.log_term_fixed = c.log_term_fixed;
-    a.gs = gamma_src(e, true, t);
-    a.gt = gamma_src(e, false, t);
     a.rec_in = e->rec[cur].p;
     a.rec_out = e->rec[cur ^ 1].p;
     a.lw = lwp;
     a.Mout = e->mbuf.p + par;
-    a.u3 = e->u3.p;
+    a.u3 = e->du3.p + (size_t)((t - 1) & 1) * n;
     a.lk = lk;
     a.idx_out = (keep_idx && t > 1) ? e->idx.p : nullptr;
-    a.feed_z = row(fz, t);
-    a.feed_gs = row(fgs, t);
-    a.feed_gt = row(fgt, t);
+    {
+      const size_t off = (size_t)(t & 1) * n;
+      a.z = fz ? row(fz, t) : e->dz.p + off;
+      a.g_s = fgs ? row(fgs, t) : e->dgs.p + off;
+      a.g_t = fgt ? row(fgt, t) : e->dgt.p + off;
+    }
     a.feed_w = row(fw, t);
+    if (t > 1) CK(cudaStreamWaitEvent(st, e->ev_draw, 0));
+    // the side stream's step t-2 work reads the buffers this step overwrites
+    if (ntg && t > 2) CK(cudaStreamWaitEvent(st, e->ev_q[t & 1], 0));
     a.kx = want_fq ? kbase : nullptr;
     a.ks = want_sq ? kbase + n : nullptr;
     a.kt = want_tq ? kbase + 2 * (size_t)n : nullptr;
@@ -666,7 +768,6 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     a.out.t_mean = e->o_tm.p;
     a.out.t_sd = e->o_tsd.p;
     a.fail = e->fail.p;
-    a.stage_off = (int64_t)stage_off;
     if (rs.resident) {
       cudaEvent_t b0, b1;
       cudaEventCreate(&b0);
@@ -681,34 +782,43 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     LAUNCHED();
     ++step_launches;
     cur ^= 1;
+    if (t < T) {
+      // draws(t+1) overwrite the resampling words step t just consumed
+      CK(cudaEventRecord(e->ev_step, st));
+      CK(cudaStreamWaitEvent(e->dstream, e->ev_step, 0));
+      launch_draws(t + 1, e->dstream);
+      CK(cudaEventRecord(e->ev_draw, e->dstream));
+    }
     mark(PH_PROP);
     if (keep_idx && t > 1)
       CK(cudaMemcpyAsync(out->indices + (size_t)(t - 2) * n, e->idx.p, n * sizeof(int64_t),
                          cudaMemcpyDeviceToHost, st));
 
-    // ---- K2-K4 CDF + cut table; K5 weighted quantiles ride on K2
+    // ---- K2-K4 CDF + cut table (main stream); K5 weighted quantiles on the
+    // side stream: window classification of step t, then the exact resolve,
+    // overlapping the CDF and the next step's propagation.
     if (ntg) {
       qa.sh = qshp;
       qa.keys[0] = want_fq ? kbase : nullptr;
       qa.keys[1] = want_sq ? kbase + n : nullptr;
       qa.keys[2] = want_tq ? kbase + 2 * (size_t)n : nullptr;
-      // previous step's resolve updated the window predictor
-      CK(cudaStreamWaitEvent(st, e->ev_e, 0));
-      if (plan.small) {
-        q_window_kernel<TQ><<<grid_for(n, 256), 256, 0, st>>>(wsrc, n, e->fail.p, qa);
-        LAUNCHED();
-        if ((rc = launch_cdf<TQ>(e->cdf, wsrc, n, qv, e->cut.p, e->fail.p, t, st, so)) != PF_OK) return rc;
-      } else {
-        CdfBufs& b = e->cdf;
-        cdf_reduce_q_kernel<TQ><<<(int)plan.chunks, CDF_THREADS, 0, st>>>(
-            wsrc, plan.R, (TQ*)b.tile_tot.p, (TQ*)b.chunk_tot.p, e->fail.p, qa);
-        LAUNCHED();
-        if ((rc = launch_cdf_tail<TQ>(e->cdf, wsrc, n, qv, e->cut.p, e->fail.p, t, st, so)) != PF_OK) return rc;
-      }
-      CK(cudaEventRecord(e->ev_b, st));
-      // side stream: resolve (overlaps the next step's propagation)
+      CK(cudaEventRecord(e->ev_b, st));  // K1b(t): keys, log-weights, M, moments
       cudaStream_t ss = e->side;
       CK(cudaStreamWaitEvent(ss, e->ev_b, 0));
+      if (plan.small) {
+        q_window_kernel<TQ><<<grid_for(n, 256), 256, 0, ss>>>(wsrc, n, e->fail.p, qa);
+        LAUNCHED();
+      } else {
+        const int qm = (want_fq ? 1 : 0) | (want_sq ? 2 : 0) | (want_tq ? 4 : 0);
+        if ((rc = launch_reduce_qr<TQ>(qm, 0, wsrc, (int)plan.tiles, nullptr, nullptr, e->fail.p, qa,
+                                       ss)) != PF_OK)
+          return rc;
+      }
+    }
+    if ((rc = launch_cdf<TQ>(e->cdf, wsrc, n, qv, e->cut.p, e->fail.p, t, st, so)) != PF_OK) return rc;
+    if (ntg) {
+      // side stream: exact resolve (overlaps the CDF and the next step)
+      cudaStream_t ss = e->side;
       QValueSrc vs;
       vs.rec = e->rec[cur].p;
       vs.seed = c.seed;
@@ -750,7 +860,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       q_select_kernel<<<ntg, 1024, 0, ss>>>(qa, vs, e->qscratch.p, ox, os, ot, t, e->fail.p, e->qunres.p);
       q_step_end_kernel<<<1, 1024, 0, ss>>>(qa, 1);
       g_launches.fetch_add(2);
-      CK(cudaEventRecord(e->ev_e, ss));
+      CK(cudaEventRecord(e->ev_q[t & 1], ss));
     } else {
       if ((rc = launch_cdf<TQ>(e->cdf, wsrc, n, qv, e->cut.p, e->fail.p, t, st, so)) != PF_OK) return rc;
     }
@@ -764,7 +874,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       m.seed = c.seed;
       m.resample = 1;
       m.rec = e->rec[cur].p;
-      m.u3 = e->u3.p;
+      m.u3 = e->du3.p + (size_t)(t & 1) * n;
       m.lk = lk;
       m.s2_direct = nullptr;
       m.gs = gamma_src(e, true, t);
@@ -807,7 +917,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     m.seed = c.seed;
     m.resample = 1;
     m.rec = e->rec[cur].p;
-    m.u3 = e->u3.p;
+    m.u3 = e->du3.p + (size_t)(T & 1) * n;
     m.lk = lk;
     m.s2_direct = nullptr;
     m.gs = gamma_src(e, true, T);
@@ -875,7 +985,10 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   }
 
   // ---- join the quantile side stream, then outputs to host
-  if (ntg) CK(cudaStreamWaitEvent(st, e->ev_e, 0));
+  if (ntg) {
+    CK(cudaStreamWaitEvent(st, e->ev_q[0], 0));
+    CK(cudaStreamWaitEvent(st, e->ev_q[1], 0));
+  }
   if (out && T > 0) {
     auto cp = [&](double* h, DevBuf<double>& d, size_t cnt) -> int {
       if (h) CK(cudaMemcpyAsync(h, d.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -905,6 +1018,13 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     unsigned int h[4];
     CK(cudaMemcpy(h, e->qunres.p, sizeof(h), cudaMemcpyDeviceToHost));
     for (int k = 0; k < 4; ++k) e->qstats[k] = h[k];
+    if (getenv("PF_QDEBUG")) {  // diagnostics: last step's window per target
+      std::vector<QTarget> tg((size_t)ntg);
+      CK(cudaMemcpy(tg.data(), e->qtg.p, ntg * sizeof(QTarget), cudaMemcpyDeviceToHost));
+      for (int k = 0; k < ntg; ++k)
+        fprintf(stderr, "qtarget %d q=%d p=%.3f h=%.4g ema=%.4g count=%u missed=%u status=%u\n", k, tg[k].q,
+                tg[k].p, tg[k].h, tg[k].ema, tg[k].count, tg[k].missed, tg[k].status);
+    }
   }
   float ms = 0;
   cudaEventElapsedTime(&ms, e->ev0, e->ev1);
@@ -1004,19 +1124,49 @@ int pf_engine_create(const pf_config* cfg, pf_engine** out) {
   // promote each miss into a 64/128-byte DRAM fetch.
   cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32);
   if ((err = cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking))) return bail(err);
+  if ((err = cudaStreamCreateWithFlags(&e->dstream, cudaStreamNonBlocking)) ||
+      (err = cudaEventCreateWithFlags(&e->ev_draw, cudaEventDisableTiming)) ||
+      (err = cudaEventCreateWithFlags(&e->ev_step, cudaEventDisableTiming)))
+    return bail(err);
   if ((err = cudaEventCreateWithFlags(&e->ev_b, cudaEventDisableTiming)) ||
-      (err = cudaEventCreateWithFlags(&e->ev_e, cudaEventDisableTiming)) || (err = e->mbuf.ensure(2)))
+      (err = cudaEventCreateWithFlags(&e->ev_e, cudaEventDisableTiming)) ||
+      (err = cudaEventCreateWithFlags(&e->ev_q[0], cudaEventDisableTiming)) ||
+      (err = cudaEventCreateWithFlags(&e->ev_q[1], cudaEventDisableTiming)) || (err = e->mbuf.ensure(2)))
     return bail(err);
   if ((err = e->rec[0].ensure(n)) || (err = e->rec[1].ensure(n)) || (err = e->lw.ensure(2 * n)) ||
-      (err = e->u3.ensure(n)) || (err = e->partials.ensure(sm_count() * 8 + 8)) ||
+      (err = e->du3.ensure(2 * n)) || (err = e->dz.ensure(2 * n)) ||
+      (err = e->dgs.ensure(2 * n)) || (err = e->dgt.ensure(2 * n)) || (err = e->partials.ensure(sm_count() * 8 + 8)) ||
       (err = e->sc.ensure(1)) || (err = e->fail.ensure(1)) ||
       (err = e->cdf.ensure(n, e->single ? 4 : 8)) || (err = e->probs.ensure(8)))
     return bail(err);
   e->strata = ilog2(n) >= STRATA_MIN_LOG2N;
   if (e->strata) {
-    if ((err = e->grp.ensure(n / GRP_STRATA)) || (err = e->fq.ensure(n + 16)) || (err = e->f32.ensure(n)) ||
-        (err = e->cut.ensure(n + 1)))
+    const size_t gbytes = (size_t)(n / GRP_STRATA) * sizeof(Grp);
+    e->rank_bytes = gbytes + (size_t)n + 16;
+    if ((err = e->rank.ensure(e->rank_bytes)) || (err = e->f32.ensure(n)) || (err = e->cut.ensure(n + 1)))
       return bail(err);
+    e->grp_p = reinterpret_cast<Grp*>(e->rank.p);
+    e->fq_p = e->rank.p + gbytes;
+    // Keep the rank tables resident in L2 while the step kernel's random
+    // record gathers stream through it (best effort: ignored if the device
+    // has no persisting carve-out).
+    int maxp = 0;
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, cfg->device);
+    int maxw = 0;
+    cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, cfg->device);
+    if (maxp > 0 && maxw > 0) {
+      const size_t want = std::min<size_t>(e->rank_bytes, (size_t)maxp);
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+      cudaStreamAttrValue av;
+      memset(&av, 0, sizeof(av));
+      av.accessPolicyWindow.base_ptr = e->rank.p;
+      av.accessPolicyWindow.num_bytes = std::min<size_t>(e->rank_bytes, (size_t)maxw);
+      av.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)want / (double)av.accessPolicyWindow.num_bytes);
+      av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaStreamSetAttribute(e->st, cudaStreamAttributeAccessPolicyWindow, &av);
+      cudaGetLastError();
+    }
     const int32_t nn = (int32_t)n;  // cut[N] = N: end of the last stratum's run
     if ((err = cudaMemcpy(e->cut.p + n, &nn, sizeof(nn), cudaMemcpyHostToDevice))) return bail(err);
   } else {
@@ -1087,11 +1237,17 @@ int pf_engine_destroy(pf_engine* e) {
   for (auto* b : bufs) b->release();
   e->rec[0].release();
   e->rec[1].release();
-  e->u3.release();
+  e->du3.release();
+  e->dz.release();
+  e->dgs.release();
+  e->dgt.release();
+  if (e->dstream) cudaStreamSynchronize(e->dstream);
+  if (e->dstream) cudaStreamDestroy(e->dstream);
+  if (e->ev_draw) cudaEventDestroy(e->ev_draw);
+  if (e->ev_step) cudaEventDestroy(e->ev_step);
   e->q.release();
   e->cut.release();
-  e->grp.release();
-  e->fq.release();
+  e->rank.release();
   e->f32.release();
   e->idx.release();
   e->partials.release();
@@ -1118,6 +1274,8 @@ int pf_engine_destroy(pf_engine* e) {
   if (e->side) cudaStreamDestroy(e->side);
   if (e->ev_b) cudaEventDestroy(e->ev_b);
   if (e->ev_e) cudaEventDestroy(e->ev_e);
+  for (auto ev : e->ev_q)
+    if (ev) cudaEventDestroy(ev);
   for (auto ev : e->evs) cudaEventDestroy(ev);
   if (e->ev0) cudaEventDestroy(e->ev0);
   if (e->ev1) cudaEventDestroy(e->ev1);
@@ -1164,6 +1322,11 @@ __global__ void stream_uniforms_kernel(uint64_t seed, uint64_t counter, int64_t 
 __global__ void ndtri_kernel(const double* u, int64_t n, double* out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = ndtri(u[i]);
+}
+
+__global__ void ndtri_table_kernel(const double* tab, const double* u, int64_t n, double* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = nt_eval(tab, u[i]);
 }
 
 __global__ void gamma_kernel(GammaSrc g, const double* u, int64_t n, double* out) {
@@ -1359,6 +1522,26 @@ int pf_ndtri(const double* u, int64_t n, double* out) {
   CK(s.alloc(&dz, n));
   CK(cudaMemcpy(du, u, n * 8, cudaMemcpyHostToDevice));
   ndtri_kernel<<<grid_for(n, 256), 256>>>(du, n, dz);
+  LAUNCHED();
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(out, dz, n * 8, cudaMemcpyDeviceToHost));
+  return PF_OK;
+}
+
+int pf_ndtri_table(const double* u, int64_t n, double* out) {
+  int rc;
+  if ((rc = need_device())) return rc;
+  if (n <= 0) return PF_OK;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  const double* tab = nullptr;
+  if ((rc = cached_ntab(dev, 0, &tab)) != PF_OK) return rc;
+  Scratch s;
+  double *du, *dz;
+  CK(s.alloc(&du, n));
+  CK(s.alloc(&dz, n));
+  CK(cudaMemcpy(du, u, n * 8, cudaMemcpyHostToDevice));
+  ndtri_table_kernel<<<grid_for(n, 256), 256>>>(tab, du, n, dz);
   LAUNCHED();
   CK(cudaGetLastError());
   CK(cudaMemcpy(out, dz, n * 8, cudaMemcpyDeviceToHost));

@@ -160,7 +160,7 @@ struct QWin {
 };
 
 // CTA-level candidate staging (shared memory).
-constexpr int Q_AGG = 2048;
+constexpr int Q_AGG = 512;
 struct QAgg {
   QCand c[Q_AGG];
   uint32_t pos[Q_AGG];
@@ -374,6 +374,219 @@ cdf_reduce_q_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ c
   }
   q_flush(qa, agg);
   q_reduce_partials(qa, win, acc, wsum);  // shared copy: dynamic indices there
+}
+
+// K2 with the quantile windows, region form (the hot path).  The K window
+// bounds of a quantity (lo_k and hi_k + 1) cut the key line into 2K+1
+// regions; an element's region r = #{bounds <= key} costs 2K compares, its
+// weight goes to a per-thread region sum in shared memory, and
+//   key < lo_k          <=>  r <= idx_k     (idx_k = #{bounds < lo_k})
+//   lo_k <= key <= hi_k <=>  idx_k < r <= jdx_k (jdx_k = #{bounds < hi_k+1})
+// so the below-window weights are prefix sums of the region sums and the
+// in-window test is one table lookup.  Same outputs as cdf_reduce_q_kernel
+// (wbelow per target, candidate lists), at a fraction of the instructions.
+// QM: bit q set when quantity q (x, sigma2, tau2) has targets.
+struct QRegions {
+  uint32_t b[Q_MAXQ][2 * Q_PER];   // sorted bounds (64-bit-safe: hi+1 clamped)
+  uint8_t idx[Q_MAXQ][Q_PER];      // #{bounds < lo_k}
+  uint16_t inmask[Q_MAXQ][2 * Q_PER + 1];  // window slots (bit s) containing region r
+};
+
+PF_D void q_make_regions(const QWin& win, QRegions& rg) {
+  if (threadIdx.x < Q_MAXQ) {
+    const int q = threadIdx.x;
+    const int K = win.nq[q];
+    uint32_t b[2 * Q_PER];
+    uint32_t hp1[Q_PER];
+    for (int k = 0; k < K; ++k) {
+      const int s = q * Q_PER + k;
+      hp1[k] = win.hi[s] == 0xFFFFFFFFu ? 0xFFFFFFFFu : win.hi[s] + 1u;
+      b[2 * k] = win.lo[s];
+      b[2 * k + 1] = hp1[k];
+    }
+    // insertion sort (<= 10 values)
+    for (int i = 1; i < 2 * K; ++i) {
+      const uint32_t v = b[i];
+      int j = i - 1;
+      while (j >= 0 && b[j] > v) {
+        b[j + 1] = b[j];
+        --j;
+      }
+      b[j + 1] = v;
+    }
+    for (int i = 0; i < 2 * Q_PER; ++i) rg.b[q][i] = i < 2 * K ? b[i] : 0xFFFFFFFFu;
+    for (int r = 0; r <= 2 * Q_PER; ++r) rg.inmask[q][r] = 0;
+    for (int k = 0; k < K; ++k) {
+      const int s = q * Q_PER + k;
+      int il = 0, ih = 0;
+      for (int i = 0; i < 2 * K; ++i) {
+        il += b[i] < win.lo[s];
+        ih += b[i] < hp1[k];
+      }
+      // a window reaching the top key also holds 0xFFFFFFFF (hi + 1 clamped)
+      if (win.hi[s] == 0xFFFFFFFFu) ih = 2 * Q_PER;
+      rg.idx[q][k] = (uint8_t)il;
+      for (int r = il + 1; r <= ih && r <= 2 * Q_PER; ++r) rg.inmask[q][r] |= (uint16_t)(1u << s % 16);
+    }
+  }
+  __syncthreads();
+}
+
+// TREE = false: the classification alone (side stream), persistent over
+// tiles (R = number of tiles); TREE = true: fused into K2 (one chunk of R
+// tiles per CTA, with the exact subtree sums).
+template <typename T, int QM, bool TREE>
+__global__ void __launch_bounds__(CDF_THREADS)
+cdf_reduce_qr_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ chunk_tot,
+                     const int64_t* __restrict__ fail, QArgs qa) {
+  if (fail && *fail) return;
+  constexpr int NR = 2 * Q_PER + 1;
+  __shared__ T wt[CDF_THREADS / 32];
+  __shared__ T tt[64];
+  __shared__ QWin win;
+  __shared__ QAgg agg;
+  __shared__ QRegions rg;
+  // per-thread region sums (dynamic shared memory, present quantities only)
+  double* rsum = pf_gtab;
+  auto RS = [&](int q, int r) -> double& {
+    const int qi = __popc((unsigned)QM & ((1u << q) - 1u));
+    return rsum[(qi * NR + r) * CDF_THREADS + threadIdx.x];
+  };
+  q_agg_init(agg);
+  q_make_windows(qa, win);
+  q_make_regions(win, rg);
+#pragma unroll
+  for (int q = 0; q < Q_MAXQ; ++q)
+    if (QM & (1 << q))
+#pragma unroll
+      for (int r = 0; r < NR; ++r) RS(q, r) = 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double M = src.mode == 0 ? *src.M : 0.0;
+  const int64_t chunk = blockIdx.x;
+  uint32_t bnd[Q_MAXQ][2 * Q_PER];
+#pragma unroll
+  for (int q = 0; q < Q_MAXQ; ++q)
+#pragma unroll
+    for (int i = 0; i < 2 * Q_PER; ++i) bnd[q][i] = rg.b[q][i];
+  double wsum = 0.0;
+  const int nloop = TREE ? R : (int)((R - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x);
+  for (int r = 0; r < nloop; ++r) {
+    const int64_t tile = TREE ? chunk * R + r : (int64_t)blockIdx.x + (int64_t)r * gridDim.x;
+    const int64_t base = tile * CDF_TILE + threadIdx.x * CDF_V;
+    T v[CDF_V], l1[4], l2[2], g;
+    load_tile_weights<T>(src, base, M, v);
+    uint32_t key[Q_MAXQ][CDF_V];
+#pragma unroll
+    for (int q = 0; q < Q_MAXQ; ++q) {
+      if (!(QM & (1 << q))) continue;
+      const uint4* kp = reinterpret_cast<const uint4*>(qa.keys[q] + base);
+      const uint4 k0 = __ldcs(kp), k1 = __ldcs(kp + 1);
+      key[q][0] = k0.x; key[q][1] = k0.y; key[q][2] = k0.z; key[q][3] = k0.w;
+      key[q][4] = k1.x; key[q][5] = k1.y; key[q][6] = k1.z; key[q][7] = k1.w;
+    }
+    uint32_t anyin = 0;
+    uint32_t inw[CDF_V];
+#pragma unroll
+    for (int e = 0; e < CDF_V; ++e) {
+      const double w = (double)v[e];
+      wsum += w;
+      inw[e] = 0;
+#pragma unroll
+      for (int q = 0; q < Q_MAXQ; ++q) {
+        if (!(QM & (1 << q))) continue;
+        int rr = 0;
+#pragma unroll
+        for (int i = 0; i < 2 * Q_PER; ++i) rr += key[q][e] >= bnd[q][i];
+        RS(q, rr) += w;
+        inw[e] |= (uint32_t)rg.inmask[q][rr];
+      }
+      anyin |= inw[e];
+    }
+    // candidates (rare): warp-aggregated appends, as in q_classify
+    if (__any_sync(0xffffffffu, anyin != 0u)) {
+#pragma unroll
+      for (int e = 0; e < CDF_V; ++e) {
+        uint32_t any = __reduce_or_sync(0xffffffffu, inw[e]);
+        while (any) {
+          const int sl = __ffs(any) - 1;
+          any &= any - 1;
+          const int q = sl / Q_PER;
+          const int tq = win.base[q] + (sl - q * Q_PER);
+          const unsigned m = __ballot_sync(0xffffffffu, (inw[e] >> sl) & 1u);
+          const int leader = __ffs(m) - 1;
+          int slot = 0;
+          uint32_t kpos = 0;
+          if (lane == leader) {
+            slot = atomicAdd(&agg.fill, __popc(m));
+            if (slot + __popc(m) <= Q_AGG) kpos = atomicAdd(&agg.cnt[tq], (uint32_t)__popc(m));
+            else kpos = 0x80000000u | atomicAdd(&qa.tg[tq].count, (uint32_t)__popc(m));
+          }
+          slot = __shfl_sync(0xffffffffu, slot, leader);
+          kpos = __shfl_sync(0xffffffffu, kpos, leader);
+          if ((inw[e] >> sl) & 1u) {
+            const uint32_t rank = __popc(m & ((1u << lane) - 1u));
+            QCand c;
+            c.key = q == 0 ? key[0][e] : (q == 1 ? key[1][e] : key[2][e]);
+            c.idx = (uint32_t)(base + e);
+            c.w = (double)v[e];
+            if (kpos & 0x80000000u) {
+              const uint32_t pos = (kpos & 0x7FFFFFFFu) + rank;
+              if (pos < qa.cap) qa.cand[(size_t)tq * qa.cap + pos] = c;
+              if (slot + (int)rank < Q_AGG) agg.tk[slot + rank] = 0xFF;  // reserved, unused
+            } else {
+              agg.c[slot + rank] = c;
+              agg.tk[slot + rank] = (uint8_t)tq;
+              agg.pos[slot + rank] = kpos + rank;
+            }
+          }
+        }
+      }
+    }
+    if (TREE) {
+      thread_tree8<T>(v, l1, l2, g);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) g = g + __shfl_xor_sync(0xffffffffu, g, o);
+      if (lane == 0) wt[warp] = g;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        T a0 = wt[0] + wt[1], a1 = wt[2] + wt[3], a2 = wt[4] + wt[5], a3 = wt[6] + wt[7];
+        T tot = (a0 + a1) + (a2 + a3);
+        tt[r] = tot;
+        tile_tot[tile] = tot;
+      }
+      __syncthreads();
+    }
+  }
+  if (TREE && threadIdx.x == 0) {
+    for (int len = R; len > 1; len >>= 1)
+      for (int i = 0; i < len / 2; ++i) tt[i] = tt[2 * i] + tt[2 * i + 1];
+    chunk_tot[chunk] = tt[0];
+  }
+  // per-thread below-window sums from the region sums
+  double acc[Q_SLOTS];
+#pragma unroll
+  for (int sl = 0; sl < Q_SLOTS; ++sl) acc[sl] = 0.0;
+#pragma unroll
+  for (int q = 0; q < Q_MAXQ; ++q) {
+    if (!(QM & (1 << q))) continue;
+    double pre[NR];
+    double run = 0.0;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      run += RS(q, r);
+      pre[r] = run;
+    }
+#pragma unroll
+    for (int k = 0; k < Q_PER; ++k) {
+      const int il = rg.idx[q][k];
+      double a = 0.0;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) a = (r == il) ? pre[r] : a;
+      acc[q * Q_PER + k] = a;
+    }
+  }
+  q_flush(qa, agg);
+  q_reduce_partials(qa, win, acc, wsum);
 }
 
 // Window pass on its own (n below one CDF tile, where K2 is not used).

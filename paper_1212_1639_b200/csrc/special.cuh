@@ -18,6 +18,12 @@
 //               u-space: 51 binades x 4 sub-segments per tail plus 32 central
 //               segments, degree 11 (Horner with FMA).  No transcendental on
 //               the draw path.
+//  * nt_eval -- the hot-path normal draw: the same u-space piecewise table
+//               for ndtri on v = min(u, 1-u) (ndtri is odd about 1/2), the
+//               central quarter fitted as ndtri(v)/(v - 1/2) so relative
+//               accuracy holds down to the zero.  Branch-free apart from
+//               the segment index, so a warp no longer executes both the
+//               central and the log/sqrt tail branch of the Cephes code.
 #pragma once
 #include <math.h>
 
@@ -274,6 +280,96 @@ PF_HD double gt_eval(CoefPtr coef, double u) {
 #pragma unroll
   for (int k = GT_DEG - 1; k >= 0; --k) r = fma(r, t, c[k]);
   return r;
+}
+
+// --------------------------------------------------- normal quantile table --
+constexpr int NT_TAIL = GT_BINADES * GT_SUB;    // v in [2^-53, 1/4): 204 segments
+constexpr int NT_CENTRAL = 16;                  // v in [1/4, 1/2]
+constexpr int NT_NSEG = NT_TAIL + NT_CENTRAL;   // 220
+constexpr int NT_TABLE_DOUBLES = NT_NSEG * GT_NC;
+
+// Segment of u, local coordinate t in [-1,1], and the factor the table
+// polynomial is multiplied by (sign; (v - 1/2) in the central segments).
+PF_HD int nt_segment(double u, double* t, double* scale) {
+  const bool up = u > 0.5;
+  const double v = up ? 1.0 - u : u;  // exact for u >= 1/2
+  const double sg = up ? -1.0 : 1.0;
+  if (v < 0.25) {
+    union { double d; uint64_t b; } c;
+    c.d = v;
+    int e = int((c.b >> 52) & 0x7FF) - 1023;
+    if (e < -53) e = -53;
+    const int i = int((c.b >> (52 - 2)) & 3);
+    c.b = (c.b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull;
+    *t = (c.d - (1.0 + (i + 0.5) * 0.25)) * 8.0;
+    *scale = sg;
+    return (e + 53) * GT_SUB + i;
+  }
+  const double xx = (v - 0.25) * (4.0 * NT_CENTRAL);
+  int j = int(xx);
+  if (j > NT_CENTRAL - 1) j = NT_CENTRAL - 1;
+  *t = (xx - j - 0.5) * 2.0;
+  *scale = sg * (v - 0.5);  // exact
+  return NT_TAIL + j;
+}
+
+// The v (<= 1/2) at local coordinate t of segment seg, and whether the
+// segment is central (fitted as ndtri(v)/(v-1/2)).
+PF_HD double nt_point(int seg, double t, bool* central) {
+  if (seg >= NT_TAIL) {
+    *central = true;
+    return 0.25 + (seg - NT_TAIL + 0.5 + 0.5 * t) / (4.0 * NT_CENTRAL);
+  }
+  *central = false;
+  const int e = seg / GT_SUB - 53, i = seg % GT_SUB;
+  return ldexp(1.0 + (i + 0.5 + 0.5 * t) * 0.25, e);
+}
+
+template <typename CoefPtr>
+PF_HD double nt_eval(CoefPtr coef, double u) {
+  double t, sc;
+  const int seg = nt_segment(u, &t, &sc);
+  const double* c = &coef[seg * GT_NC];
+  double r = c[GT_DEG];
+#pragma unroll
+  for (int k = GT_DEG - 1; k >= 0; --k) r = fma(r, t, c[k]);
+  return sc * r;
+}
+
+// Chebyshev interpolant through f at the GT_NC Chebyshev nodes of [-1,1],
+// converted to monomial coefficients in t (one thread).  Coefficients below
+// trunc * max|f| are rounding noise of the DCT; the monomial expansion would
+// amplify them (T_11 has coefficients up to 2^10), so they are dropped.
+PF_HD void cheb_to_mono(const double* f, double* out, double trunc = 0.0) {
+  const double PI = 3.14159265358979323846;
+  double c[GT_NC];
+  for (int k = 0; k < GT_NC; ++k) {
+    double s = 0.0;
+    for (int i = 0; i < GT_NC; ++i) s += f[i] * cos(PI * k * (i + 0.5) / GT_NC);
+    c[k] = s * (2.0 / GT_NC);
+  }
+  c[0] *= 0.5;
+  if (trunc > 0.0) {
+    double fm = 0.0;
+    for (int i = 0; i < GT_NC; ++i) fm = fmax(fm, fabs(f[i]));
+    for (int k = 1; k < GT_NC; ++k)
+      if (fabs(c[k]) < trunc * fm) c[k] = 0.0;
+  }
+  double tm[GT_NC] = {0}, tk[GT_NC] = {0}, mono[GT_NC] = {0};
+  tm[0] = 1.0;
+  tk[1] = 1.0;
+  mono[0] = c[0];
+  for (int i = 0; i < GT_NC; ++i) mono[i] += c[1] * tk[i];
+  for (int k = 2; k < GT_NC; ++k) {
+    double tn[GT_NC];
+    for (int i = 0; i < GT_NC; ++i) tn[i] = (i ? 2.0 * tk[i - 1] : 0.0) - tm[i];
+    for (int i = 0; i < GT_NC; ++i) {
+      mono[i] += c[k] * tn[i];
+      tm[i] = tk[i];
+      tk[i] = tn[i];
+    }
+  }
+  for (int i = 0; i < GT_NC; ++i) out[i] = mono[i];
 }
 
 }  // namespace pf

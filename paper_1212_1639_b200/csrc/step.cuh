@@ -23,7 +23,7 @@
 namespace pf {
 
 constexpr double LOG_TWO_PI = 1.8378770664093453;  // math.log(2*math.pi), models.py:20
-constexpr int STEP_SB = 4;  // slots per thread whose gathers are in flight together
+constexpr int STEP_SB = 2;  // slots per thread per pipeline stage (double buffered)
 
 // Order-preserving 32-bit image of a double (float32 rounded down, sign
 // folded): the quantile keys of quantile.cuh.
@@ -57,14 +57,19 @@ PF_D double gamma_draw(const GammaSrc& g, double u) {
 // extern symbol directly keeps the loads LDS (not generic LD).
 extern __shared__ double pf_gtab[];
 
+// Staged tables are coefficient-major ([k][seg]): the lanes of a warp read
+// coefficient k of their own (random) segments, which then spread over all
+// 16 double-wide bank pairs instead of the 4 a 12-double segment stride
+// leaves (4x fewer shared-memory wavefronts).  Same coefficients and Horner
+// order as gt_eval on the global [seg][k] table, so the values are identical.
 PF_D double gamma_draw_slot(const GammaSrc& g, int slot, double u) {
   if (slot < 0) return gamma_draw(g, u);
   double t;
   const int seg = gt_segment(u, &t);
-  const double* c = pf_gtab + slot * GT_TABLE_DOUBLES + seg * GT_NC;
-  double r = c[GT_DEG];
+  const double* c = pf_gtab + slot * GT_TABLE_DOUBLES + seg;
+  double r = c[GT_DEG * GT_NSEG];
 #pragma unroll
-  for (int k = GT_DEG - 1; k >= 0; --k) r = fma(r, t, c[k]);
+  for (int k = GT_DEG - 1; k >= 0; --k) r = fma(r, t, c[k * GT_NSEG]);
   return r;
 }
 
@@ -85,30 +90,7 @@ gamma_table_build_kernel(const double* __restrict__ shapes, double* __restrict__
     f[j] = gamma_quantile_pv(a, u, v, !up);
   }
   __syncthreads();
-  if (j == 0) {
-    double c[GT_NC];
-    for (int k = 0; k < GT_NC; ++k) {
-      double s = 0.0;
-      for (int i = 0; i < GT_NC; ++i) s += f[i] * cos(PI * k * (i + 0.5) / GT_NC);
-      c[k] = s * (2.0 / GT_NC);
-    }
-    c[0] *= 0.5;
-    double tm[GT_NC] = {0}, tk[GT_NC] = {0}, mono[GT_NC] = {0};
-    tm[0] = 1.0;
-    tk[1] = 1.0;
-    mono[0] = c[0];
-    for (int i = 0; i < GT_NC; ++i) mono[i] += c[1] * tk[i];
-    for (int k = 2; k < GT_NC; ++k) {
-      double tn[GT_NC];
-      for (int i = 0; i < GT_NC; ++i) tn[i] = (i ? 2.0 * tk[i - 1] : 0.0) - tm[i];
-      for (int i = 0; i < GT_NC; ++i) {
-        mono[i] += c[k] * tn[i];
-        tm[i] = tk[i];
-        tk[i] = tn[i];
-      }
-    }
-    for (int i = 0; i < GT_NC; ++i) out[i] = mono[i];
-  }
+  if (j == 0) cheb_to_mono(f, out);
 }
 
 // --------------------------------------------------------------- init ---
@@ -177,17 +159,16 @@ struct StepArgs {
   uint64_t seed;
   double y;
   double sigma2_fixed, tau2_fixed, sqrt_tau2_fixed, log_term_fixed;
-  GammaSrc gs, gt;
   const Rec* rec_in;
   Rec* rec_out;
   double* lw;            // log-weights (or fed weights when feed_w)
   double* Mout;          // max log-weight of this step (per-parity slot)
-  uint64_t* u3;          // resampling word of the previous step (in), this step (out)
+  const uint64_t* u3;    // resampling words of step t-1 (draws_kernel)
   Lookup<TQ> lk;         // resampling table of step t-1 (t > 1)
   int64_t* idx_out;      // optional 1-based ancestors of step t-1
-  const double* feed_z;  // oracle feed rows for step t (or null)
-  const double* feed_gs;
-  const double* feed_gt;
+  const double* z;       // step t normals / gamma draws: draws_kernel output,
+  const double* g_s;     // or the oracle feed rows
+  const double* g_t;
   const double* feed_w;
   uint32_t* kx;          // optional order-preserving 32-bit keys for the
   uint32_t* ks;          // weighted quantiles (quantile.cuh)
@@ -197,7 +178,6 @@ struct StepArgs {
   Scalars* sc;
   StepOut out;
   int64_t* fail;
-  int64_t stage_off;     // offset (doubles) of the record stage in dynamic smem
 };
 
 PF_D double warp_sum(double v) {
@@ -211,48 +191,126 @@ PF_D double warp_max(double v) {
   return v;
 }
 
+// ---------------------------------------------------------------- draws ---
+// K1a: the record-independent half of step t -- Philox block t of every
+// stream, the normal draw and the two inverse-gamma draws (filtering.py:
+// 273,280,286; counter layout rng.py:221-224) -- compute-bound work that
+// runs on its own stream, concurrently with the memory-bound CDF kernels of
+// step t-1.  Writes z, g_sigma, g_tau and the resampling word (slot 3).
+struct DrawArgs {
+  int64_t n;
+  int64_t t;
+  uint64_t seed;
+  GammaSrc gs, gt;
+  const double* ntab;    // normal-quantile table (null: Cephes ndtri)
+  double* z;
+  double* g_s;
+  double* g_t;
+  uint64_t* u3;
+  const int64_t* fail;
+};
+
+PF_D double nt_eval_slot(int off, double u) {
+  double t, sc;
+  const int seg = nt_segment(u, &t, &sc);
+  const double* c = pf_gtab + off + seg;
+  double r = c[GT_DEG * NT_NSEG];
+#pragma unroll
+  for (int k = GT_DEG - 1; k >= 0; --k) r = fma(r, t, c[k * NT_NSEG]);
+  return sc * r;
+}
+
+// Stage this step's tables in shared memory: gamma table(s) (one copy when
+// sigma2 and tau2 share the shape schedule), then the normal table.
+template <bool LS, bool LT>
+PF_D void stage_tables(const GammaSrc& gs, const GammaSrc& gt, const double* ntab, int& slot_s, int& slot_t,
+                       int& noff) {
+  slot_s = slot_t = -1;
+  const double* srcs[3] = {LS && gs.method == 0 ? gs.table : nullptr,
+                           LT && gt.method == 0 && !(LS && gt.table == gs.table) ? gt.table : nullptr, ntab};
+  const int len[3] = {GT_TABLE_DOUBLES, GT_TABLE_DOUBLES, NT_TABLE_DOUBLES};
+  const int nseg[3] = {GT_NSEG, GT_NSEG, NT_NSEG};
+  int off = 0;
+  for (int k = 0; k < 3; ++k) {
+    if (!srcs[k]) continue;
+    // global [seg][coef] -> shared [coef][seg]
+    for (int i = threadIdx.x; i < len[k]; i += blockDim.x) {
+      const int sg = i / GT_NC, cf = i - sg * GT_NC;
+      pf_gtab[off + cf * nseg[k] + sg] = __ldg(srcs[k] + i);
+    }
+    if (k == 0) slot_s = off / GT_TABLE_DOUBLES;
+    else if (k == 1) slot_t = off / GT_TABLE_DOUBLES;
+    else noff = off;
+    off += len[k];
+  }
+  if (LS && LT && gs.method == 0 && gt.table == gs.table) slot_t = slot_s;
+  __syncthreads();
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) draws_kernel(DrawArgs a) {
+  constexpr bool LS = MODE & M_LS, LT = MODE & M_LT;
+  if (*a.fail) return;
+  int slot_s, slot_t, noff = -1;
+  stage_tables<LS, LT>(a.gs, a.gt, a.ntab, slot_s, slot_t, noff);
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const Philox4 P = philox_block(a.seed, (uint64_t)j, (uint64_t)a.t);
+    a.u3[j] = P.w[3];
+    const double u0 = unit_open(P.w[0]);
+    a.z[j] = noff >= 0 ? nt_eval_slot(noff, u0) : ndtri(u0);
+    if (LS) a.g_s[j] = gamma_draw_slot(a.gs, slot_s, unit_open(P.w[1]));
+    if (LT) a.g_t[j] = gamma_draw_slot(a.gt, slot_t, unit_open(P.w[2]));
+  }
+}
+
+// ---------------------------------------------------------------- K1b ---
+PF_D void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
+}
+PF_D void cp_async8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src));
+}
+
 template <int MODE, typename TQ>
 __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
   constexpr bool LS = MODE & M_LS, LT = MODE & M_LT, SINGLE = MODE & M_SINGLE;
   if (*a.fail) return;
-  // This step's inverse-gamma table(s) -> shared memory (41 KB each; one
-  // copy when sigma2 and tau2 share the shape schedule).
-  const GammaSrc gs = a.gs, gt = a.gt;
-  int slot_s = -1, slot_t = -1;  // table slots in pf_gtab (shared), -1 = not tabulated
-  {
-    const double* srcs[2] = {LS && gs.method == 0 ? gs.table : nullptr,
-                             LT && gt.method == 0 && !(LS && gt.table == gs.table) ? gt.table : nullptr};
-    int slot = 0;
-    for (int k = 0; k < 2; ++k) {
-      if (!srcs[k]) continue;
-      const double2* s2p = reinterpret_cast<const double2*>(srcs[k]);
-      double2* d2p = reinterpret_cast<double2*>(pf_gtab + slot * GT_TABLE_DOUBLES);
-      for (int i = threadIdx.x; i < GT_TABLE_DOUBLES / 2; i += blockDim.x) d2p[i] = __ldg(&s2p[i]);
-      if (k == 0) slot_s = slot; else slot_t = slot;
-      ++slot;
-    }
-    if (LS && LT && gs.method == 0 && a.gt.table == a.gs.table) slot_t = slot_s;
-    __syncthreads();
-  }
   const bool feedw = a.feed_w != nullptr;
   const double cs = a.sc->cs, ct = a.sc->ct, cx = a.sc->cx;
   double m = feedw ? 0.0 : -INFINITY;
   double s0 = 0, sx = 0, s2x = 0, s1s = 0, s2s = 0, s1t = 0, s2t = 0;
   bool bad = false;
 
-  // Software pipeline over batches of STEP_SB x 256 slots (batches are
-  // dealt to CTAs round robin).  Iteration i: resolve the ancestors of
-  // batch i+1 (cut-point lookups: L2-resident tables) and start their
-  // 32-byte record gathers with cp.async into the other half of a double
-  // buffer; then wait for batch i's gathers (issued one iteration earlier)
-  // and run its compute -- Philox, ndtri, the two inverse-gamma draws,
-  // propagation, log-weight, moments -- while batch i+1's random DRAM reads
-  // are in flight.  Each thread only reads back its own staged records.
-  Rec* stage = reinterpret_cast<Rec*>(pf_gtab + a.stage_off);  // [2][STEP_SB][blockDim]
+  // Software pipeline over batches of STEP_SB x blockDim slots (batches are
+  // dealt to CTAs round robin).  Iteration i: resolve the ancestors of batch
+  // i+1 (cut-point lookups against L2-resident tables) and start, with
+  // cp.async into the other half of a double buffer, their 32-byte record
+  // gathers (the one random DRAM access per slot) and the coalesced loads
+  // of their draws; then wait for batch i (issued one iteration earlier) and
+  // run its arithmetic while batch i+1's reads are in flight.  Each thread
+  // reads back only what it staged itself.
   const int nth = blockDim.x;
   const int64_t batch = (int64_t)STEP_SB * nth;
   const int64_t nbatches = (a.n + batch - 1) / batch;
-  auto issue = [&](int64_t bi, int buf) {
+  char* smem = reinterpret_cast<char*>(pf_gtab);
+  const size_t buf_bytes = (size_t)STEP_SB * nth * (sizeof(Rec) + 3 * sizeof(double));
+  auto rec_at = [&](int buf, int b) {
+    return reinterpret_cast<Rec*>(smem + buf * buf_bytes) + b * nth + threadIdx.x;
+  };
+  auto val_at = [&](int buf, int k, int b) {
+    return reinterpret_cast<double*>(smem + buf * buf_bytes + (size_t)STEP_SB * nth * sizeof(Rec)) +
+           (k * STEP_SB + b) * nth + threadIdx.x;
+  };
+  // resampling words are loaded one pipeline stage ahead of their lookups
+  auto load_w3 = [&](int64_t bi, uint64_t (&w3)[STEP_SB]) {
+#pragma unroll
+    for (int b = 0; b < STEP_SB; ++b) {
+      const int64_t j = bi * batch + b * (int64_t)nth + threadIdx.x;
+      w3[b] = (a.t > 1 && bi < nbatches && j < a.n) ? __ldcs(a.u3 + j) : 0ull;
+    }
+  };
+  auto issue = [&](int64_t bi, int buf, const uint64_t (&w3)[STEP_SB]) {
     int64_t jj[STEP_SB], anc[STEP_SB];
     bool ok[STEP_SB];
 #pragma unroll
@@ -262,9 +320,6 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
       anc[b] = jj[b];
     }
     if (a.t > 1) {
-      uint64_t w3[STEP_SB];
-#pragma unroll
-      for (int b = 0; b < STEP_SB; ++b) w3[b] = ok[b] ? __ldcs(a.u3 + jj[b]) : 0ull;
       ancestors_of<TQ, STEP_SB>(a.lk, w3, ok, anc);
       if (a.idx_out) {
 #pragma unroll
@@ -275,29 +330,36 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
 #pragma unroll
     for (int b = 0; b < STEP_SB; ++b) {
       if (!ok[b]) continue;
-      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(stage + ((size_t)buf * STEP_SB + b) * nth + threadIdx.x);
-      const Rec* src = a.rec_in + anc[b];
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16), "l"(reinterpret_cast<const char*>(src) + 16));
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(rec_at(buf, b));
+      const char* src = reinterpret_cast<const char*>(a.rec_in + anc[b]);
+      cp_async16(dst, src);
+      cp_async16(dst + 16, src + 16);
+      cp_async8((uint32_t)__cvta_generic_to_shared(val_at(buf, 0, b)), a.z + jj[b]);
+      if (LS) cp_async8((uint32_t)__cvta_generic_to_shared(val_at(buf, 1, b)), a.g_s + jj[b]);
+      if (LT) cp_async8((uint32_t)__cvta_generic_to_shared(val_at(buf, 2, b)), a.g_t + jj[b]);
     }
     asm volatile("cp.async.commit_group;");
   };
   int cur = 0;
   int64_t bi = blockIdx.x;
-  if (bi < nbatches) issue(bi, 0);
+  uint64_t w3n[STEP_SB];
+  load_w3(bi, w3n);
+  if (bi < nbatches) issue(bi, 0, w3n);
+  load_w3(bi + gridDim.x, w3n);
   for (; bi < nbatches; bi += gridDim.x) {
-    if (bi + gridDim.x < nbatches) issue(bi + gridDim.x, cur ^ 1);
-    else asm volatile("cp.async.commit_group;");
+    if (bi + gridDim.x < nbatches) {
+      issue(bi + gridDim.x, cur ^ 1, w3n);
+      load_w3(bi + 2 * (int64_t)gridDim.x, w3n);
+    } else {
+      asm volatile("cp.async.commit_group;");
+    }
     asm volatile("cp.async.wait_group 1;" ::: "memory");
 #pragma unroll 1
   for (int b = 0; b < STEP_SB; ++b) {
     const int64_t j = bi * batch + b * (int64_t)nth + threadIdx.x;
     if (j >= a.n) continue;
-    const Rec r = stage[((size_t)cur * STEP_SB + b) * nth + threadIdx.x];
-    // ---- propagate with Philox block t of stream j
-    const Philox4 P = philox_block(a.seed, (uint64_t)j, (uint64_t)a.t);
-    a.u3[j] = P.w[3];
-    const double z = a.feed_z ? a.feed_z[j] : ndtri(unit_open(P.w[0]));
+    const Rec r = *rec_at(cur, b);
+    const double z = *val_at(cur, 0, b);
     const double sq = LT ? sqrt(r.tau2) : a.sqrt_tau2_fixed;
     const double step = sq * z;
     double xn = r.x + step;
@@ -311,13 +373,11 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
     double s2 = a.sigma2_fixed, t2 = a.tau2_fixed;
     if (LS) {
       o.bs = r.bs + h;
-      const double g = a.feed_gs ? a.feed_gs[j] : gamma_draw_slot(gs, slot_s, unit_open(P.w[1]));
-      s2 = o.bs / g;
+      s2 = o.bs / *val_at(cur, 1, b);
     }
     if (LT) {
       o.bt = r.bt + (0.5 * step) * step;
-      const double g = a.feed_gt ? a.feed_gt[j] : gamma_draw_slot(gt, slot_t, unit_open(P.w[2]));
-      t2 = o.bt / g;
+      t2 = o.bt / *val_at(cur, 2, b);
     }
     o.tau2 = t2;
     a.rec_out[j] = o;

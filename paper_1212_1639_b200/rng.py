@@ -62,13 +62,15 @@ def uniforms_at(seed, stream_ids, counters):
     return out.reshape(shape)
 
 
-def ndtri(u):
-    """Standard-normal quantile on the device (Cephes restatement of the
-    scipy.special.ndtri the reference calls, rng.py:223-224)."""
+def ndtri(u, method="exact"):
+    """Standard-normal quantile on the device (scipy.special.ndtri as the
+    reference calls it, rng.py:223-224).  ``method="exact"`` is the Cephes
+    restatement, ``"table"`` the piecewise table the hot path evaluates."""
     u = np.ascontiguousarray(np.asarray(u, dtype=np.float64))
     out = np.empty_like(u)
     lib = _lib.require_device()
-    _lib.check(lib.pf_ndtri(_lib.ptr(u.reshape(-1)), u.size, _lib.ptr(out.reshape(-1))), lib)
+    fn = lib.pf_ndtri if method == "exact" else lib.pf_ndtri_table
+    _lib.check(fn(_lib.ptr(u.reshape(-1)), u.size, _lib.ptr(out.reshape(-1))), lib)
     return out
 
 

@@ -1,5 +1,5 @@
 """Per-CUDA-source-line instruction / stall totals of one kernel in an ncu
-report (page source, cuda,sass): ncu_lines.py rep [top]"""
+report (page source, cuda,sass): ncu_lines.py rep [top] [function-substring]"""
 import csv
 import io
 import subprocess
@@ -7,10 +7,16 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+fsub = sys.argv[3] if len(sys.argv) > 3 else ""
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
                      capture_output=True, text=True).stdout
-fname, hdr, rows = None, None, []
+fname, hdr, rows, func = None, None, [], ""
 for r in csv.reader(io.StringIO(out)):
+    if len(r) >= 2 and r[0] == "Function Name":
+        func = r[1]
+        continue
+    if fsub not in func:
+        continue
     if len(r) >= 2 and r[0] == "File Path":
         fname = r[1].split("/")[-1]
         continue
@@ -19,7 +25,7 @@ for r in csv.reader(io.StringIO(out)):
         continue
     if hdr and r and r[0] not in ("", "Function Name") and len(r) == len(hdr):
         d = dict(zip(hdr, r))
-        rows.append((fname, d))
+        rows.append((fname or "?", d))
 ie = "Instructions Executed"
 ws = "Warp Stall Sampling (All Samples)"
 ti = sum(float(d[ie] or 0) for _, d in rows)

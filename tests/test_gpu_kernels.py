@@ -68,6 +68,24 @@ def test_ndtri_vs_scipy(gpu):
     assert ulp.max() <= 2, ulp.max()
 
 
+def test_ndtri_table_vs_scipy(gpu):
+    """The hot-path normal draw (u-space table) against scipy's ndtri."""
+    d = golden("special")
+    u, want = d["u"], d["ndtri"]
+    got = prng.ndtri(u, method="table")
+    err = np.abs(got - want)
+    # the table is within ~1 ulp of the exact quantile (fitted at 50 digits,
+    # scripts/gen_ndtri_table.py); scipy's Cephes itself is up to 3 ulp off
+    tol = np.maximum(5 * np.spacing(np.abs(want)), 1e-17)
+    assert (err <= tol).all(), float((err / tol).max())
+    # odd symmetry about 1/2 and the extremes of the open unit interval
+    v = np.array([2.0 ** -53, 1 - 2.0 ** -53, 0.5 - 2.0 ** -53, 0.5 + 2.0 ** -53, 0.25, 0.75])
+    from scipy.special import ndtri as sp_ndtri  # noqa: F401  (host-side check only)
+    g = prng.ndtri(v, method="table")
+    assert np.allclose(g, sp_ndtri(v), rtol=4e-16, atol=1e-17)
+    assert g[0] == -g[1] and g[2] == -g[3]
+
+
 @pytest.mark.parametrize("method", ["table", "accurate"])
 def test_gammaincinv_vs_scipy(gpu, method):
     d = golden("special")
