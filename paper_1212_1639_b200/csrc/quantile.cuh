@@ -435,6 +435,30 @@ PF_D void q_make_regions(const QWin& win, QRegions& rg) {
 // TREE = false: the classification alone (side stream), persistent over
 // tiles (R = number of tiles); TREE = true: fused into K2 (one chunk of R
 // tiles per CTA, with the exact subtree sums).
+// Flush of a CTA buffer filled by warp-compacted appends: per-target
+// positions by shared atomics, one global atomic per target, then the copy.
+// Called by all threads.
+PF_D void q_flush_compact(const QArgs& qa, QAgg& agg) {
+  __syncthreads();
+  const int nfill = min(agg.fill, Q_AGG);
+  for (int s = threadIdx.x; s < nfill; s += blockDim.x) agg.pos[s] = atomicAdd(&agg.cnt[agg.tk[s]], 1u);
+  __syncthreads();
+  if (threadIdx.x < Q_MAXT) {
+    const uint32_t c = agg.cnt[threadIdx.x];
+    agg.base[threadIdx.x] = c ? atomicAdd(&qa.tg[threadIdx.x].count, c) : 0u;
+  }
+  __syncthreads();
+  for (int s = threadIdx.x; s < nfill; s += blockDim.x) {
+    const int k = agg.tk[s];
+    const uint32_t pos = agg.base[k] + agg.pos[s];
+    if (pos < qa.cap) qa.cand[(size_t)k * qa.cap + pos] = agg.c[s];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) agg.fill = 0;
+  if (threadIdx.x < Q_MAXT) agg.cnt[threadIdx.x] = 0;
+  __syncthreads();
+}
+
 template <typename T, int QM, bool TREE>
 __global__ void __launch_bounds__(CDF_THREADS)
 cdf_reduce_qr_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ chunk_tot,
@@ -452,22 +476,23 @@ cdf_reduce_qr_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ 
     const int qi = __popc((unsigned)QM & ((1u << q) - 1u));
     return rsum[(qi * NR + r) * CDF_THREADS + threadIdx.x];
   };
+  __shared__ uint32_t sb[Q_MAXQ][16];  // sorted bounds padded to 15 (+1) for the binary search
   q_agg_init(agg);
   q_make_windows(qa, win);
   q_make_regions(win, rg);
+  if (threadIdx.x < Q_MAXQ * 16) {
+    const int q = threadIdx.x >> 4, i = threadIdx.x & 15;
+    sb[q][i] = i < 2 * Q_PER ? rg.b[q][i] : 0xFFFFFFFFu;
+  }
 #pragma unroll
   for (int q = 0; q < Q_MAXQ; ++q)
     if (QM & (1 << q))
 #pragma unroll
       for (int r = 0; r < NR; ++r) RS(q, r) = 0.0;
+  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double M = src.mode == 0 ? *src.M : 0.0;
   const int64_t chunk = blockIdx.x;
-  uint32_t bnd[Q_MAXQ][2 * Q_PER];
-#pragma unroll
-  for (int q = 0; q < Q_MAXQ; ++q)
-#pragma unroll
-    for (int i = 0; i < 2 * Q_PER; ++i) bnd[q][i] = rg.b[q][i];
   double wsum = 0.0;
   const int nloop = TREE ? R : (int)((R - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x);
   for (int r = 0; r < nloop; ++r) {
@@ -494,53 +519,63 @@ cdf_reduce_qr_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ 
 #pragma unroll
       for (int q = 0; q < Q_MAXQ; ++q) {
         if (!(QM & (1 << q))) continue;
-        int rr = 0;
-#pragma unroll
-        for (int i = 0; i < 2 * Q_PER; ++i) rr += key[q][e] >= bnd[q][i];
+        // #{bounds <= key}: branch-free binary search over 15 sorted bounds
+        const uint32_t kk = key[q][e];
+        int rr = kk >= sb[q][7] ? 8 : 0;
+        rr += kk >= sb[q][rr + 3] ? 4 : 0;
+        rr += kk >= sb[q][rr + 1] ? 2 : 0;
+        rr += kk >= sb[q][rr] ? 1 : 0;
+        rr = rr < 2 * Q_PER ? rr : 2 * Q_PER;
         RS(q, rr) += w;
         inw[e] |= (uint32_t)rg.inmask[q][rr];
       }
       anyin |= inw[e];
     }
-    // candidates (rare): warp-aggregated appends, as in q_classify
-    if (__any_sync(0xffffffffu, anyin != 0u)) {
+    // candidates: one warp-wide scan and one shared atomic per warp per tile
+    // reserve the buffer; per-target positions are assigned at the flush
+    {
+      int mine = 0;
 #pragma unroll
-      for (int e = 0; e < CDF_V; ++e) {
-        uint32_t any = __reduce_or_sync(0xffffffffu, inw[e]);
-        while (any) {
-          const int sl = __ffs(any) - 1;
-          any &= any - 1;
-          const int q = sl / Q_PER;
-          const int tq = win.base[q] + (sl - q * Q_PER);
-          const unsigned m = __ballot_sync(0xffffffffu, (inw[e] >> sl) & 1u);
-          const int leader = __ffs(m) - 1;
-          int slot = 0;
-          uint32_t kpos = 0;
-          if (lane == leader) {
-            slot = atomicAdd(&agg.fill, __popc(m));
-            if (slot + __popc(m) <= Q_AGG) kpos = atomicAdd(&agg.cnt[tq], (uint32_t)__popc(m));
-            else kpos = 0x80000000u | atomicAdd(&qa.tg[tq].count, (uint32_t)__popc(m));
-          }
-          slot = __shfl_sync(0xffffffffu, slot, leader);
-          kpos = __shfl_sync(0xffffffffu, kpos, leader);
-          if ((inw[e] >> sl) & 1u) {
-            const uint32_t rank = __popc(m & ((1u << lane) - 1u));
+      for (int e = 0; e < CDF_V; ++e) mine += __popc(inw[e]);
+      int incl = mine;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int tq = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += tq;
+      }
+      const int wtot = __shfl_sync(0xffffffffu, incl, 31);
+      if (wtot) {
+        int wb = 0;
+        if (lane == 31) wb = atomicAdd(&agg.fill, wtot);
+        wb = __shfl_sync(0xffffffffu, wb, 31);
+        int pos = wb + incl - mine;
+#pragma unroll
+        for (int e = 0; e < CDF_V; ++e) {
+          uint32_t mk = inw[e];
+          while (mk) {
+            const int sl = __ffs(mk) - 1;
+            mk &= mk - 1;
+            const int q = sl / Q_PER;
+            const int tq = win.base[q] + (sl - q * Q_PER);
             QCand c;
             c.key = q == 0 ? key[0][e] : (q == 1 ? key[1][e] : key[2][e]);
             c.idx = (uint32_t)(base + e);
             c.w = (double)v[e];
-            if (kpos & 0x80000000u) {
-              const uint32_t pos = (kpos & 0x7FFFFFFFu) + rank;
-              if (pos < qa.cap) qa.cand[(size_t)tq * qa.cap + pos] = c;
-              if (slot + (int)rank < Q_AGG) agg.tk[slot + rank] = 0xFF;  // reserved, unused
-            } else {
-              agg.c[slot + rank] = c;
-              agg.tk[slot + rank] = (uint8_t)tq;
-              agg.pos[slot + rank] = kpos + rank;
+            if (pos < Q_AGG) {
+              agg.c[pos] = c;
+              agg.tk[pos] = (uint8_t)tq;
+            } else {  // buffer full: straight to the global list
+              const uint32_t gp = atomicAdd(&qa.tg[tq].count, 1u);
+              if (gp < qa.cap) qa.cand[(size_t)tq * qa.cap + gp] = c;
             }
+            ++pos;
           }
         }
       }
+    }
+    if (!TREE) {
+      __syncthreads();
+      if (agg.fill > Q_AGG / 2) q_flush_compact(qa, agg);
     }
     if (TREE) {
       thread_tree8<T>(v, l1, l2, g);
@@ -585,7 +620,7 @@ cdf_reduce_qr_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ 
       acc[q * Q_PER + k] = a;
     }
   }
-  q_flush(qa, agg);
+  q_flush_compact(qa, agg);
   q_reduce_partials(qa, win, acc, wsum);
 }
 
