@@ -768,6 +768,8 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     a.out.t_mean = e->o_tm.p;
     a.out.t_sd = e->o_tsd.p;
     a.fail = e->fail.p;
+    a.xrec = nullptr;
+    a.shard = 0;
     if (rs.resident) {
       cudaEvent_t b0, b1;
       cudaEventCreate(&b0);

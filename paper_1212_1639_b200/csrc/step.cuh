@@ -178,6 +178,8 @@ struct StepArgs {
   Scalars* sc;
   StepOut out;
   int64_t* fail;
+  Partial* xrec;         // sharded run: shard partials [G] (null: single run)
+  int shard;
 };
 
 PF_D double warp_sum(double v) {
@@ -189,6 +191,100 @@ PF_D double warp_max(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
+}
+
+// Combine `count` partials (each rescaled to its own max) in a fixed order:
+// M = max (NaN when any partial saw a NaN / +inf log-weight), S = sums
+// rescaled to M.  Called by all threads of one CTA; results in thread 0.
+PF_D void reduce_partials(const Partial* p, int count, double (*red)[8], double& M_out, double& bad_out,
+                          double (&S)[7]) {
+  __shared__ double mfin;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double M = -INFINITY, badsum = 0.0;
+  for (int b = threadIdx.x; b < count; b += blockDim.x) {
+    M = fmax(M, __ldcg(&p[b].m));
+    badsum += __ldcg(&p[b].bad);
+  }
+  M = warp_max(M);
+  badsum = warp_sum(badsum);
+  __syncthreads();
+  if (lane == 0) { red[warp][0] = M; red[warp][1] = badsum; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mm = red[0][0], bb = red[0][1];
+    for (int w = 1; w < nw; ++w) { mm = fmax(mm, red[w][0]); bb += red[w][1]; }
+    mfin = (bb > 0.0) ? NAN : mm;
+    bad_out = bb;
+  }
+  __syncthreads();
+  M = mfin;
+  double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int b = threadIdx.x; b < count; b += blockDim.x) {
+    const double mb2 = __ldcg(&p[b].m);
+    const double f = (mb2 == -INFINITY) ? 0.0 : exp(mb2 - M);
+    acc[0] += f * __ldcg(&p[b].s0);
+    acc[1] += f * __ldcg(&p[b].sx);
+    acc[2] += f * __ldcg(&p[b].s2x);
+    acc[3] += f * __ldcg(&p[b].s1s);
+    acc[4] += f * __ldcg(&p[b].s2s);
+    acc[5] += f * __ldcg(&p[b].s1t);
+    acc[6] += f * __ldcg(&p[b].s2t);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 7; ++k) {
+    const double sv = warp_sum(acc[k]);
+    if (lane == 0) red[warp][k] = sv;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 7; ++k) S[k] = 0.0;
+    for (int w = 0; w < nw; ++w)
+      for (int k = 0; k < 7; ++k) S[k] += red[w][k];
+    M_out = M;
+  }
+}
+
+// Step t's summaries from the combined sums (filtering.py:344-355), the
+// moment shifts of the next step, the max log-weight and the degeneracy
+// check (filtering.py:294-296).  One thread.
+template <bool LS, bool LT>
+PF_D void finalize_step(int64_t t, double M, double bsum, const double (&S)[7], bool feedw, double cs,
+                        double ct, double cx, const StepOut& out, double* qmom, Scalars* sc, double* Mout,
+                        int64_t* fail) {
+  (void)bsum;
+  const int64_t i = t - 1;
+  const double W = S[0];
+  const double fm = S[1] / W;
+  out.fmean[i] = fm;
+  {
+    const double d = fm - cx;
+    const double var = S[2] / W - d * d;
+    if (qmom) { qmom[0] = fm; qmom[3] = sqrt(fmax(var, 0.0)); }
+    sc->cx = fm;
+  }
+  if (LS) {
+    const double d = S[3] / W;
+    const double var = S[4] / W - d * d;
+    out.s_mean[i] = cs + d;
+    out.s_sd[i] = sqrt(fmax(var, 0.0));
+    sc->cs = cs + d;
+    if (qmom) { qmom[1] = cs + d; qmom[4] = out.s_sd[i]; }
+  }
+  if (LT) {
+    const double d = S[5] / W;
+    const double var = S[6] / W - d * d;
+    out.t_mean[i] = ct + d;
+    out.t_sd[i] = sqrt(fmax(var, 0.0));
+    sc->ct = ct + d;
+    if (qmom) { qmom[2] = ct + d; qmom[5] = out.t_sd[i]; }
+  }
+  sc->M = feedw ? 0.0 : M;
+  *Mout = feedw ? 0.0 : M;
+  sc->W = W;
+  sc->counter = 0;
+  if (!feedw && !(M > -INFINITY && M < INFINITY))
+    atomicCAS((unsigned long long*)fail, 0ull, (unsigned long long)t);
 }
 
 // ---------------------------------------------------------------- draws ---
@@ -467,81 +563,38 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
 
   // ---- last CTA: combine the partials (fixed order -> deterministic)
   __threadfence();
-  const int G = gridDim.x;
-  double M = -INFINITY, badsum = 0.0;
-  for (int b = threadIdx.x; b < G; b += blockDim.x) {
-    const double mb2 = __ldcg(&a.partials[b].m);
-    M = fmax(M, mb2);
-    badsum += __ldcg(&a.partials[b].bad);
-  }
-  M = warp_max(M);
-  badsum = warp_sum(badsum);
-  __syncthreads();
-  if (lane == 0) { red[warp][0] = M; red[warp][1] = badsum; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double mm = red[0][0], bb = red[0][1];
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { mm = fmax(mm, red[w][0]); bb += red[w][1]; }
-    mblk = (bb > 0.0) ? NAN : mm;
-  }
-  __syncthreads();
-  M = mblk;
-  double acc[7] = {0, 0, 0, 0, 0, 0, 0};
-  for (int b = threadIdx.x; b < G; b += blockDim.x) {
-    const double mb2 = __ldcg(&a.partials[b].m);
-    const double f = (mb2 == -INFINITY) ? 0.0 : exp(mb2 - M);
-    acc[0] += f * __ldcg(&a.partials[b].s0);
-    acc[1] += f * __ldcg(&a.partials[b].sx);
-    acc[2] += f * __ldcg(&a.partials[b].s2x);
-    acc[3] += f * __ldcg(&a.partials[b].s1s);
-    acc[4] += f * __ldcg(&a.partials[b].s2s);
-    acc[5] += f * __ldcg(&a.partials[b].s1t);
-    acc[6] += f * __ldcg(&a.partials[b].s2t);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < 7; ++k) {
-    const double s = warp_sum(acc[k]);
-    if (lane == 0) red[warp][k] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double S[7] = {0, 0, 0, 0, 0, 0, 0};
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
-      for (int k = 0; k < 7; ++k) S[k] += red[w][k];
-    const int64_t i = a.t - 1;
-    const double W = S[0];
-    const double fm = S[1] / W;
-    a.out.fmean[i] = fm;
-    {
-      const double d = fm - cx;
-      const double var = S[2] / W - d * d;
-      if (a.qmom) { a.qmom[0] = fm; a.qmom[3] = sqrt(fmax(var, 0.0)); }
-      a.sc->cx = fm;
-    }
-    if (LS) {
-      const double d = S[3] / W;
-      const double var = S[4] / W - d * d;
-      a.out.s_mean[i] = cs + d;
-      a.out.s_sd[i] = sqrt(fmax(var, 0.0));
-      a.sc->cs = cs + d;
-      if (a.qmom) { a.qmom[1] = cs + d; a.qmom[4] = a.out.s_sd[i]; }
-    }
-    if (LT) {
-      const double d = S[5] / W;
-      const double var = S[6] / W - d * d;
-      a.out.t_mean[i] = ct + d;
-      a.out.t_sd[i] = sqrt(fmax(var, 0.0));
-      a.sc->ct = ct + d;
-      if (a.qmom) { a.qmom[2] = ct + d; a.qmom[5] = a.out.t_sd[i]; }
-    }
-    a.sc->M = feedw ? 0.0 : M;
-    *a.Mout = feedw ? 0.0 : M;
-    a.sc->W = W;
+  double M, bsum, S[7];
+  reduce_partials(a.partials, (int)gridDim.x, red, M, bsum, S);
+  if (threadIdx.x != 0) return;
+  if (a.xrec) {
+    // sharded run: this shard's partial goes to the exchange array; the
+    // combine kernel finalises the step from all shards' partials
+    Partial p;
+    p.m = M;
+    p.s0 = S[0]; p.sx = S[1]; p.s2x = S[2]; p.s1s = S[3]; p.s2s = S[4]; p.s1t = S[5]; p.s2t = S[6];
+    p.bad = bsum;
+    a.xrec[a.shard] = p;
+    __threadfence_system();
     a.sc->counter = 0;
-    if (!feedw && !(M > -INFINITY && M < INFINITY))
-      atomicCAS((unsigned long long*)a.fail, 0ull, (unsigned long long)a.t);
+    return;
   }
+  finalize_step<LS, LT>(a.t, M, bsum, S, feedw, cs, ct, cx, a.out, a.qmom, a.sc, a.Mout, a.fail);
+}
+
+// Sharded run: every shard finalises step t from the G shard partials (the
+// same fixed-order combination, so all shards hold identical M / shifts).
+template <int MODE>
+__global__ void __launch_bounds__(256) combine_kernel(const Partial* __restrict__ xrec, int G, int64_t t,
+                                                      int feedw, StepOut out, double* qmom, Scalars* sc,
+                                                      double* Mout, int64_t* fail) {
+  constexpr bool LS = MODE & M_LS, LT = MODE & M_LT;
+  if (*fail) return;
+  __shared__ double red[8][8];
+  const double cs = sc->cs, ct = sc->ct, cx = sc->cx;
+  double M, bsum, S[7];
+  reduce_partials(xrec, G, red, M, bsum, S);
+  if (threadIdx.x != 0) return;
+  finalize_step<LS, LT>(t, M, bsum, S, feedw != 0, cs, ct, cx, out, qmom, sc, Mout, fail);
 }
 
 // -------------------------------------------------------- materialize ---
