@@ -144,6 +144,21 @@ int pf_engine_last_timing(pf_engine* e, double* total_ms, double* step_kernel_ms
 int pf_engine_quantile_stats(pf_engine* e, int64_t* stats4);
 int pf_engine_destroy(pf_engine* e);
 
+/* ----------------------------------------- sharded run (multi-GPU) --- */
+/* One filter of cfg->n particles split into nshards (1, 2, 4, 8) shards of
+ * n/nshards consecutive slots, shard s on devices[s] (NULL: all on device 0;
+ * distinct devices need P2P access, e.g. NVLink / NVSwitch).  Same drop-in
+ * boundary as pf_engine_run (filtering.py:200-374) and bit-identical to it
+ * in ancestors and particles; the per-step exchange is one partial record
+ * and one subtree total per shard, plus the cross-shard resampling reads.
+ * Oracle feeds and store_particles are not supported. */
+typedef struct pf_group pf_group;
+int pf_group_create(const pf_config* cfg, int32_t nshards, const int32_t* devices, pf_group** out);
+int pf_group_reconfigure(pf_group* g, const pf_config* cfg);
+int pf_group_run(pf_group* g, const double* y, int64_t t_len, pf_outputs* out);
+int pf_group_last_timing(pf_group* g, double* total_ms);
+int pf_group_destroy(pf_group* g);
+
 /* ------------------------------------------------- kernel level (L2) --- */
 /* All kernel-level entries take HOST pointers and run synchronously on the
  * current device; they exist for parity tests and for the reference's

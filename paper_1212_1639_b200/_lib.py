@@ -89,6 +89,11 @@ SIGNATURES = {
     "pf_engine_last_timing": (C.c_int, [C.c_void_p, _dp, _dp, _i64p, _i64p]),
     "pf_engine_quantile_stats": (C.c_int, [C.c_void_p, _i64p]),
     "pf_engine_destroy": (C.c_int, [C.c_void_p]),
+    "pf_group_create": (C.c_int, [C.POINTER(PfConfig), C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_void_p)]),
+    "pf_group_reconfigure": (C.c_int, [C.c_void_p, C.POINTER(PfConfig)]),
+    "pf_group_run": (C.c_int, [C.c_void_p, _dp, C.c_int64, C.POINTER(PfOutputs)]),
+    "pf_group_last_timing": (C.c_int, [C.c_void_p, _dp]),
+    "pf_group_destroy": (C.c_int, [C.c_void_p]),
     "pf_philox_block": (C.c_int, [C.c_uint64, _u64p, C.c_int64, C.c_uint64, _u64p]),
     "pf_philox4x64": (C.c_int, [_u64p, _u64p, C.c_int64, _u64p]),
     "pf_uniforms_at": (C.c_int, [C.c_uint64, _u64p, _u64p, C.c_int64, _dp]),

@@ -30,17 +30,33 @@ class Backend:
         Kept for API compatibility (``split``).
     device : int
         CUDA device ordinal.
+    shards : int
+        Split one filter's particles into this many shards (1, 2, 4, 8) of
+        consecutive slots -- the multi-GPU run of SURVEY §8e.  Results are
+        bit-identical to one shard in ancestors and particles.
+    devices : sequence of int, optional
+        Device of each shard (default: all on ``device``); distinct devices
+        must have peer access (NVLink / NVSwitch).
     """
 
-    def __init__(self, mode="cuda", lanes=1, min_chunk=4096, device=0):
+    def __init__(self, mode="cuda", lanes=1, min_chunk=4096, device=0, shards=1, devices=None):
         if mode not in MODES:
             raise ValueError(f"unknown backend mode: {mode!r}")
         if lanes < 1:
             raise ValueError("lanes must be >= 1")
+        shards = int(shards)
+        if shards not in (1, 2, 4, 8):
+            raise ValueError("shards must be 1, 2, 4 or 8")
+        if devices is not None:
+            devices = [int(d) for d in devices]
+            if len(devices) != shards:
+                raise ValueError("devices must list one device per shard")
         self.mode = mode
         self.lanes = lanes if mode == "parallel" else 1
         self.min_chunk = min_chunk
         self.device = int(device)
+        self.shards = shards
+        self.devices = devices if devices is not None else [self.device] * shards
         self._engines = {}
 
     def split(self, n):
@@ -82,7 +98,8 @@ class Backend:
             pass
 
     def __repr__(self):
-        return f"Backend(mode={self.mode!r}, lanes={self.lanes}, device={self.device})"
+        return (f"Backend(mode={self.mode!r}, lanes={self.lanes}, device={self.device}, "
+                f"shards={self.shards})")
 
 
 def device_available():

@@ -294,7 +294,7 @@ cdf_expand_kernel(WSrc src, int64_t n, int R, const T* __restrict__ tile_tot,
                   const T* __restrict__ node, const T* __restrict__ carry,
                   const T* __restrict__ total_p, T* __restrict__ q_out,
                   int32_t* __restrict__ cut_out, const int64_t* __restrict__ fail,
-                  RankOut ro = RankOut()) {
+                  RankOut ro = RankOut(), int64_t gbase = 0) {
   if (fail && *fail) return;
   __shared__ T wt[CDF_THREADS / 32];
   __shared__ T wmax[CDF_THREADS / 32];
@@ -411,11 +411,11 @@ cdf_expand_kernel(WSrc src, int64_t n, int R, const T* __restrict__ tile_tot,
 #pragma unroll
     for (int i = 0; i < CDF_V; ++i) {
       T qi = clip01(fmax(pre, run[i]));
-      if (base + i == n - 1) qi = (T)1;
+      if (gbase + base + i == n - 1) qi = (T)1;
       qv[i] = qi;
       const int64_t L = (int64_t)ceil(qi * nf);
       int32_t* ct = STRATA ? ro.cut : cut_out;
-      for (int64_t kk = Lprev; kk < L; ++kk) ct[kk] = (int32_t)(base + i);
+      for (int64_t kk = Lprev; kk < L; ++kk) ct[kk] = (int32_t)(gbase + base + i);
       if (STRATA) {
         const uint32_t f = strata_f<T>(qi, L, ro.B);
         fx[i] = f;
@@ -435,6 +435,161 @@ cdf_expand_kernel(WSrc src, int64_t n, int R, const T* __restrict__ tile_tot,
     }
     __syncthreads();
   }
+}
+
+// ------------------------------------------------ sharded (multi-GPU) ---
+// G shards of N/G consecutive particles: each shard is a subtree of the
+// reference's adder tree, so the run is bit-identical to one device.
+//   K3a cdf_shard_total: the shard's subtree total (forward tree over its
+//       chunk totals) -> the exchange array (one value per shard);
+//   K3b cdf_top_shard: every shard rebuilds the G-level top tree from the
+//       exchanged totals (root = the reference's total), runs the backward
+//       adder down to all shard nodes, then down its own chunks; the carry
+//       into a shard is the running max of the shard nodes before it (a
+//       node never exceeds its parent, so a shard's largest prefix is its
+//       node); and the stratum boundaries L_end of every shard for the
+//       cross-shard cut-point lookup.
+constexpr int PF_MAX_SHARDS = 8;
+
+template <typename T>
+__global__ void __launch_bounds__(1024)
+cdf_shard_total_kernel(const T* __restrict__ chunk_tot, int64_t C, T* __restrict__ xtot, int shard,
+                       const int64_t* fail) {
+  if (fail && *fail) return;
+  extern __shared__ unsigned char smem_raw[];
+  T* fw = reinterpret_cast<T*>(smem_raw);  // 2C
+  for (int64_t i = threadIdx.x; i < C; i += blockDim.x) fw[i] = chunk_tot[i];
+  __syncthreads();
+  int64_t off = 0, len = C;
+  while (len > 1) {
+    for (int64_t i = threadIdx.x; i < len / 2; i += blockDim.x) fw[off + len + i] = fw[off + 2 * i] + fw[off + 2 * i + 1];
+    __syncthreads();
+    off += len;
+    len >>= 1;
+  }
+  if (threadIdx.x == 0) {
+    xtot[shard] = fw[off];
+    __threadfence_system();
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024)
+cdf_top_shard_kernel(const T* __restrict__ chunk_tot, int64_t C, const T* __restrict__ xtot, int G, int shard,
+                     int64_t n_total, T* __restrict__ node, T* __restrict__ carry, T* __restrict__ total_out,
+                     int64_t* __restrict__ lend, int64_t* fail, int64_t step) {
+  if (fail && *fail) return;
+  extern __shared__ unsigned char smem_raw[];
+  T* fw = reinterpret_cast<T*>(smem_raw);  // forward levels of the chunk tree, 2C
+  T* b0 = fw + 2 * C;
+  T* b1 = b0 + C;
+  __shared__ T snode[PF_MAX_SHARDS];
+  __shared__ T sroot, scarry;
+  // top tree over the G shard totals, backward to the shard nodes (thread 0)
+  if (threadIdx.x == 0) {
+    T lv[2 * PF_MAX_SHARDS];
+    for (int g = 0; g < G; ++g) lv[g] = __ldcg(&xtot[g]);
+    int offs[4], k = 0, off = 0, len = G;
+    offs[k++] = 0;
+    while (len > 1) {
+      for (int i = 0; i < len / 2; ++i) lv[off + len + i] = lv[off + 2 * i] + lv[off + 2 * i + 1];
+      off += len;
+      len >>= 1;
+      offs[k++] = off;
+    }
+    const T root = lv[off];
+    T bw[PF_MAX_SHARDS], nb[PF_MAX_SHARDS];
+    bw[0] = root;
+    int plen = 1;
+    for (int lvl = k - 2; lvl >= 0; --lvl) {
+      const int co = offs[lvl];
+      for (int i = 0; i < plen * 2; ++i) nb[i] = (i & 1) ? bw[i >> 1] : (T)(bw[i >> 1] - lv[co + i + 1]);
+      plen *= 2;
+      for (int i = 0; i < plen; ++i) bw[i] = nb[i];
+    }
+    // carries (exclusive running max of shard nodes) and stratum bounds
+    T m = (T)(-INFINITY);
+    const T nf = (T)n_total;
+    for (int g = 0; g < G; ++g) {
+      snode[g] = bw[g];
+      if (g == shard) scarry = m;
+      m = fmax(m, bw[g]);
+      const T qe = (g == G - 1) ? (T)1 : clip01(m / root);
+      lend[g] = (int64_t)ceil(qe * nf);
+    }
+    sroot = root;
+    *total_out = root;
+    if (!(root > (T)0) || !isfinite((double)root)) {
+      if (fail) atomicCAS((unsigned long long*)fail, 0ull, (unsigned long long)(-step));
+    }
+  }
+  // forward tree over this shard's chunk totals
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int64_t i = tid; i < C; i += nt) fw[i] = chunk_tot[i];
+  __syncthreads();
+  int64_t off = 0, len = C;
+  while (len > 1) {
+    for (int64_t i = tid; i < len / 2; i += nt) fw[off + len + i] = fw[off + 2 * i] + fw[off + 2 * i + 1];
+    __syncthreads();
+    off += len;
+    len >>= 1;
+  }
+  // backward from the shard node
+  T* par = b0;
+  T* chi = b1;
+  if (tid == 0) par[0] = snode[shard];
+  __syncthreads();
+  int64_t plen = 1, loff = off;
+  while (plen < C) {
+    const int64_t clen = plen * 2, coff = loff - clen;
+    for (int64_t i = tid; i < clen; i += nt) {
+      const T pv = par[i >> 1];
+      chi[i] = (i & 1) ? pv : (T)(pv - fw[coff + i + 1]);
+    }
+    __syncthreads();
+    T* tmp = par;
+    par = chi;
+    chi = tmp;
+    plen = clen;
+    loff = coff;
+  }
+  for (int64_t i = tid; i < C; i += nt) node[i] = par[i];
+  // chunk carries: running max seeded with the shard carry (serial over the
+  // shard's chunks: C <= 4096)
+  __syncthreads();
+  if (tid == 0) {
+    T m = scarry;
+    for (int64_t i = 0; i < C; ++i) {
+      carry[i] = m;
+      m = fmax(m, par[i]);
+    }
+  }
+  (void)sroot;
+}
+
+// Cross-shard cut-point lookup (resampling.py:146-158): the stratum's owner
+// shard from the L_end bounds, I_s from its cut table, then the advance
+// over q(k) wherever particle k lives.
+template <typename TQ>
+struct ShardLookup {
+  const int32_t* cut[PF_MAX_SHARDS];  // full-size (N) per shard, own strata written
+  const TQ* q[PF_MAX_SHARDS];         // per shard, local particles
+  const int64_t* lend;                // [G], this shard's copy
+  int G;
+  int lg;                             // log2(N / G)
+  int64_t n;                          // N total
+};
+
+template <typename TQ>
+PF_D int64_t sharded_lookup(const ShardLookup<TQ>& L, uint64_t w3) {
+  const double u = unit_open(w3);
+  const int64_t s0 = (int64_t)ceil(u * (double)L.n) - 1;
+  int g = 0;
+  while (g < L.G - 1 && __ldcg(&L.lend[g]) <= s0) ++g;
+  int64_t k = __ldcg(&L.cut[g][s0]);
+  const int64_t mask = ((int64_t)1 << L.lg) - 1;
+  while (u > (double)__ldcg(&L.q[k >> L.lg][k & mask])) ++k;
+  return k;
 }
 
 // ------------------------------------------------------- small n path ---

@@ -192,6 +192,33 @@ int launch_reduce_qr_m(int grid, WSrc src, int R, TQ* tt, TQ* ct, int64_t* fail,
   return PF_OK;
 }
 
+// Classification with a caller-fixed grid (sharded runs: every shard's
+// launch must use the same grid so the partial slots line up).
+template <typename TQ, int QM>
+int launch_classify_m(int grid, WSrc src, int tiles, int64_t* fail, const QArgs& qa, cudaStream_t st) {
+  constexpr int NQ = (QM & 1) + ((QM >> 1) & 1) + ((QM >> 2) & 1);
+  const size_t smem = (size_t)NQ * (2 * Q_PER + 1) * CDF_THREADS * sizeof(double);
+  CK(cudaFuncSetAttribute(cdf_reduce_qr_kernel<TQ, QM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  cdf_reduce_qr_kernel<TQ, QM, false><<<grid, CDF_THREADS, smem, st>>>(src, tiles, nullptr, nullptr, fail, qa);
+  LAUNCHED();
+  return PF_OK;
+}
+
+template <typename TQ>
+int launch_classify(int qm, int grid, WSrc src, int tiles, int64_t* fail, const QArgs& qa, cudaStream_t st) {
+  switch (qm) {
+    case 1: return launch_classify_m<TQ, 1>(grid, src, tiles, fail, qa, st);
+    case 2: return launch_classify_m<TQ, 2>(grid, src, tiles, fail, qa, st);
+    case 3: return launch_classify_m<TQ, 3>(grid, src, tiles, fail, qa, st);
+    case 4: return launch_classify_m<TQ, 4>(grid, src, tiles, fail, qa, st);
+    case 5: return launch_classify_m<TQ, 5>(grid, src, tiles, fail, qa, st);
+    case 6: return launch_classify_m<TQ, 6>(grid, src, tiles, fail, qa, st);
+    case 7: return launch_classify_m<TQ, 7>(grid, src, tiles, fail, qa, st);
+  }
+  return set_err(PF_ERR_VALUE, "quantile mask");
+}
+
 template <typename TQ>
 int launch_reduce_qr(int qm, int grid, WSrc src, int R, TQ* tt, TQ* ct, int64_t* fail, const QArgs& qa,
                      cudaStream_t st) {
@@ -613,6 +640,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   // ---- K0 init
   {
     InitArgs a;
+    a.gbase = 0;
     a.n = n;
     a.seed = c.seed;
     a.x0_mean = c.x0_mean;
@@ -665,6 +693,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   const int draw_grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sms * docc);
   auto launch_draws = [&](int64_t t, cudaStream_t s_) {
     DrawArgs d;
+    d.gbase = 0;
     d.n = n;
     d.t = t;
     d.seed = c.seed;
@@ -731,6 +760,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     QShared* qshp = ntg ? e->qsh.p + par : nullptr;
     // ---- K1
     StepArgs<TQ> a;
+    memset(&a, 0, sizeof(a));
     a.n = n;
     a.t = t;
     a.seed = c.seed;
@@ -822,6 +852,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       // side stream: exact resolve (overlaps the CDF and the next step)
       cudaStream_t ss = e->side;
       QValueSrc vs;
+      memset(&vs, 0, sizeof(vs));
       vs.rec = e->rec[cur].p;
       vs.seed = c.seed;
       vs.t = t;
@@ -1082,6 +1113,8 @@ RunFn pick_run(int mode) {
 
 }  // namespace
 
+#include "group.cuh"
+
 // ================================================================ C ABI ===
 extern "C" {
 
@@ -1211,6 +1244,154 @@ int pf_engine_run_resident(pf_engine* e, int64_t t_len) {
   int rc = pick_run(e->mode)(e, rs);
   e->last_kernels = g_launches.load() - k0;
   return rc;
+}
+
+// ------------------------------------------------- sharded (group) run ---
+int pf_group_destroy(pf_group* g);
+
+int pf_group_create(const pf_config* cfg, int32_t nshards, const int32_t* devices, pf_group** out) {
+  if (!cfg || !out) return set_err(PF_ERR_VALUE, "null argument");
+  *out = nullptr;
+  const int64_t n = cfg->n;
+  const int G = nshards;
+  if (n < 1) return set_err(PF_ERR_VALUE, "particle count must be >= 1");
+  if (!is_pow2(n)) return set_err(PF_ERR_NOT_POWER_OF_TWO, "particle count must be a power of two, got " + std::to_string(n));
+  if (G < 1 || G > PF_MAX_SHARDS || !is_pow2(G)) return set_err(PF_ERR_VALUE, "shard count must be 1, 2, 4 or 8");
+  if (n / G < 4096) return set_err(PF_ERR_VALUE, "sharded runs need at least 4096 particles per shard");
+  if (n > ((int64_t)1 << 31)) return set_err(PF_ERR_VALUE, "particle count above 2^31");
+  const int ndev = pf_device_count();
+  if (ndev < 1) return set_err(PF_ERR_CUDA, "no CUDA device visible");
+  pf_group* g = new pf_group();
+  g->cfg = *cfg;
+  g->G = G;
+  g->ns = n / G;
+  g->lg = ilog2(g->ns);
+  for (int s = 0; s < G; ++s) {
+    const int d = devices ? devices[s] : 0;
+    if (d < 0 || d >= ndev) {
+      pf_group_destroy(g);
+      return set_err(PF_ERR_VALUE, "shard device ordinal out of range");
+    }
+    g->dev.push_back(d);
+  }
+  // peer access between distinct devices (NVLink / NVSwitch P2P)
+  for (int a = 0; a < G; ++a)
+    for (int b = 0; b < G; ++b) {
+      if (g->dev[a] == g->dev[b]) continue;
+      int ok = 0;
+      cudaDeviceCanAccessPeer(&ok, g->dev[a], g->dev[b]);
+      if (!ok) {
+        pf_group_destroy(g);
+        return set_err(PF_ERR_CUDA, "devices without peer access cannot share a sharded run");
+      }
+      cudaSetDevice(g->dev[a]);
+      cudaError_t e = cudaDeviceEnablePeerAccess(g->dev[b], 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+        pf_group_destroy(g);
+        return set_err(PF_ERR_CUDA, std::string("peer access: ") + cudaGetErrorString(e));
+      }
+      cudaGetLastError();
+    }
+  const size_t esz = cfg->precision == PF_DTYPE_F32 ? 4 : 8;
+  for (int s = 0; s < G; ++s) {
+    pf_config cs = *cfg;
+    cs.n = g->ns;
+    cs.device = g->dev[s];
+    pf_engine* e = nullptr;
+    int rc = pf_engine_create(&cs, &e);
+    if (rc != PF_OK) {
+      pf_group_destroy(g);
+      return rc;
+    }
+    g->sh.push_back(e);
+    cudaSetDevice(g->dev[s]);
+    int32_t* cut = nullptr;
+    void* q = nullptr;
+    int64_t* le = nullptr;
+    cudaError_t err;
+    if ((err = cudaMalloc((void**)&cut, (size_t)(n + 1) * sizeof(int32_t))) ||
+        (err = cudaMalloc(&q, (size_t)g->ns * esz)) || (err = cudaMalloc((void**)&le, PF_MAX_SHARDS * sizeof(int64_t)))) {
+      pf_group_destroy(g);
+      return set_err(err == cudaErrorMemoryAllocation ? PF_ERR_OUT_OF_MEMORY : PF_ERR_CUDA,
+                     std::string("shard allocation: ") + cudaGetErrorString(err));
+    }
+    g->gcut.push_back(cut);
+    g->gq.push_back(q);
+    g->lend.push_back(le);
+    cudaEvent_t ev[5];
+    for (auto& x : ev) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+    g->evA.push_back(ev[0]);
+    g->evB.push_back(ev[1]);
+    g->evC.push_back(ev[2]);
+    g->evK.push_back(ev[3]);
+    g->evD.push_back(ev[4]);
+  }
+  cudaSetDevice(g->dev[0]);
+  cudaError_t err;
+  if ((err = cudaMalloc((void**)&g->xrec, PF_MAX_SHARDS * sizeof(Partial))) ||
+      (err = cudaMalloc(&g->xtot, PF_MAX_SHARDS * sizeof(double))) ||
+      (err = cudaEventCreateWithFlags(&g->evM, cudaEventDisableTiming))) {
+    pf_group_destroy(g);
+    return set_err(PF_ERR_CUDA, std::string("exchange allocation: ") + cudaGetErrorString(err));
+  }
+  *out = g;
+  return PF_OK;
+}
+
+int pf_group_run(pf_group* g, const double* y, int64_t t_len, pf_outputs* out) {
+  if (!g) return set_err(PF_ERR_VALUE, "null group");
+  if (t_len < 0) return set_err(PF_ERR_VALUE, "negative series length");
+  for (int64_t i = 0; i < t_len; ++i)
+    if (!std::isfinite(y[i])) return set_err(PF_ERR_NON_FINITE_WEIGHT, "observations contain NaN or infinity");
+  if (out && out->hist_states)
+    return set_err(PF_ERR_NOT_IMPLEMENTED, "store_particles is not supported by sharded runs");
+  const pf_config& c = g->cfg;
+  const int mode = (c.learn && c.learn_sigma2 ? M_LS : 0) | (c.learn && c.learn_tau2 ? M_LT : 0) |
+                   (c.precision == PF_DTYPE_F32 ? M_SINGLE : 0);
+  return pick_group_run(mode)(g, y, t_len, out);
+}
+
+int pf_group_reconfigure(pf_group* g, const pf_config* cfg) {
+  if (!g || !cfg) return set_err(PF_ERR_VALUE, "null argument");
+  if (cfg->n != g->cfg.n || cfg->precision != g->cfg.precision)
+    return set_err(PF_ERR_VALUE, "reconfigure cannot change n or precision");
+  g->cfg = *cfg;
+  for (int s = 0; s < g->G; ++s) {
+    pf_config cs = *cfg;
+    cs.n = g->ns;
+    cs.device = g->dev[s];
+    int rc = pf_engine_reconfigure(g->sh[s], &cs);
+    if (rc != PF_OK) return rc;
+  }
+  return PF_OK;
+}
+
+int pf_group_last_timing(pf_group* g, double* total_ms) {
+  if (!g) return set_err(PF_ERR_VALUE, "null group");
+  if (total_ms) *total_ms = g->last_ms;
+  return PF_OK;
+}
+
+int pf_group_destroy(pf_group* g) {
+  if (!g) return PF_OK;
+  for (size_t s = 0; s < g->sh.size(); ++s) pf_engine_destroy(g->sh[s]);
+  for (size_t s = 0; s < g->gcut.size(); ++s) {
+    cudaSetDevice(g->dev[s]);
+    cudaFree(g->gcut[s]);
+    cudaFree(g->gq[s]);
+    cudaFree(g->lend[s]);
+    cudaEventDestroy(g->evA[s]);
+    cudaEventDestroy(g->evB[s]);
+    cudaEventDestroy(g->evC[s]);
+    cudaEventDestroy(g->evK[s]);
+    cudaEventDestroy(g->evD[s]);
+  }
+  if (!g->dev.empty()) cudaSetDevice(g->dev[0]);
+  if (g->xrec) cudaFree(g->xrec);
+  if (g->xtot) cudaFree(g->xtot);
+  if (g->evM) cudaEventDestroy(g->evM);
+  delete g;
+  return PF_OK;
 }
 
 int pf_engine_quantile_stats(pf_engine* e, int64_t* stats4) {

@@ -100,7 +100,14 @@ struct QArgs {
   unsigned int* stats;         // [0] unresolved, [1] fallbacks, [2] max candidates, [3] resolves
   uint32_t* lidx;              // [ntarget][Q_LIST] exact-resolve lists
   double* lw;
+  // sharded runs: every shard's passes feed shard 0's state; partial slots
+  // pbase + block of ptotal (0: this launch alone), particle index offset
+  int pbase, ptotal;
+  uint32_t gbase;
 };
+
+PF_D int q_pslot(const QArgs& qa) { return qa.pbase + (int)blockIdx.x; }
+PF_D unsigned q_ptotal(const QArgs& qa) { return qa.ptotal ? (unsigned)qa.ptotal : gridDim.x; }
 
 // Window of target k for this step from mean/sd of its quantity.
 PF_D void window_of(const QTarget& t, double mean, double sd, uint32_t* lo, uint32_t* hi) {
@@ -121,7 +128,9 @@ PF_D uint32_t sub_bin(uint32_t key, uint32_t lo, uint32_t hi, int nb) {
 
 // Exact value of quantity q for particle idx at step t (resolve side).
 struct QValueSrc {
-  const Rec* rec;        // records written by step t
+  const Rec* rec;        // records written by step t (single run)
+  const Rec* recs[PF_MAX_SHARDS];  // sharded run: per-shard records, nsh > 0
+  int nsh, lg;
   uint64_t seed;
   int64_t t;
   GammaSrc gs;           // step t's sigma2 table
@@ -131,7 +140,7 @@ struct QValueSrc {
 };
 
 PF_D double quantity_value(const QValueSrc& s, int q, uint32_t idx) {
-  const Rec r = s.rec[idx];
+  const Rec r = s.nsh ? s.recs[idx >> s.lg][idx & ((1u << s.lg) - 1u)] : s.rec[idx];
   if (q == 0) return r.x;
   if (q == 2) return s.learn_t ? r.tau2 : s.tau2_fixed;
   if (!s.learn_s) return s.sigma2_fixed;
@@ -268,17 +277,17 @@ PF_D void q_reduce_partials(const QArgs& qa, const QWin& win, double (&acc)[Q_SL
   if (threadIdx.x <= Q_SLOTS) {
     double s = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w][threadIdx.x];
-    qa.part[(size_t)blockIdx.x * (Q_SLOTS + 1) + threadIdx.x] = s;
+    qa.part[(size_t)q_pslot(qa) * (Q_SLOTS + 1) + threadIdx.x] = s;
   }
-  __threadfence();
+  __threadfence_system();
   __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&qa.sh->counter, 1u) == gridDim.x - 1;
+  if (threadIdx.x == 0) last = atomicAdd(&qa.sh->counter, 1u) == q_ptotal(qa) - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
   if (threadIdx.x <= Q_SLOTS) {
     double s = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(&qa.part[(size_t)b * (Q_SLOTS + 1) + threadIdx.x]);
+    for (unsigned b = 0; b < q_ptotal(qa); ++b) s += __ldcg(&qa.part[(size_t)b * (Q_SLOTS + 1) + threadIdx.x]);
     if (threadIdx.x == Q_SLOTS) {
       qa.sh->W = s;
     } else {
@@ -559,7 +568,7 @@ cdf_reduce_qr_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ 
             const int tq = win.base[q] + (sl - q * Q_PER);
             QCand c;
             c.key = q == 0 ? key[0][e] : (q == 1 ? key[1][e] : key[2][e]);
-            c.idx = (uint32_t)(base + e);
+            c.idx = qa.gbase + (uint32_t)(base + e);
             c.w = (double)v[e];
             if (pos < Q_AGG) {
               agg.c[pos] = c;
@@ -960,17 +969,17 @@ q_fallback_hist_kernel(QArgs qa, const double* __restrict__ lw, int wmode, const
   if (threadIdx.x < Q_MAXT) {
     double s = 0.0;
     for (int w = 0; w < 8; ++w) s += red[w][threadIdx.x];
-    qa.part[(size_t)blockIdx.x * (Q_MAXT + 1) + threadIdx.x] = s;
+    qa.part[(size_t)q_pslot(qa) * (Q_MAXT + 1) + threadIdx.x] = s;
   }
-  __threadfence();
+  __threadfence_system();
   __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&qa.sh->fb_counter, 1u) == gridDim.x - 1;
+  if (threadIdx.x == 0) last = atomicAdd(&qa.sh->fb_counter, 1u) == q_ptotal(qa) - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
   if (threadIdx.x < qa.ntarget && act[threadIdx.x]) {
     double s = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(&qa.part[(size_t)b * (Q_MAXT + 1) + threadIdx.x]);
+    for (unsigned b = 0; b < q_ptotal(qa); ++b) s += __ldcg(&qa.part[(size_t)b * (Q_MAXT + 1) + threadIdx.x]);
     qa.tg[threadIdx.x].ibelow = s;
   }
   if (threadIdx.x == 0) qa.sh->fb_counter = 0;
@@ -1043,7 +1052,7 @@ __global__ void __launch_bounds__(256) q_fallback_fill_kernel(QArgs qa, const do
         if (pos < qa.cap) {
           QCand c;
           c.key = key;
-          c.idx = (uint32_t)i;
+          c.idx = qa.gbase + (uint32_t)i;
           c.w = w;
           qa.cand[(size_t)k * qa.cap + pos] = c;
         }

@@ -106,6 +106,7 @@ struct InitArgs {
   const double* feed_gt;
   Rec* rec;
   double* s2_init;          // optional: sigma2 draws (T == 0 keep_final)
+  int64_t gbase;            // global index of this shard's first slot
 };
 
 template <int MODE>
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(256) init_kernel(InitArgs a) {
   constexpr bool LS = MODE & M_LS, LT = MODE & M_LT, SINGLE = MODE & M_SINGLE;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n;
        j += (int64_t)gridDim.x * blockDim.x) {
-    const Philox4 P = philox_block(a.seed, (uint64_t)j, 0);
+    const Philox4 P = philox_block(a.seed, (uint64_t)(a.gbase + j), 0);
     const double z = a.feed_z ? a.feed_z[j] : ndtri(unit_open(P.w[0]));
     double x0 = a.x0_mean + a.sqrt_x0_var * z;
     if (SINGLE) x0 = (double)(float)x0;
@@ -180,6 +181,8 @@ struct StepArgs {
   int64_t* fail;
   Partial* xrec;         // sharded run: shard partials [G] (null: single run)
   int shard;
+  ShardLookup<TQ> slk;   // sharded run (slk.G > 0): cross-shard lookup
+  const Rec* recs[PF_MAX_SHARDS];  // sharded run: every shard's records of step t-1
 };
 
 PF_D double warp_sum(double v) {
@@ -304,6 +307,7 @@ struct DrawArgs {
   double* g_t;
   uint64_t* u3;
   const int64_t* fail;
+  int64_t gbase;         // global index of this shard's first slot (stream id offset)
 };
 
 PF_D double nt_eval_slot(int off, double u) {
@@ -351,7 +355,7 @@ __global__ void __launch_bounds__(256) draws_kernel(DrawArgs a) {
   stage_tables<LS, LT>(a.gs, a.gt, a.ntab, slot_s, slot_t, noff);
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n;
        j += (int64_t)gridDim.x * blockDim.x) {
-    const Philox4 P = philox_block(a.seed, (uint64_t)j, (uint64_t)a.t);
+    const Philox4 P = philox_block(a.seed, (uint64_t)(a.gbase + j), (uint64_t)a.t);
     a.u3[j] = P.w[3];
     const double u0 = unit_open(P.w[0]);
     a.z[j] = noff >= 0 ? nt_eval_slot(noff, u0) : ndtri(u0);
@@ -416,7 +420,13 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
       anc[b] = jj[b];
     }
     if (a.t > 1) {
-      ancestors_of<TQ, STEP_SB>(a.lk, w3, ok, anc);
+      if (a.slk.G > 0) {
+#pragma unroll
+        for (int b = 0; b < STEP_SB; ++b)
+          if (ok[b]) anc[b] = sharded_lookup<TQ>(a.slk, w3[b]);
+      } else {
+        ancestors_of<TQ, STEP_SB>(a.lk, w3, ok, anc);
+      }
       if (a.idx_out) {
 #pragma unroll
         for (int b = 0; b < STEP_SB; ++b)
@@ -427,7 +437,11 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
     for (int b = 0; b < STEP_SB; ++b) {
       if (!ok[b]) continue;
       const uint32_t dst = (uint32_t)__cvta_generic_to_shared(rec_at(buf, b));
-      const char* src = reinterpret_cast<const char*>(a.rec_in + anc[b]);
+      // ancestors are global indices in a sharded run (identity, local, at t = 1)
+      const Rec* rp = (a.slk.G > 0 && a.t > 1)
+          ? a.recs[anc[b] >> a.slk.lg] + (anc[b] & (((int64_t)1 << a.slk.lg) - 1))
+          : a.rec_in + anc[b];
+      const char* src = reinterpret_cast<const char*>(rp);
       cp_async16(dst, src);
       cp_async16(dst + 16, src + 16);
       cp_async8((uint32_t)__cvta_generic_to_shared(val_at(buf, 0, b)), a.z + jj[b]);
@@ -643,6 +657,49 @@ __global__ void __launch_bounds__(256) materialize_kernel(MatArgs<TQ> a) {
           const double g = a.feed_gs ? a.feed_gs[anc] : gamma_draw(a.gs, unit_open(P.w[1]));
           s2 = r.bs / g;
         }
+      }
+      a.s2[j] = s2;
+    }
+    if (a.t2) a.t2[j] = a.learn_t ? r.tau2 : a.tau2_fixed;
+    if (a.as) a.as[j] = a.learn_s ? a.a_s : 0.0;
+    if (a.bs) a.bs[j] = a.learn_s ? r.bs : 0.0;
+    if (a.at) a.at[j] = a.learn_t ? a.a_t : 0.0;
+    if (a.bt) a.bt[j] = a.learn_t ? r.bt : 0.0;
+  }
+}
+
+// Sharded run: post-resample system of the last step (keep_final /
+// keep_indices row T) with the cross-shard lookup and remote records.
+template <typename TQ>
+struct GroupMatArgs {
+  int64_t ns, gbase, t;
+  uint64_t seed;
+  const uint64_t* u3;
+  ShardLookup<TQ> slk;
+  const Rec* recs[PF_MAX_SHARDS];
+  GammaSrc gs;
+  int learn_s, learn_t;
+  double sigma2_fixed, tau2_fixed, a_s, a_t;
+  int64_t* idx;
+  double *x, *s2, *t2, *as, *bs, *at, *bt;
+  const int64_t* fail;
+};
+
+template <typename TQ>
+__global__ void __launch_bounds__(256) group_materialize_kernel(GroupMatArgs<TQ> a) {
+  if (*a.fail) return;
+  const int64_t mask = ((int64_t)1 << a.slk.lg) - 1;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.ns;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t anc = sharded_lookup<TQ>(a.slk, a.u3[j]);
+    if (a.idx) a.idx[j] = anc + 1;
+    const Rec r = a.recs[anc >> a.slk.lg][anc & mask];
+    if (a.x) a.x[j] = r.x;
+    if (a.s2) {
+      double s2 = a.sigma2_fixed;
+      if (a.learn_s) {
+        const Philox4 P = philox_block(a.seed, (uint64_t)anc, (uint64_t)a.t);
+        s2 = r.bs / gamma_draw(a.gs, unit_open(P.w[1]));
       }
       a.s2[j] = s2;
     }

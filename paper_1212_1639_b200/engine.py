@@ -96,3 +96,41 @@ class Engine:
             self.close()
         except Exception:
             pass
+
+
+class Group:
+    """One filter sharded over several devices (pf_group_* in the C ABI)."""
+
+    def __init__(self, cfg, devices):
+        self.lib = _lib.require_device()
+        self.h = C.c_void_p()
+        devs = (C.c_int32 * len(devices))(*devices)
+        _lib.check(self.lib.pf_group_create(C.byref(cfg), len(devices), devs, C.byref(self.h)), self.lib)
+        self.cfg = cfg
+        self.devices = list(devices)
+
+    def reconfigure(self, cfg):
+        _lib.check(self.lib.pf_group_reconfigure(self.h, C.byref(cfg)), self.lib)
+        self.cfg = cfg
+
+    def run(self, y, outputs, feed=None):
+        if feed is not None:
+            raise NotImplementedError("oracle feeds are not supported by sharded runs")
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        _lib.check(self.lib.pf_group_run(self.h, _lib.ptr(y), len(y), C.byref(outputs)), self.lib)
+
+    def last_timing(self):
+        tot = C.c_double()
+        _lib.check(self.lib.pf_group_last_timing(self.h, C.byref(tot)), self.lib)
+        return {"total_ms": tot.value}
+
+    def close(self):
+        if self.h:
+            self.lib.pf_group_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

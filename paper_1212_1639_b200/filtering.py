@@ -25,7 +25,7 @@ import numpy as np
 from . import _lib
 from .backend import Backend
 from .core import ParamDraws, ParticleSystem, SuffStats, check_power_of_two
-from .engine import Engine, make_config
+from .engine import Engine, Group, make_config
 from .errors import NonFiniteWeightError
 from .models import Priors
 
@@ -201,10 +201,19 @@ def _run_loop(model, priors, y, n, seed, backend, resampler, precision, store_pa
         backend = Backend()
     try:
         cfg, ls, lt = _build_config(model, priors, n, seed, precision, flags, backend.device)
-        key = ("engine", n, precision, backend.device)
+        shards = getattr(backend, "shards", 1)
+        if shards > 1:
+            if store_particles:
+                raise NotImplementedError("store_particles is not supported by sharded runs")
+            key = ("group", n, precision, tuple(backend.devices))
 
-        def factory():
-            return Engine(cfg)
+            def factory():
+                return Group(cfg, backend.devices)
+        else:
+            key = ("engine", n, precision, backend.device)
+
+            def factory():
+                return Engine(cfg)
 
         eng = backend.engine(key, factory)
         eng.reconfigure(cfg)
