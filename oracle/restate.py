@@ -261,6 +261,47 @@ def tree_cdf_chunked(w, chunk):
     return finalize_cdf(s.reshape(n), top[-1][0])
 
 
+def shard_exchange(totals, n_total):
+    """Host restatement of the sharded CDF exchange (the device's
+    cdf_top_shard_kernel): from the G shard subtree totals (each a node of
+    the adder tree, prefix_sum.py:64), rebuild the top levels -> the root,
+    run the backward adder (prefix_sum.py:86-87) down to every shard node,
+    and derive each shard's carry (running max of the shard nodes before it;
+    a node never exceeds its parent) and stratum bound L_end = ceil(N q_end)
+    (resampling.py:124).  Returns (root, nodes, carries, lend)."""
+    totals = np.asarray(totals)
+    top = forward_adder(totals)
+    nodes = backward_adder(top)
+    root = top[-1][0]
+    carries = np.empty_like(nodes)
+    lend = np.empty(len(nodes), dtype=np.int64)
+    m = totals.dtype.type(-np.inf)
+    for g in range(len(nodes)):
+        carries[g] = m
+        m = max(m, nodes[g])
+        qe = totals.dtype.type(1) if g == len(nodes) - 1 else min(max(m / root, 0), 1)
+        lend[g] = int(np.ceil(totals.dtype.type(qe) * totals.dtype.type(n_total)))
+    return root, nodes, carries, lend
+
+
+def tree_cdf_shard(w_shard, shard, node, carry, root, n_total):
+    """The CDF values of one shard's particles given its node value and
+    carry from :func:`shard_exchange`: backward adder inside the shard's
+    subtree, divide by the root, running max seeded with the carry, clip,
+    pin the global last element (prefix_sum.py:72-106)."""
+    w_shard = np.asarray(w_shard)
+    ns = len(w_shard)
+    lv = forward_adder(w_shard)
+    lv[-1] = np.array([node], dtype=w_shard.dtype)
+    s = backward_adder(lv)
+    q = s / root
+    q = np.maximum.accumulate(np.concatenate([[carry / root], q]))[1:]
+    np.clip(q, q.dtype.type(0), q.dtype.type(1), out=q)
+    if (shard + 1) * ns == n_total:
+        q[-1] = 1
+    return q
+
+
 # ------------------------------------------------------------ cut points ---
 def cut_points(q):
     """resampling.py:110-134: L_j = ceil(N q_j); slots (L_{j-1}, L_j] get j
