@@ -540,7 +540,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
         t.q = q;
         t.col = i;
         t.zprev = ndtri(ps[i]);  // normal start; learned from step 1 on
-        t.h = 0.25;
+        t.h = Q_H0;
         tgs.push_back(t);
       }
     };

@@ -94,7 +94,7 @@ int run_group(pf_group* g, const double* y, int64_t T, pf_outputs* out) {
         t.q = q;
         t.col = i;
         t.zprev = ndtri(ps[i]);
-        t.h = 0.25;
+        t.h = Q_H0;
         tgs.push_back(t);
       }
     };

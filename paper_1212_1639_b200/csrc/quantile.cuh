@@ -33,6 +33,14 @@ constexpr int Q_SUB = 2048;      // sub-bins per window
 constexpr int Q_FB = 4096;       // fallback bins per missed interval
 constexpr int Q_LIST = 4096;     // exact-resolve list capacity (per target)
 constexpr int Q_RESOLVE_SMEM = Q_LIST * (8 + 8 + 4);
+// Window half-widths: the first step's (standardized units), then sized in
+// probability mass from the observed prediction error.  Narrow windows keep
+// the candidate lists short; a miss costs the fallback passes (two sweeps),
+// which is cheaper than classifying a few percent of all particles as
+// candidates every step.
+constexpr double Q_H0 = 0.05;
+constexpr double Q_MASS_MIN = 5e-4;
+constexpr double Q_MASS_MAX = 0.006;
 
 enum : uint32_t { QS_OK = 0, QS_MISS_LO = 1, QS_MISS_HI = 2, QS_OVERFLOW = 3, QS_CROWD = 4,
                   QS_REFILL = 5, QS_FB = 6, QS_RETRY = 7, QS_LOCATED = 8 };
@@ -865,7 +873,7 @@ q_finish_kernel(QArgs qa, QValueSrc vs, double* out_x, double* out_s, double* ou
       const double phi = fmax(normal_pdf(z), 1e-4);
       const double em = fabs(z - tg.zprev) * phi;
       tg.ema = 0.7 * tg.ema + 0.3 * em;
-      const double mass = fmin(0.03, fmax(1e-3, 4.0 * fmax(em, tg.ema)));
+      const double mass = fmin(Q_MASS_MAX, fmax(Q_MASS_MIN, 4.0 * fmax(em, tg.ema)));
       tg.h = fmin(2.0, mass / phi);
       tg.zprev = z;
     }
