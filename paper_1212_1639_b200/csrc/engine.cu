@@ -323,6 +323,7 @@ struct pf_engine {
   DevBuf<uint64_t> du3;
   cudaStream_t dstream = nullptr;  // draws run here, overlapping the CDF kernels
   cudaEvent_t ev_draw = nullptr, ev_step = nullptr;
+  cudaEvent_t ev_steps[3] = {nullptr, nullptr, nullptr};  // step kernel t done, by t % 3
   const double* ntab = nullptr;    // cached normal-quantile table (not owned)
   DevBuf<unsigned char> q;
   DevBuf<int32_t> cut;
@@ -689,7 +690,13 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   if (docc < 1) docc = 1;
   // persistent grids: one wave of resident CTAs
   const int64_t nbatches = (n + STEP_SB * 256 - 1) / (STEP_SB * 256);
-  const int step_grid = (int)std::min<int64_t>(nbatches, (int64_t)sms * occ);
+  // The step kernel keeps fewer CTAs per SM than it could, leaving room for
+  // the next step's draws_kernel to run beside it (PF_STEP_CTAS overrides).
+  static const int step_ctas = [] {
+    const char* v = getenv("PF_STEP_CTAS");
+    return v ? atoi(v) : 2;
+  }();
+  const int step_grid = (int)std::min<int64_t>(nbatches, (int64_t)sms * std::min(occ, std::max(1, step_ctas)));
   const int draw_grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sms * docc);
   auto launch_draws = [&](int64_t t, cudaStream_t s_) {
     DrawArgs d;
@@ -700,7 +707,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     d.gs = gamma_src(e, true, t);
     d.gt = gamma_src(e, false, t);
     d.ntab = e->ntab;
-    const size_t off = (size_t)(t & 1) * n;
+    const size_t off = (size_t)(t % 3) * n;  // draws are triple-buffered
     d.z = e->dz.p + off;
     d.g_s = e->dgs.p + off;
     d.g_t = e->dgt.p + off;
@@ -773,11 +780,11 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     a.rec_out = e->rec[cur ^ 1].p;
     a.lw = lwp;
     a.Mout = e->mbuf.p + par;
-    a.u3 = e->du3.p + (size_t)((t - 1) & 1) * n;
+    a.u3 = e->du3.p + (size_t)((t - 1) % 3) * n;
     a.lk = lk;
     a.idx_out = (keep_idx && t > 1) ? e->idx.p : nullptr;
     {
-      const size_t off = (size_t)(t & 1) * n;
+      const size_t off = (size_t)(t % 3) * n;
       a.z = fz ? row(fz, t) : e->dz.p + off;
       a.g_s = fgs ? row(fgs, t) : e->dgs.p + off;
       a.g_t = fgt ? row(fgt, t) : e->dgt.p + off;
@@ -814,10 +821,11 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     LAUNCHED();
     ++step_launches;
     cur ^= 1;
+    CK(cudaEventRecord(e->ev_steps[t % 3], st));
     if (t < T) {
-      // draws(t+1) overwrite the resampling words step t just consumed
-      CK(cudaEventRecord(e->ev_step, st));
-      CK(cudaStreamWaitEvent(e->dstream, e->ev_step, 0));
+      // draws(t+1) reuse the buffers of step t-2, last read by step t-1: they
+      // run concurrently with step t and the CDF kernels
+      if (t >= 2) CK(cudaStreamWaitEvent(e->dstream, e->ev_steps[(t - 1) % 3], 0));
       launch_draws(t + 1, e->dstream);
       CK(cudaEventRecord(e->ev_draw, e->dstream));
     }
@@ -907,7 +915,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       m.seed = c.seed;
       m.resample = 1;
       m.rec = e->rec[cur].p;
-      m.u3 = e->du3.p + (size_t)(t & 1) * n;
+      m.u3 = e->du3.p + (size_t)(t % 3) * n;
       m.lk = lk;
       m.s2_direct = nullptr;
       m.gs = gamma_src(e, true, t);
@@ -950,7 +958,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     m.seed = c.seed;
     m.resample = 1;
     m.rec = e->rec[cur].p;
-    m.u3 = e->du3.p + (size_t)(T & 1) * n;
+    m.u3 = e->du3.p + (size_t)(T % 3) * n;
     m.lk = lk;
     m.s2_direct = nullptr;
     m.gs = gamma_src(e, true, T);
@@ -1161,7 +1169,10 @@ int pf_engine_create(const pf_config* cfg, pf_engine** out) {
   if ((err = cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking))) return bail(err);
   if ((err = cudaStreamCreateWithFlags(&e->dstream, cudaStreamNonBlocking)) ||
       (err = cudaEventCreateWithFlags(&e->ev_draw, cudaEventDisableTiming)) ||
-      (err = cudaEventCreateWithFlags(&e->ev_step, cudaEventDisableTiming)))
+      (err = cudaEventCreateWithFlags(&e->ev_step, cudaEventDisableTiming)) ||
+      (err = cudaEventCreateWithFlags(&e->ev_steps[0], cudaEventDisableTiming)) ||
+      (err = cudaEventCreateWithFlags(&e->ev_steps[1], cudaEventDisableTiming)) ||
+      (err = cudaEventCreateWithFlags(&e->ev_steps[2], cudaEventDisableTiming)))
     return bail(err);
   if ((err = cudaEventCreateWithFlags(&e->ev_b, cudaEventDisableTiming)) ||
       (err = cudaEventCreateWithFlags(&e->ev_e, cudaEventDisableTiming)) ||
@@ -1169,8 +1180,8 @@ int pf_engine_create(const pf_config* cfg, pf_engine** out) {
       (err = cudaEventCreateWithFlags(&e->ev_q[1], cudaEventDisableTiming)) || (err = e->mbuf.ensure(2)))
     return bail(err);
   if ((err = e->rec[0].ensure(n)) || (err = e->rec[1].ensure(n)) || (err = e->lw.ensure(2 * n)) ||
-      (err = e->du3.ensure(2 * n)) || (err = e->dz.ensure(2 * n)) ||
-      (err = e->dgs.ensure(2 * n)) || (err = e->dgt.ensure(2 * n)) || (err = e->partials.ensure(sm_count() * 8 + 8)) ||
+      (err = e->du3.ensure(3 * n)) || (err = e->dz.ensure(3 * n)) ||
+      (err = e->dgs.ensure(3 * n)) || (err = e->dgt.ensure(3 * n)) || (err = e->partials.ensure(sm_count() * 8 + 8)) ||
       (err = e->sc.ensure(1)) || (err = e->fail.ensure(1)) ||
       (err = e->cdf.ensure(n, e->single ? 4 : 8)) || (err = e->probs.ensure(8)))
     return bail(err);
@@ -1428,6 +1439,8 @@ int pf_engine_destroy(pf_engine* e) {
   if (e->dstream) cudaStreamDestroy(e->dstream);
   if (e->ev_draw) cudaEventDestroy(e->ev_draw);
   if (e->ev_step) cudaEventDestroy(e->ev_step);
+  for (auto ev : e->ev_steps)
+    if (ev) cudaEventDestroy(ev);
   e->q.release();
   e->cut.release();
   e->rank.release();
