@@ -120,3 +120,24 @@ def test_phase_timings_total():
     t = P.PhaseTimings(initialize=1, cdf=2, resample=3, resample_sort_only=1, propagate=4,
                        store=5, other=6)
     assert t.total == 21 and t.as_dict()["cdf_ns"] == 2
+
+
+def test_replication_seeds_partition():
+    from paper_1212_1639_b200.replications import rank_seeds
+
+    seeds = list(range(1000))
+    parts = [rank_seeds(seeds, r, 8) for r in range(8)]
+    assert sorted(x for p in parts for x in p) == seeds
+    assert max(len(p) for p in parts) - min(len(p) for p in parts) <= 1
+
+
+def test_backend_shard_arguments():
+    import paper_1212_1639_b200 as P
+
+    b = P.Backend("cuda", shards=4, devices=[0, 1, 2, 3])
+    assert b.shards == 4 and b.devices == [0, 1, 2, 3]
+    assert P.Backend("cuda", shards=2, device=1).devices == [1, 1]
+    with pytest.raises(ValueError):
+        P.Backend("cuda", shards=3)
+    with pytest.raises(ValueError):
+        P.Backend("cuda", shards=2, devices=[0])

@@ -268,3 +268,19 @@ def test_oracle_mode_strata_path(gpu, learn):
         for nm in ("sigma2", "tau2"):
             assert np.array_equal(out.param_posterior[nm].quantiles, ref[nm]["quantiles"])
             assert _rel(out.param_posterior[nm].mean, ref[nm]["mean"]) <= REL
+
+
+def test_replications_match_individual_runs(gpu):
+    """run_replications (configs[4]) reuses one engine across seeds; each
+    replication equals the stand-alone run with that seed."""
+    from paper_1212_1639_b200.replications import rank_seeds, run_replications
+
+    _, y = P.simulate(P.TrendNoiseModel(), 8, P.RngStream(3, P.rng.AUX_STREAM_BASE + 1))
+    seeds = [0, 1, 2, 3]
+    with P.Backend() as b:
+        outs = run_replications(P.Priors(), y, 1 << 12, seeds, backend=b, keep_indices=True)
+    for s, o in zip(seeds, outs):
+        ref = P.run_particle_learning(P.Priors(), y, 1 << 12, seed=s, keep_indices=True)
+        assert np.array_equal(o.resampled_indices, ref.resampled_indices)
+        assert np.array_equal(o.param_posterior["tau2"].quantiles, ref.param_posterior["tau2"].quantiles)
+    assert rank_seeds(range(10), 1, 4) == [1, 5, 9]
