@@ -175,7 +175,7 @@ class Recorder:
 
 
 def run_fixture(name, kind, n, t_len, seed, data_seed, priors=None, model=None,
-                precision="double"):
+                precision="double", resampler="cutpoint"):
     from parsmc import (InverseGammaPrior, Priors, RngStream, TrendNoiseModel,
                         run_particle_filter, run_particle_learning, simulate)
 
@@ -184,7 +184,7 @@ def run_fixture(name, kind, n, t_len, seed, data_seed, priors=None, model=None,
     rec = Recorder()
     try:
         kw = dict(seed=seed, keep_indices=True, keep_final=True, track_quantiles=True,
-                  precision=precision)
+                  precision=precision, resampler=resampler)
         if kind == "learn":
             pri = priors if priors is not None else Priors()
             out = run_particle_learning(pri, y, n, **kw)
@@ -195,11 +195,13 @@ def run_fixture(name, kind, n, t_len, seed, data_seed, priors=None, model=None,
         rec.restore()
     c = rec.calls
     d = {"y": y, "n": np.array(n), "seed": np.array(seed), "precision": np.array(precision),
+         "resampler": np.array(resampler),
          "filtered_mean": out.filtered_mean, "filtered_quantiles": out.filtered_quantiles,
          "indices": out.resampled_indices,
-         "final_states": out.final_particles.states,
-         "z": np.stack(c["z"]), "w": np.stack(c["w"]), "q": np.stack(c["q"]),
-         "idx": np.stack(c["idx"])}
+         "final_states": out.final_particles.states, "z": np.stack(c["z"])}
+    for k in ("w", "q", "idx"):  # only the cut-point path goes through these hooks
+        if c[k]:
+            d[k] = np.stack(c[k])
     if kind == "learn":
         pri = priors if priors is not None else Priors()
         d["prior"] = np.array([pri.x0_mean, pri.x0_var,
@@ -230,9 +232,31 @@ def run_fixture(name, kind, n, t_len, seed, data_seed, priors=None, model=None,
     np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **d)
 
 
+def resampler_fixtures():
+    """The reference's sequential baseline resamplers (resampling.py:29-87) in
+    the loop (filtering.py:305-316), including a non-power-of-two N."""
+    from parsmc import TrendNoiseModel
+
+    run_fixture("run_pl_sorted", "learn", 1000, 10, seed=21, data_seed=2, resampler="sorted")
+    run_fixture("run_pl_systematic", "learn", 1024, 10, seed=22, data_seed=3, resampler="systematic")
+    run_fixture("run_pl_stratified", "learn", 768, 10, seed=23, data_seed=4, resampler="stratified")
+    run_fixture("run_pl_naive", "learn", 300, 8, seed=24, data_seed=5, resampler="naive")
+    run_fixture("run_pf_sorted", "filter", 999, 10, seed=25, data_seed=6, resampler="sorted",
+                model=TrendNoiseModel())
+    run_fixture("run_pl_sorted_single", "learn", 1000, 8, seed=26, data_seed=7, resampler="sorted",
+                precision="single")
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     tmp = import_reference()
+    if len(sys.argv) > 1 and sys.argv[1] == "resamplers":
+        try:
+            resampler_fixtures()
+        finally:
+            shutil.rmtree(tmp, ignore_errors=True)
+        print("resampler fixtures written to", OUT)
+        return
     try:
         from parsmc import InverseGammaPrior, Priors, TrendNoiseModel
 

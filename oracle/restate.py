@@ -336,6 +336,35 @@ def cutpoint_indices(q, cuts, u):
     return k
 
 
+# ------------------------------------------- sequential baselines (CPU) ---
+def sequential_cdf(w):
+    """prefix_sum.py:130-134: plain left-to-right cumsum (in the weights'
+    dtype), finalised against its own last element."""
+    w = np.asarray(w)
+    prefix = np.cumsum(w)
+    return finalize_cdf(prefix, prefix[-1])
+
+
+def merge_indices(q, u):
+    """resampling.py:29-36: smallest 1-based i with u < q(i)."""
+    return np.searchsorted(q, u, side="right") + 1
+
+
+def resample_uniforms(scheme, u_slot, n, v_aux=None):
+    """The uniforms each baseline resampler searches for (resampling.py:
+    51-87): naive -> the slot's own uniform; sorted -> all of them sorted;
+    stratified -> (j + v_j)/n; systematic -> (j + v)/n with one aux draw."""
+    if scheme == "naive":
+        return u_slot
+    if scheme == "sorted":
+        return np.sort(u_slot)
+    if scheme == "stratified":
+        return (np.arange(n) + u_slot) / n
+    if scheme == "systematic":
+        return (np.arange(n) + v_aux) / n
+    raise ValueError(scheme)
+
+
 # -------------------------------------------------------------- summaries --
 PARAM_PROBS = (0.005, 0.05, 0.5, 0.95, 0.995)  # filtering.py:40
 STATE_PROBS = (0.05, 0.5, 0.95)  # filtering.py:41
@@ -368,7 +397,7 @@ class Degenerate(Exception):
 def run_loop(y, n, seed=0, *, x0_mean=0.0, x0_var=10.0,
              sigma2=(5.0, 4.0), tau2=(5.0, 0.4), precision="double",
              track_quantiles=True, keep_indices=False, keep_final=False,
-             lanes=_SERIAL, feed=None, record=None):
+             lanes=_SERIAL, feed=None, record=None, resampler="cutpoint"):
     """Restatement of ``filtering._run_loop`` (filtering.py:200-374) for the
     cut-point resampler.
 
@@ -462,18 +491,27 @@ def run_loop(y, n, seed=0, *, x0_mean=0.0, x0_var=10.0,
             wts = feed["w"][t].astype(dtype)
         rec("w", t, wts)
         w_sum = float(wts.sum(dtype=np.float64))
-        q = tree_cdf(wts, lanes)
+        # cutpoint: the adder tree; the baselines: a sequential cumsum
+        # (filtering.py:299-302)
+        q = tree_cdf(wts, lanes) if resampler == "cutpoint" else sequential_cdf(wts)
         if q is None:
             raise Degenerate(t)
-        # resample (resampling.py:161-177) with u = slot 3 of block t
+        # resample (filtering.py:305-317) with u = slot 3 of block t
         u = unit_open(wt[3])
-        cuts = cut_points(q)
-        idx = np.empty(n, dtype=np.int64)
+        if resampler == "cutpoint":  # resampling.py:161-177
+            cuts = cut_points(q)
+            idx = np.empty(n, dtype=np.int64)
 
-        def lane(lo, hi):
-            idx[lo:hi] = cutpoint_indices(q, cuts, u[lo:hi])
+            def lane(lo, hi):
+                idx[lo:hi] = cutpoint_indices(q, cuts, u[lo:hi])
 
-        lanes.run(n, lane)
+            lanes.run(n, lane)
+        else:
+            # systematic draws one uniform from the aux stream 2^62 (counter t-1)
+            v_aux = (uniforms_at(seed, np.array([AUX_STREAM_BASE], dtype=np.uint64),
+                                 np.array([t - 1], dtype=np.uint64))[0]
+                     if resampler == "systematic" else None)
+            idx = merge_indices(q, resample_uniforms(resampler, u, n, v_aux))
         rec("u", t, u)
         rec("idx", t, idx)
         take = idx - 1

@@ -99,19 +99,23 @@ def test_lookup_equals_searchsorted_left():
 
 
 RUNS = ["run_pl", "run_pl_fixed_tau", "run_pl_priors", "run_pf", "run_pf_model", "run_pl_single"]
+# the reference's sequential baseline resamplers (resampling.py:29-87), some at non-power-of-two N
+RESAMPLER_RUNS = ["run_pl_sorted", "run_pl_systematic", "run_pl_stratified", "run_pl_naive",
+                  "run_pf_sorted", "run_pl_sorted_single"]
 
 
 def _oracle_kwargs(d):
+    kw = {"resampler": str(d["resampler"])} if "resampler" in d else {}
     if "prior" in d:
         p = d["prior"]
         s2 = (p[2], p[3]) if p[2] > 0 else float(p[3])
         t2 = (p[4], p[5]) if p[4] > 0 else float(p[5])
-        return dict(x0_mean=p[0], x0_var=p[1], sigma2=s2, tau2=t2)
+        return dict(x0_mean=p[0], x0_var=p[1], sigma2=s2, tau2=t2, **kw)
     m = d["model"]
-    return dict(x0_mean=m[2], x0_var=m[3], sigma2=float(m[0]), tau2=float(m[1]))
+    return dict(x0_mean=m[2], x0_var=m[3], sigma2=float(m[0]), tau2=float(m[1]), **kw)
 
 
-@pytest.mark.parametrize("name", RUNS)
+@pytest.mark.parametrize("name", RUNS + RESAMPLER_RUNS)
 def test_full_loop_restatement_matches_reference(name):
     d = golden(name)
     rec = {}
