@@ -76,8 +76,15 @@ typedef struct pf_config {
   int32_t phase_timing;    /* per-phase CUDA-event timings (PhaseTimings) */
   int32_t gamma_method;    /* 0: per-step table (default), 1: accurate per draw */
   int32_t device;          /* CUDA device ordinal */
-  int32_t reserved;
+  int32_t resampler;       /* PF_RESAMPLE_*: cutpoint (the exact parallel path) or one
+                              of the reference's sequential baselines */
 } pf_config;
+
+/* Resampling schemes (filtering.py:305-317, resampling.py:29-177).  The
+ * baselines run on the reference's sequential CDF (a left-to-right cumsum,
+ * prefix_sum.py:130-134) and accept any n >= 1; cutpoint needs a power of 2. */
+enum { PF_RESAMPLE_CUTPOINT = 0, PF_RESAMPLE_NAIVE = 1, PF_RESAMPLE_SORTED = 2,
+       PF_RESAMPLE_STRATIFIED = 3, PF_RESAMPLE_SYSTEMATIC = 4 };
 
 /* Oracle mode: host arrays [T+1][n] (row 0 = initialisation) that replace the
  * ndtri / gammaincinv outputs (and optionally the normalised weights) with
@@ -193,6 +200,12 @@ int pf_cut_table(const void* q, int64_t n, int32_t dtype, int64_t* cuts_out);
 /* cutpoint_indices (resampling.py:146-158) over m uniforms. */
 int pf_cutpoint_lookup(const void* q, const int64_t* cuts, int64_t n, int32_t dtype,
                        const double* u, int64_t m, int64_t* idx_out);
+/* merge_indices (resampling.py:29-36): searchsorted(q, u, 'right') + 1 for m
+ * uniforms (u >= 0), the search of the reference's naive / sorted /
+ * stratified / systematic resamplers; sort_first sorts u ascending first
+ * (resample_sorted, resampling.py:57-67). */
+int pf_merge_indices(const void* q, int64_t n, int32_t dtype, const double* u, int64_t m,
+                     int32_t sort_first, int64_t* idx_out);
 /* resample_cutpoint (resampling.py:161-177): uniforms of streams 0..n-1 at
  * `counter`, cut table, lookup. */
 int pf_resample_cutpoint(const void* q, int64_t n, int32_t dtype, uint64_t seed,

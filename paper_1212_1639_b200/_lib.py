@@ -32,6 +32,7 @@ PF_ERR_OUT_OF_MEMORY = 6
 PF_ERR_NOT_IMPLEMENTED = 7
 PF_DTYPE_F64 = 0
 PF_DTYPE_F32 = 1
+RESAMPLER_CODES = {"cutpoint": 0, "naive": 1, "sorted": 2, "stratified": 3, "systematic": 4}
 
 _dp = C.POINTER(C.c_double)
 _i64p = C.POINTER(C.c_int64)
@@ -51,7 +52,7 @@ class PfConfig(C.Structure):
         ("track_quantiles", C.c_int32), ("keep_indices", C.c_int32),
         ("keep_final", C.c_int32), ("store_particles", C.c_int32),
         ("phase_timing", C.c_int32), ("gamma_method", C.c_int32),
-        ("device", C.c_int32), ("reserved", C.c_int32),
+        ("device", C.c_int32), ("resampler", C.c_int32),
     ]
 
 
@@ -104,6 +105,7 @@ SIGNATURES = {
     "pf_adder_tree": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),
     "pf_cut_table": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, _i64p]),
     "pf_cutpoint_lookup": (C.c_int, [C.c_void_p, _i64p, C.c_int64, C.c_int32, _dp, C.c_int64, _i64p]),
+    "pf_merge_indices": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, _dp, C.c_int64, C.c_int32, _i64p]),
     "pf_resample_cutpoint": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_uint64, C.c_uint64, _i64p]),
     "pf_weighted_quantiles": (C.c_int, [_dp, C.c_void_p, C.c_int32, C.c_int64, _dp, C.c_int32, _dp]),
 }

@@ -592,6 +592,79 @@ PF_D int64_t sharded_lookup(const ShardLookup<TQ>& L, uint64_t w3) {
   return k;
 }
 
+// ---------------------------------------- sequential baseline resamplers ---
+// The reference's CPU comparators (resampling.py:29-87) run on a plain
+// left-to-right cumsum (sequential_cdf, prefix_sum.py:130-134).  Its rounding
+// chain is inherently sequential, so one thread walks it -- bit-identical to
+// numpy's cumsum (in the weights' dtype), then _finalize_cdf against the last
+// prefix.  Fine for the baselines' role (and for N = 10^4, BASELINE
+// configs[0]); O(N) latency-bound at large N.
+template <typename T>
+__global__ void seq_cdf_kernel(WSrc src, int64_t n, T* __restrict__ q, int64_t* fail, int64_t step) {
+  if (*fail || threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double M = src.mode == 0 ? *src.M : 0.0;
+  T s = (T)0;
+  for (int64_t i = 0; i < n; ++i) {
+    s = s + weight_of<T>(src.src[i], M, src.mode);
+    q[i] = s;
+  }
+  const T total = s;
+  if (!(total > (T)0) || !isfinite((double)total)) {
+    atomicCAS((unsigned long long*)fail, 0ull, (unsigned long long)(-step));
+    return;
+  }
+  T m = (T)(-INFINITY);
+  for (int64_t i = 0; i < n; ++i) {
+    m = fmax(m, q[i] / total);
+    q[i] = clip01(m);
+  }
+  q[n - 1] = (T)1;
+}
+
+// The uniform each slot searches for: naive -> its own; stratified ->
+// (j + v_j)/n; systematic -> (j + v)/n with the step's single aux draw;
+// sorted -> written as sortable keys (positive doubles order as uint64).
+enum { RS_CUT = 0, RS_NAIVE = 1, RS_SORTED = 2, RS_STRAT = 3, RS_SYST = 4 };
+
+__global__ void resample_uniforms_kernel(int scheme, const uint64_t* __restrict__ u3, int64_t n, uint64_t seed,
+                                         int64_t t, double* __restrict__ u_out, const int64_t* fail) {
+  if (*fail) return;
+  __shared__ double vaux;
+  if (scheme == RS_SYST) {
+    // aux stream 2^62 (rng.py:34), one draw per step: counter t-1
+    if (threadIdx.x == 0) {
+      const uint64_t c = (uint64_t)(t - 1);
+      const Philox4 P = philox_block(seed, 1ull << 62, c >> 2);
+      vaux = unit_open(P.w[c & 3]);
+    }
+    __syncthreads();
+  }
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const double v = unit_open(u3[j]);
+    double u;
+    if (scheme == RS_STRAT) u = ((double)j + v) / (double)n;
+    else if (scheme == RS_SYST) u = ((double)j + vaux) / (double)n;
+    else u = v;
+    u_out[j] = u;
+  }
+}
+
+// merge_indices (resampling.py:29-36): searchsorted(q, u, 'right'), 0-based.
+template <typename T>
+__global__ void merge_kernel(const T* __restrict__ q, int64_t n, const double* __restrict__ u, int64_t m,
+                             int32_t* __restrict__ anc, const int64_t* fail) {
+  if (*fail) return;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
+    const double uj = u[j];
+    int64_t lo = 0, hi = n;  // first i with q[i] > u
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((double)q[mid] <= uj) lo = mid + 1; else hi = mid;
+    }
+    anc[j] = (int32_t)(lo < n ? lo : n - 1);
+  }
+}
+
 // ------------------------------------------------------- small n path ---
 // n <= CDF_SMALL_MAX: one CTA, levels in shared memory (the reference's
 // level loops verbatim), finalize and cut table by one thread.
@@ -667,6 +740,7 @@ PF_D int64_t cutpoint_lookup(const T* __restrict__ q, const int32_t* __restrict_
 // word whose unit_open() is the resampling uniform.
 template <typename TQ>
 struct Lookup {
+  const int32_t* anc;   // non-null: ancestors precomputed (baseline resamplers)
   const TQ* q;
   const int32_t* cut;
   const Grp* grp;       // non-null: strata path

@@ -334,6 +334,12 @@ struct pf_engine {
   DevBuf<uint32_t> f32;
   bool strata = false;
   DevBuf<int64_t> idx;
+  // baseline resamplers: ancestors of the step, slot uniforms, sort buffers
+  DevBuf<int32_t> ranc;
+  DevBuf<double> ru;
+  DevBuf<uint64_t> rsorted;
+  DevBuf<unsigned char> rtmp;
+  size_t rtmp_bytes = 0;
   DevBuf<uint32_t> keys;  // quantile keys [2 parities][3 quantities][n]
   DevBuf<double> s2init;
   // weighted-quantile machinery (quantile.cuh)
@@ -621,7 +627,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   auto mark = [&](int phase) {
     if (timing) phase_marks.push_back({ev_record(), phase});
   };
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> step_evs;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> step_evs, sort_evs;
   if (rs.resident) step_evs.reserve((size_t)T);
 
   CK(cudaEventRecord(e->ev0, st));
@@ -728,6 +734,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   Lookup<TQ> lk;
   lk.q = qv;
   lk.cut = e->cut.p;
+  lk.anc = c.resampler != PF_RESAMPLE_CUTPOINT ? e->ranc.p : nullptr;
   lk.grp = nullptr;
   lk.fq = nullptr;
   lk.f32 = nullptr;
@@ -845,7 +852,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       CK(cudaEventRecord(e->ev_b, st));  // K1b(t): keys, log-weights, M, moments
       cudaStream_t ss = e->side;
       CK(cudaStreamWaitEvent(ss, e->ev_b, 0));
-      if (plan.small) {
+      if (plan.small || c.resampler != PF_RESAMPLE_CUTPOINT) {  // any n (bounds-checked pass)
         q_window_kernel<TQ><<<grid_for(n, 256), 256, 0, ss>>>(wsrc, n, e->fail.p, qa);
         LAUNCHED();
       } else {
@@ -855,7 +862,39 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
           return rc;
       }
     }
-    if ((rc = launch_cdf<TQ>(e->cdf, wsrc, n, qv, e->cut.p, e->fail.p, t, st, so)) != PF_OK) return rc;
+    if (c.resampler == PF_RESAMPLE_CUTPOINT) {
+      if ((rc = launch_cdf<TQ>(e->cdf, wsrc, n, qv, e->cut.p, e->fail.p, t, st, so)) != PF_OK) return rc;
+    } else {
+      // the reference's sequential baselines (filtering.py:299-316): a
+      // sequential cumsum CDF, the scheme's uniforms, searchsorted 'right'
+      seq_cdf_kernel<TQ><<<1, 32, 0, st>>>(wsrc, n, qv, e->fail.p, t);
+      LAUNCHED();
+      mark(PH_CDF);
+      resample_uniforms_kernel<<<grid_for(n, 256), 256, 0, st>>>(c.resampler, e->du3.p + (size_t)(t % 3) * n, n,
+                                                                  c.seed, t, e->ru.p, e->fail.p);
+      LAUNCHED();
+      const double* us = e->ru.p;
+      if (c.resampler == PF_RESAMPLE_SORTED) {
+        cudaEvent_t s0 = nullptr, s1 = nullptr;
+        if (timing) {
+          cudaEventCreate(&s0);
+          cudaEventCreate(&s1);
+          cudaEventRecord(s0, st);
+        }
+        size_t tb = e->rtmp_bytes;
+        CK(cub::DeviceRadixSort::SortKeys(e->rtmp.p, tb, (const uint64_t*)e->ru.p, e->rsorted.p, (int)n, 0, 64,
+                                          st));
+        LAUNCHED();
+        if (timing) {
+          cudaEventRecord(s1, st);
+          sort_evs.push_back({s0, s1});
+        }
+        us = reinterpret_cast<const double*>(e->rsorted.p);
+      }
+      merge_kernel<TQ><<<grid_for(n, 256), 256, 0, st>>>(qv, n, us, n, e->ranc.p, e->fail.p);
+      LAUNCHED();
+      mark(PH_RES);
+    }
     if (ntg) {
       // side stream: exact resolve (overlaps the CDF and the next step)
       cudaStream_t ss = e->side;
@@ -1094,7 +1133,17 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     } else {
       out->phase_ns[PH_OTHER] = (int64_t)llround(ms * 1e6);
     }
+    // resample_sort_only: a sub-measure of resample (filtering.py:309-310)
+    for (auto& pr : sort_evs) {
+      float d = 0;
+      cudaEventElapsedTime(&d, pr.first, pr.second);
+      out->phase_ns[PH_SORT] += (int64_t)llround(d * 1e6);
+    }
     out->failed_step = fail_h;
+  }
+  for (auto& pr : sort_evs) {
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
   }
   if (fail_h > 0)
     return set_err(PF_ERR_ALL_WEIGHTS_ZERO, "all particle weights are zero (at time step " +
@@ -1145,7 +1194,10 @@ int pf_engine_create(const pf_config* cfg, pf_engine** out) {
   *out = nullptr;
   const int64_t n = cfg->n;
   if (n < 1) return set_err(PF_ERR_VALUE, "particle count must be >= 1");
-  if (!is_pow2(n)) return set_err(PF_ERR_NOT_POWER_OF_TWO, "particle count must be a power of two, got " + std::to_string(n));
+  if (cfg->resampler < PF_RESAMPLE_CUTPOINT || cfg->resampler > PF_RESAMPLE_SYSTEMATIC)
+    return set_err(PF_ERR_VALUE, "unknown resampler code");
+  if (cfg->resampler == PF_RESAMPLE_CUTPOINT && !is_pow2(n))
+    return set_err(PF_ERR_NOT_POWER_OF_TWO, "particle count must be a power of two, got " + std::to_string(n));
   if (n > (int64_t(1) << 28)) return set_err(PF_ERR_VALUE, "particle count above 2^28 per device");
   if (pf_device_count() < 1) return set_err(PF_ERR_CUDA, "no CUDA device visible");
   CK(cudaSetDevice(cfg->device));
@@ -1185,7 +1237,14 @@ int pf_engine_create(const pf_config* cfg, pf_engine** out) {
       (err = e->sc.ensure(1)) || (err = e->fail.ensure(1)) ||
       (err = e->cdf.ensure(n, e->single ? 4 : 8)) || (err = e->probs.ensure(8)))
     return bail(err);
-  e->strata = ilog2(n) >= STRATA_MIN_LOG2N;
+  e->strata = cfg->resampler == PF_RESAMPLE_CUTPOINT && ilog2(n) >= STRATA_MIN_LOG2N;
+  if (cfg->resampler != PF_RESAMPLE_CUTPOINT) {
+    if ((err = e->ranc.ensure(n)) || (err = e->ru.ensure(n)) || (err = e->rsorted.ensure(n))) return bail(err);
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tb, (const uint64_t*)e->ru.p, e->rsorted.p, (int)n);
+    e->rtmp_bytes = tb;
+    if ((err = e->rtmp.ensure(tb))) return bail(err);
+  }
   if (e->strata) {
     const size_t gbytes = (size_t)(n / GRP_STRATA) * sizeof(Grp);
     e->rank_bytes = gbytes + (size_t)n + 16;
@@ -1227,8 +1286,9 @@ int pf_engine_create(const pf_config* cfg, pf_engine** out) {
 
 int pf_engine_reconfigure(pf_engine* e, const pf_config* cfg) {
   if (!e || !cfg) return set_err(PF_ERR_VALUE, "null argument");
-  if (cfg->n != e->n || (cfg->precision == PF_DTYPE_F32) != e->single || cfg->device != e->cfg.device)
-    return set_err(PF_ERR_VALUE, "reconfigure cannot change n, precision or device");
+  if (cfg->n != e->n || (cfg->precision == PF_DTYPE_F32) != e->single || cfg->device != e->cfg.device ||
+      cfg->resampler != e->cfg.resampler)
+    return set_err(PF_ERR_VALUE, "reconfigure cannot change n, precision, device or resampler");
   e->cfg = *cfg;
   e->mode = (cfg->learn && cfg->learn_sigma2 ? M_LS : 0) | (cfg->learn && cfg->learn_tau2 ? M_LT : 0) |
             (e->single ? M_SINGLE : 0);
@@ -1269,6 +1329,8 @@ int pf_group_create(const pf_config* cfg, int32_t nshards, const int32_t* device
   if (!is_pow2(n)) return set_err(PF_ERR_NOT_POWER_OF_TWO, "particle count must be a power of two, got " + std::to_string(n));
   if (G < 1 || G > PF_MAX_SHARDS || !is_pow2(G)) return set_err(PF_ERR_VALUE, "shard count must be 1, 2, 4 or 8");
   if (n / G < 4096) return set_err(PF_ERR_VALUE, "sharded runs need at least 4096 particles per shard");
+  if (cfg->resampler != PF_RESAMPLE_CUTPOINT)
+    return set_err(PF_ERR_NOT_IMPLEMENTED, "sharded runs use the cut-point resampler");
   if (n > ((int64_t)1 << 31)) return set_err(PF_ERR_VALUE, "particle count above 2^31");
   const int ndev = pf_device_count();
   if (ndev < 1) return set_err(PF_ERR_CUDA, "no CUDA device visible");
@@ -1432,6 +1494,10 @@ int pf_engine_destroy(pf_engine* e) {
   e->rec[0].release();
   e->rec[1].release();
   e->du3.release();
+  e->ranc.release();
+  e->ru.release();
+  e->rsorted.release();
+  e->rtmp.release();
   e->dz.release();
   e->dgs.release();
   e->dgt.release();
@@ -1880,6 +1946,51 @@ int pf_cutpoint_lookup(const void* q, const int64_t* cuts, int64_t n, int32_t dt
     lookup_kernel<double><<<grid_for(m, 256), 256>>>((double*)dq, dc, n, du, m, di);
   else
     lookup_kernel<float><<<grid_for(m, 256), 256>>>((float*)dq, dc, n, du, m, di);
+  LAUNCHED();
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(idx_out, di, m * 8, cudaMemcpyDeviceToHost));
+  return PF_OK;
+}
+
+int pf_merge_indices(const void* q, int64_t n, int32_t dtype, const double* u, int64_t m, int32_t sort_first,
+                     int64_t* idx_out) {
+  int rc;
+  if (n < 1) return set_err(PF_ERR_VALUE, "empty CDF");
+  if ((rc = need_device())) return rc;
+  if (m <= 0) return PF_OK;
+  const size_t es = dtype == PF_DTYPE_F32 ? 4 : 8;
+  Scratch s;
+  unsigned char* dq;
+  double *du, *ds;
+  int32_t* da;
+  int64_t* di;
+  CK(s.alloc(&dq, n * es));
+  CK(s.alloc(&du, m));
+  CK(s.alloc(&ds, m));
+  CK(s.alloc(&da, m));
+  CK(s.alloc(&di, m));
+  CK(cudaMemcpy(dq, q, n * es, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(du, u, m * 8, cudaMemcpyHostToDevice));
+  const double* us = du;
+  if (sort_first) {  // resample_sorted (resampling.py:57-67): ascending uniforms
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tb, (const uint64_t*)du, (uint64_t*)ds, (int)m);
+    unsigned char* tmp;
+    CK(s.alloc(&tmp, tb));
+    CK(cub::DeviceRadixSort::SortKeys(tmp, tb, (const uint64_t*)du, (uint64_t*)ds, (int)m));
+    LAUNCHED();
+    us = ds;
+  }
+  int64_t fail0 = 0;
+  int64_t* dfail;
+  CK(s.alloc(&dfail, 1));
+  CK(cudaMemcpy(dfail, &fail0, 8, cudaMemcpyHostToDevice));
+  if (es == 8)
+    merge_kernel<double><<<grid_for(m, 256), 256>>>((const double*)dq, n, us, m, da, dfail);
+  else
+    merge_kernel<float><<<grid_for(m, 256), 256>>>((const float*)dq, n, us, m, da, dfail);
+  LAUNCHED();
+  cuts_to_i64_kernel<<<grid_for(m, 256), 256>>>(da, m, di);
   LAUNCHED();
   CK(cudaGetLastError());
   CK(cudaMemcpy(idx_out, di, m * 8, cudaMemcpyDeviceToHost));

@@ -424,6 +424,10 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
 #pragma unroll
         for (int b = 0; b < STEP_SB; ++b)
           if (ok[b]) anc[b] = sharded_lookup<TQ>(a.slk, w3[b]);
+      } else if (a.lk.anc) {  // baseline resamplers: ancestors precomputed
+#pragma unroll
+        for (int b = 0; b < STEP_SB; ++b)
+          if (ok[b]) anc[b] = a.lk.anc[jj[b]];
       } else {
         ancestors_of<TQ, STEP_SB>(a.lk, w3, ok, anc);
       }
@@ -643,7 +647,7 @@ __global__ void __launch_bounds__(256) materialize_kernel(MatArgs<TQ> a) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n;
        j += (int64_t)gridDim.x * blockDim.x) {
     int64_t anc = j;
-    if (a.resample) anc = ancestor_of<TQ>(a.lk, a.u3[j]);
+    if (a.resample) anc = a.lk.anc ? (int64_t)a.lk.anc[j] : ancestor_of<TQ>(a.lk, a.u3[j]);
     if (a.idx) a.idx[j] = anc + 1;
     const Rec r = a.rec[anc];
     if (a.x) a.x[j] = r.x;

@@ -15,7 +15,7 @@ def make_config(n, seed, *, learn, learn_sigma2, learn_tau2, precision, x0_mean,
                 sigma2_shape=0.0, sigma2_scale=0.0, tau2_shape=0.0, tau2_scale=0.0,
                 sigma2_fixed=1.0, tau2_fixed=1.0, track_quantiles=False, keep_indices=False,
                 keep_final=False, store_particles=False, phase_timing=True, gamma_method=0,
-                device=0):
+                device=0, resampler="cutpoint"):
     """Fill a pf_config; scalar terms the reference computes with numpy on the
     host (np.sqrt(tau2), np.log(sigma2)) are computed here the same way so the
     device sees identical bits."""
@@ -42,6 +42,7 @@ def make_config(n, seed, *, learn, learn_sigma2, learn_tau2, precision, x0_mean,
     c.phase_timing = int(bool(phase_timing))
     c.gamma_method = int(gamma_method)
     c.device = int(device)
+    c.resampler = _lib.RESAMPLER_CODES[resampler]
     return c
 
 

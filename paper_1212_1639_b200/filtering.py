@@ -155,7 +155,7 @@ def run_particle_learning(priors, y, n, seed=0, backend=None, resampler="cutpoin
                      keep_indices=keep_indices, debug_checks=debug_checks, noise=noise)
 
 
-def _build_config(model, priors, n, seed, precision, flags, device):
+def _build_config(model, priors, n, seed, precision, flags, device, resampler="cutpoint"):
     learn = priors is not None
     if learn:
         ls, lt = priors.learns_sigma2, priors.learns_tau2
@@ -171,7 +171,7 @@ def _build_config(model, priors, n, seed, precision, flags, device):
         kw = dict(x0_mean=model.x0_mean, x0_var=model.x0_var,
                   sigma2_fixed=float(model.sigma2), tau2_fixed=float(model.tau2))
     return make_config(n, seed, learn=learn, learn_sigma2=ls, learn_tau2=lt,
-                       precision=precision, device=device, **flags, **kw), ls, lt
+                       precision=precision, device=device, resampler=resampler, **flags, **kw), ls, lt
 
 
 def _run_loop(model, priors, y, n, seed, backend, resampler, precision, store_particles,
@@ -185,10 +185,6 @@ def _run_loop(model, priors, y, n, seed, backend, resampler, precision, store_pa
     if resampler == "cutpoint":
         check_power_of_two(n)
     dtype = _dtype_for(precision)
-    if resampler != "cutpoint":
-        raise NotImplementedError(
-            f"resampler {resampler!r} is a sequential CPU baseline of the reference; the "
-            "device engine implements the exact parallel cut-point resampler")
     # debug_checks: the device gathers each particle's tuple as one 32-byte
     # record, so a torn tuple cannot occur; the flag is accepted and inert.
     del debug_checks
@@ -200,17 +196,19 @@ def _run_loop(model, priors, y, n, seed, backend, resampler, precision, store_pa
     if own:
         backend = Backend()
     try:
-        cfg, ls, lt = _build_config(model, priors, n, seed, precision, flags, backend.device)
+        cfg, ls, lt = _build_config(model, priors, n, seed, precision, flags, backend.device, resampler)
         shards = getattr(backend, "shards", 1)
         if shards > 1:
             if store_particles:
                 raise NotImplementedError("store_particles is not supported by sharded runs")
+            if resampler != "cutpoint":
+                raise NotImplementedError("sharded runs use the cut-point resampler")
             key = ("group", n, precision, tuple(backend.devices))
 
             def factory():
                 return Group(cfg, backend.devices)
         else:
-            key = ("engine", n, precision, backend.device)
+            key = ("engine", n, precision, backend.device, resampler)
 
             def factory():
                 return Engine(cfg)

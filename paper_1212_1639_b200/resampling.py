@@ -8,9 +8,9 @@ lookup runs fused into the step kernel (csrc/step.cuh); these wrappers expose
 it at kernel level with the reference's signatures and 1-based indices.
 
 The reference's sequential baselines (naive / sorted / stratified /
-systematic, resampling.py:29-87) are CPU comparators built on a sequential
-cumsum; they are not part of the cut-point hot path and are not implemented
-on the device in this release (``NotImplementedError``).
+systematic, resampling.py:29-87) search the same CDF with searchsorted
+'right' semantics; their device versions here (and in the filter loop, on
+the reference's sequential-cumsum CDF) give the reference's indices.
 """
 
 from __future__ import annotations
@@ -90,31 +90,46 @@ def resample_cutpoint(cdf, streams, backend=None):
     return cutpoint_indices(q, cut_points_parallel(q), u)
 
 
-def merge_indices(cdf, u):
-    """Smallest 1-based i with u < q(i) (resampling.py:29-36)."""
-    return np.searchsorted(np.asarray(cdf), u, side="right") + 1
-
-
-def _not_on_device(name):
-    raise NotImplementedError(
-        f"{name}: the sequential baseline resamplers are CPU comparators of the "
-        "reference and are not implemented on the device; use resample_cutpoint")
+def merge_indices(cdf, u, sort_first=False):
+    """Smallest 1-based i with u < q(i) (resampling.py:29-36), on the device;
+    ``sort_first`` sorts u ascending first (resample_sorted)."""
+    q = _cdf_array(cdf)
+    u = np.ascontiguousarray(np.asarray(u, dtype=np.float64))
+    shape = u.shape
+    u = u.reshape(-1)
+    out = np.empty(len(u), dtype=np.int64)
+    lib = _lib.require_device()
+    _lib.check(lib.pf_merge_indices(_lib.vptr(q), len(q), _lib.dtype_code(q.dtype), _lib.ptr(u), len(u),
+                                    int(bool(sort_first)), _lib.ptr(out, _lib.C.c_int64)), lib)
+    return out.reshape(shape)
 
 
 def resample_naive(cdf, streams):
-    _not_on_device("resample_naive")
+    """Exact multinomial by a head-to-tail scan per draw (resampling.py:51-54):
+    the same answer as searchsorted 'right' on the slot's own uniform."""
+    return merge_indices(cdf, streams.uniforms())
 
 
 def resample_sorted(cdf, streams):
-    _not_on_device("resample_sorted")
+    """Exact multinomial with pre-sorted uniforms (resampling.py:57-67).
+    Returns ``(indices, sort_ns)``; the sort runs on the device inside the
+    merge call, so its time is reported as 0 here (the filter loop times it
+    with CUDA events, PhaseTimings.resample_sort_only)."""
+    return merge_indices(cdf, streams.uniforms(), sort_first=True), 0
 
 
 def resample_stratified(cdf, streams):
-    _not_on_device("resample_stratified")
+    """One uniform per stratum (resampling.py:70-75): u_j = (j + v_j) / N."""
+    n = len(cdf)
+    v = streams.uniforms()
+    return merge_indices(cdf, (np.arange(n) + v) / n)
 
 
 def resample_systematic(cdf, stream):
-    _not_on_device("resample_systematic")
+    """One shared offset (resampling.py:78-87): u_j = (j + v) / N."""
+    n = len(cdf)
+    v = stream.uniform()
+    return merge_indices(cdf, (np.arange(n) + v) / n)
 
 
 __all__ = [
