@@ -251,10 +251,10 @@ struct RankOut {  // K4 outputs on the strata path
 };
 
 template <typename T>
-PF_D uint32_t strata_f(T q, int64_t L, int B) {
+PF_D uint32_t strata_f(T q, int64_t L, double unitB /* 2^B */) {
   if (L <= 0) return 0u;
   const double x = (double)q * 9007199254740992.0;          // q 2^53, exact
-  const double sub = (double)(L - 1) * ldexp(1.0, B);       // exact
+  const double sub = (double)(L - 1) * unitB;               // exact
   const double d = floor(x - sub);                          // exact (Sterbenz)
   return d >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)d;
 }
@@ -404,6 +404,7 @@ cdf_expand_kernel(WSrc src, int64_t n, int R, const T* __restrict__ tile_tot,
     for (int w = 0; w < warp; ++w) pre = fmax(pre, wmax[w]);
     pre = fmax(pre, excl);
     // finalize and scatter the cut table
+    const double unitB = STRATA ? ldexp(1.0, ro.B) : 0.0;
     T qv[CDF_V];
     int64_t Lprev = (int64_t)ceil(clip01(pre) * nf);
     uint64_t fqw = 0;
@@ -417,7 +418,7 @@ cdf_expand_kernel(WSrc src, int64_t n, int R, const T* __restrict__ tile_tot,
       int32_t* ct = STRATA ? ro.cut : cut_out;
       for (int64_t kk = Lprev; kk < L; ++kk) ct[kk] = (int32_t)(gbase + base + i);
       if (STRATA) {
-        const uint32_t f = strata_f<T>(qi, L, ro.B);
+        const uint32_t f = strata_f<T>(qi, L, unitB);
         fx[i] = f;
         const uint32_t h = f >> (ro.B - 8);
         fqw |= (uint64_t)(h > 255u ? 255u : h) << (8 * i);
