@@ -23,7 +23,7 @@
 namespace pf {
 
 constexpr double LOG_TWO_PI = 1.8378770664093453;  // math.log(2*math.pi), models.py:20
-constexpr int STEP_SB = 3;  // slots per thread per pipeline stage (double buffered)
+constexpr int STEP_SB = 2;  // slots per thread per pipeline stage (double buffered)
 
 // Order-preserving 32-bit image of a double (float32 rounded down, sign
 // folded): the quantile keys of quantile.cuh.
