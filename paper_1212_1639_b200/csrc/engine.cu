@@ -678,31 +678,30 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   const bool share_tab = LS && LT && e->tab_s == e->tab_t && c.gamma_method == 0;
   const int ngt = c.gamma_method == 0 ? (LS ? 1 : 0) + (LT && !share_tab ? 1 : 0) : 0;
   const size_t draw_smem = ((size_t)ngt * GT_TABLE_DOUBLES + (e->ntab ? NT_TABLE_DOUBLES : 0)) * sizeof(double);
-  const size_t step_smem = (size_t)2 * STEP_SB * 256 * (sizeof(Rec) + 3 * sizeof(double));
+  // The step kernel computes the next step's draws itself (FD): 512 threads,
+  // shared memory = the step's tables + the double-buffered gather stage.
+  constexpr int STEP_THREADS = 512;
+  const size_t step_smem = (size_t)(((draw_smem / 8) + 3) & ~size_t(3)) * 8 +
+                           (size_t)2 * STEP_SB * STEP_THREADS * (sizeof(Rec) + 3 * sizeof(double));
   {
     static bool attr[8] = {false};
     if (!attr[MODE]) {
       CK(cudaFuncSetAttribute(draws_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)((2 * GT_TABLE_DOUBLES + NT_TABLE_DOUBLES) * sizeof(double))));
-      CK(cudaFuncSetAttribute(step_kernel<MODE, TQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)step_smem));
+      CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)((2 * GT_TABLE_DOUBLES + NT_TABLE_DOUBLES + 4) * sizeof(double) +
+                                    2 * STEP_SB * STEP_THREADS * (sizeof(Rec) + 3 * sizeof(double)))));
       attr[MODE] = true;
     }
   }
   int occ = 0, docc = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, step_kernel<MODE, TQ>, 256, step_smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, step_kernel<MODE, TQ, true>, STEP_THREADS, step_smem));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&docc, draws_kernel<MODE>, 256, draw_smem));
   if (occ < 1) occ = 1;
   if (docc < 1) docc = 1;
   // persistent grids: one wave of resident CTAs
-  const int64_t nbatches = (n + STEP_SB * 256 - 1) / (STEP_SB * 256);
-  // The step kernel keeps fewer CTAs per SM than it could, leaving room for
-  // the next step's draws_kernel to run beside it (PF_STEP_CTAS overrides).
-  static const int step_ctas = [] {
-    const char* v = getenv("PF_STEP_CTAS");
-    return v ? atoi(v) : 2;
-  }();
-  const int step_grid = (int)std::min<int64_t>(nbatches, (int64_t)sms * std::min(occ, std::max(1, step_ctas)));
+  const int64_t nbatches = (n + STEP_SB * STEP_THREADS - 1) / (STEP_SB * STEP_THREADS);
+  const int step_grid = (int)std::min<int64_t>(nbatches, (int64_t)sms * occ);
   const int draw_grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sms * docc);
   auto launch_draws = [&](int64_t t, cudaStream_t s_) {
     DrawArgs d;
@@ -797,7 +796,6 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       a.g_t = fgt ? row(fgt, t) : e->dgt.p + off;
     }
     a.feed_w = row(fw, t);
-    if (t > 1) CK(cudaStreamWaitEvent(st, e->ev_draw, 0));
     // the side stream's step t-2 work reads the buffers this step overwrites
     if (ntg && t > 2) CK(cudaStreamWaitEvent(st, e->ev_q[t & 1], 0));
     a.kx = want_fq ? kbase : nullptr;
@@ -814,28 +812,42 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     a.fail = e->fail.p;
     a.xrec = nullptr;
     a.shard = 0;
+    // the draws of step t+1 (buffers of step t-2, last read by step t-1)
+    memset(&a.nd, 0, sizeof(a.nd));
+    if (t < T) {
+      a.nd.n = n;
+      a.nd.t = t + 1;
+      a.nd.seed = c.seed;
+      a.nd.gs = gamma_src(e, true, t + 1);
+      a.nd.gt = gamma_src(e, false, t + 1);
+      a.nd.ntab = e->ntab;
+      const size_t off = (size_t)((t + 1) % 3) * n;
+      a.nd.z = e->dz.p + off;
+      a.nd.g_s = e->dgs.p + off;
+      a.nd.g_t = e->dgt.p + off;
+      a.nd.u3 = e->du3.p + off;
+      a.nd.fail = e->fail.p;
+      a.nd.gbase = 0;
+    } else {
+      // last step: no next draws, but the kernel stages the same tables
+      a.nd.gs = gamma_src(e, true, t);
+      a.nd.gt = gamma_src(e, false, t);
+      a.nd.ntab = e->ntab;
+    }
     if (rs.resident) {
       cudaEvent_t b0, b1;
       cudaEventCreate(&b0);
       cudaEventCreate(&b1);
       cudaEventRecord(b0, st);
-      step_kernel<MODE, TQ><<<step_grid, 256, step_smem, st>>>(a);
+      step_kernel<MODE, TQ, true><<<step_grid, STEP_THREADS, step_smem, st>>>(a);
       cudaEventRecord(b1, st);
       step_evs.push_back({b0, b1});
     } else {
-      step_kernel<MODE, TQ><<<step_grid, 256, step_smem, st>>>(a);
+      step_kernel<MODE, TQ, true><<<step_grid, STEP_THREADS, step_smem, st>>>(a);
     }
     LAUNCHED();
     ++step_launches;
     cur ^= 1;
-    CK(cudaEventRecord(e->ev_steps[t % 3], st));
-    if (t < T) {
-      // draws(t+1) reuse the buffers of step t-2, last read by step t-1: they
-      // run concurrently with step t and the CDF kernels
-      if (t >= 2) CK(cudaStreamWaitEvent(e->dstream, e->ev_steps[(t - 1) % 3], 0));
-      launch_draws(t + 1, e->dstream);
-      CK(cudaEventRecord(e->ev_draw, e->dstream));
-    }
     mark(PH_PROP);
     if (keep_idx && t > 1)
       CK(cudaMemcpyAsync(out->indices + (size_t)(t - 2) * n, e->idx.p, n * sizeof(int64_t),

@@ -153,6 +153,20 @@ struct StepOut {   // device arrays indexed by t-1
   double* t_sd;
 };
 
+struct DrawArgs {
+  int64_t n;
+  int64_t t;
+  uint64_t seed;
+  GammaSrc gs, gt;
+  const double* ntab;    // normal-quantile table (null: Cephes ndtri)
+  double* z;
+  double* g_s;
+  double* g_t;
+  uint64_t* u3;
+  const int64_t* fail;
+  int64_t gbase;         // global index of this shard's first slot (stream id offset)
+};
+
 template <typename TQ>
 struct StepArgs {
   int64_t n;
@@ -181,6 +195,7 @@ struct StepArgs {
   int64_t* fail;
   Partial* xrec;         // sharded run: shard partials [G] (null: single run)
   int shard;
+  DrawArgs nd;           // FD: the draws of step t+1, computed here (nd.z null: none)
   ShardLookup<TQ> slk;   // sharded run (slk.G > 0): cross-shard lookup
   const Rec* recs[PF_MAX_SHARDS];  // sharded run: every shard's records of step t-1
 };
@@ -296,19 +311,6 @@ PF_D void finalize_step(int64_t t, double M, double bsum, const double (&S)[7], 
 // 273,280,286; counter layout rng.py:221-224) -- compute-bound work that
 // runs on its own stream, concurrently with the memory-bound CDF kernels of
 // step t-1.  Writes z, g_sigma, g_tau and the resampling word (slot 3).
-struct DrawArgs {
-  int64_t n;
-  int64_t t;
-  uint64_t seed;
-  GammaSrc gs, gt;
-  const double* ntab;    // normal-quantile table (null: Cephes ndtri)
-  double* z;
-  double* g_s;
-  double* g_t;
-  uint64_t* u3;
-  const int64_t* fail;
-  int64_t gbase;         // global index of this shard's first slot (stream id offset)
-};
 
 PF_D double nt_eval_slot(int off, double u) {
   double t, sc;
@@ -323,8 +325,8 @@ PF_D double nt_eval_slot(int off, double u) {
 // Stage this step's tables in shared memory: gamma table(s) (one copy when
 // sigma2 and tau2 share the shape schedule), then the normal table.
 template <bool LS, bool LT>
-PF_D void stage_tables(const GammaSrc& gs, const GammaSrc& gt, const double* ntab, int& slot_s, int& slot_t,
-                       int& noff) {
+PF_D int stage_tables(const GammaSrc& gs, const GammaSrc& gt, const double* ntab, int& slot_s, int& slot_t,
+                      int& noff) {
   slot_s = slot_t = -1;
   const double* srcs[3] = {LS && gs.method == 0 ? gs.table : nullptr,
                            LT && gt.method == 0 && !(LS && gt.table == gs.table) ? gt.table : nullptr, ntab};
@@ -345,6 +347,7 @@ PF_D void stage_tables(const GammaSrc& gs, const GammaSrc& gt, const double* nta
   }
   if (LS && LT && gs.method == 0 && gt.table == gs.table) slot_t = slot_s;
   __syncthreads();
+  return off;
 }
 
 template <int MODE>
@@ -372,10 +375,17 @@ PF_D void cp_async8(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src));
 }
 
-template <int MODE, typename TQ>
-__global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
+// FD: also compute the draws of step t+1 (Philox block t+1, ndtri and
+// gamma tables of t+1 staged in shared memory) for every slot, in the issue
+// slots the latency-bound gather pipeline leaves idle -- instead of a
+// separate compute-bound draws kernel.
+template <int MODE, typename TQ, bool FD = false>
+__global__ void __launch_bounds__(FD ? 512 : 256) step_kernel(StepArgs<TQ> a) {
   constexpr bool LS = MODE & M_LS, LT = MODE & M_LT, SINGLE = MODE & M_SINGLE;
   if (*a.fail) return;
+  int slot_s = -1, slot_t = -1, noff = -1, tab_doubles = 0;
+  const bool fd = FD && a.nd.z != nullptr;
+  if (FD) tab_doubles = stage_tables<LS, LT>(a.nd.gs, a.nd.gt, a.nd.ntab, slot_s, slot_t, noff);
   const bool feedw = a.feed_w != nullptr;
   const double cs = a.sc->cs, ct = a.sc->ct, cx = a.sc->cx;
   double m = feedw ? 0.0 : -INFINITY;
@@ -393,7 +403,7 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
   const int nth = blockDim.x;
   const int64_t batch = (int64_t)STEP_SB * nth;
   const int64_t nbatches = (a.n + batch - 1) / batch;
-  char* smem = reinterpret_cast<char*>(pf_gtab);
+  char* smem = reinterpret_cast<char*>(pf_gtab + ((tab_doubles + 3) & ~3));
   const size_t buf_bytes = (size_t)STEP_SB * nth * (sizeof(Rec) + 3 * sizeof(double));
   auto rec_at = [&](int buf, int b) {
     return reinterpret_cast<Rec*>(smem + buf * buf_bytes) + b * nth + threadIdx.x;
@@ -532,13 +542,22 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs<TQ> a) {
     s2s = fma(eds, ds, s2s);
     s1t += edt;
     s2t = fma(edt, dt, s2t);
+    if (fd) {
+      // next step's draws for this slot (filtering.py:273,280,286 at t+1)
+      const Philox4 P = philox_block(a.nd.seed, (uint64_t)(a.nd.gbase + j), (uint64_t)(a.t + 1));
+      a.nd.u3[j] = P.w[3];
+      const double u0 = unit_open(P.w[0]);
+      a.nd.z[j] = noff >= 0 ? nt_eval_slot(noff, u0) : ndtri(u0);
+      if (LS) a.nd.g_s[j] = gamma_draw_slot(a.nd.gs, slot_s, unit_open(P.w[1]));
+      if (LT) a.nd.g_t[j] = gamma_draw_slot(a.nd.gt, slot_t, unit_open(P.w[2]));
+    }
   }
     cur ^= 1;
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
 
   // ---- CTA reduction with rescaling to the CTA max
-  __shared__ double red[8][8];
+  __shared__ double red[16][8];
   __shared__ double mblk;
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
