@@ -721,7 +721,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     draws_kernel<MODE><<<draw_grid, 256, draw_smem, s_>>>(d);
     LAUNCHED();
   };
-  if (T >= 1) launch_draws(1, st);
+  (void)launch_draws;  // the step kernel computes its own draws (sharded runs use draws_kernel)
 
   int cur = 0;
   WSrc wsrc;
@@ -812,28 +812,20 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     a.fail = e->fail.p;
     a.xrec = nullptr;
     a.shard = 0;
-    // the draws of step t+1 (buffers of step t-2, last read by step t-1)
-    memset(&a.nd, 0, sizeof(a.nd));
-    if (t < T) {
-      a.nd.n = n;
-      a.nd.t = t + 1;
-      a.nd.seed = c.seed;
-      a.nd.gs = gamma_src(e, true, t + 1);
-      a.nd.gt = gamma_src(e, false, t + 1);
-      a.nd.ntab = e->ntab;
-      const size_t off = (size_t)((t + 1) % 3) * n;
-      a.nd.z = e->dz.p + off;
-      a.nd.g_s = e->dgs.p + off;
-      a.nd.g_t = e->dgt.p + off;
-      a.nd.u3 = e->du3.p + off;
-      a.nd.fail = e->fail.p;
-      a.nd.gbase = 0;
-    } else {
-      // last step: no next draws, but the kernel stages the same tables
-      a.nd.gs = gamma_src(e, true, t);
-      a.nd.gt = gamma_src(e, false, t);
-      a.nd.ntab = e->ntab;
-    }
+    // this step's draws are computed in the step kernel (tables of step t);
+    // only the resampling word goes to memory (for step t+1's lookups)
+    memset(&a.dr, 0, sizeof(a.dr));
+    a.dr.n = n;
+    a.dr.t = t;
+    a.dr.seed = c.seed;
+    a.dr.gs = gamma_src(e, true, t);
+    a.dr.gt = gamma_src(e, false, t);
+    a.dr.ntab = e->ntab;
+    a.dr.u3 = e->du3.p + (size_t)(t % 3) * n;
+    a.dr.fail = e->fail.p;
+    a.z = fz ? row(fz, t) : nullptr;
+    a.g_s = fgs ? row(fgs, t) : nullptr;
+    a.g_t = fgt ? row(fgt, t) : nullptr;
     if (rs.resident) {
       cudaEvent_t b0, b1;
       cudaEventCreate(&b0);
@@ -1244,8 +1236,7 @@ int pf_engine_create(const pf_config* cfg, pf_engine** out) {
       (err = cudaEventCreateWithFlags(&e->ev_q[1], cudaEventDisableTiming)) || (err = e->mbuf.ensure(2)))
     return bail(err);
   if ((err = e->rec[0].ensure(n)) || (err = e->rec[1].ensure(n)) || (err = e->lw.ensure(2 * n)) ||
-      (err = e->du3.ensure(3 * n)) || (err = e->dz.ensure(3 * n)) ||
-      (err = e->dgs.ensure(3 * n)) || (err = e->dgt.ensure(3 * n)) || (err = e->partials.ensure(sm_count() * 8 + 8)) ||
+      (err = e->du3.ensure(3 * n)) || (err = e->partials.ensure(sm_count() * 8 + 8)) ||
       (err = e->sc.ensure(1)) || (err = e->fail.ensure(1)) ||
       (err = e->cdf.ensure(n, e->single ? 4 : 8)) || (err = e->probs.ensure(8)))
     return bail(err);

@@ -72,6 +72,10 @@ int run_group(pf_group* g, const double* y, int64_t T, pf_outputs* out) {
     if (want_fq) CK(e->o_fq.ensure(TT * 3));
     if (keep_idx) CK(e->idx.ensure(ns));
     if (want_fq || LS || LT) CK(e->keys.ensure((size_t)6 * ns));  // quantile keys [2][3][ns]
+    // sharded runs precompute the draws (draws_kernel, by step parity)
+    CK(e->dz.ensure(2 * ns));
+    CK(e->dgs.ensure(2 * ns));
+    CK(e->dgt.ensure(2 * ns));
     Scalars s0h;
     memset(&s0h, 0, sizeof(s0h));
     s0h.cs = (LS && c.sigma2_shape > 1.0) ? c.sigma2_scale / (c.sigma2_shape - 1.0) : 0.0;

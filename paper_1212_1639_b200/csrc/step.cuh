@@ -195,7 +195,7 @@ struct StepArgs {
   int64_t* fail;
   Partial* xrec;         // sharded run: shard partials [G] (null: single run)
   int shard;
-  DrawArgs nd;           // FD: the draws of step t+1, computed here (nd.z null: none)
+  DrawArgs dr;           // FD: this step's draws are computed here (tables, seed, u3 out)
   ShardLookup<TQ> slk;   // sharded run (slk.G > 0): cross-shard lookup
   const Rec* recs[PF_MAX_SHARDS];  // sharded run: every shard's records of step t-1
 };
@@ -375,17 +375,17 @@ PF_D void cp_async8(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src));
 }
 
-// FD: also compute the draws of step t+1 (Philox block t+1, ndtri and
-// gamma tables of t+1 staged in shared memory) for every slot, in the issue
-// slots the latency-bound gather pipeline leaves idle -- instead of a
-// separate compute-bound draws kernel.
+// FD: compute the step's draws (Philox block t, ndtri and gamma tables
+// staged in shared memory) for each batch while its record gathers are in
+// flight -- the issue slots the latency-bound gather pipeline leaves idle --
+// instead of a separate compute-bound draws kernel and a round trip of the
+// draws through HBM.
 template <int MODE, typename TQ, bool FD = false>
 __global__ void __launch_bounds__(FD ? 512 : 256) step_kernel(StepArgs<TQ> a) {
   constexpr bool LS = MODE & M_LS, LT = MODE & M_LT, SINGLE = MODE & M_SINGLE;
   if (*a.fail) return;
   int slot_s = -1, slot_t = -1, noff = -1, tab_doubles = 0;
-  const bool fd = FD && a.nd.z != nullptr;
-  if (FD) tab_doubles = stage_tables<LS, LT>(a.nd.gs, a.nd.gt, a.nd.ntab, slot_s, slot_t, noff);
+  if (FD) tab_doubles = stage_tables<LS, LT>(a.dr.gs, a.dr.gt, a.dr.ntab, slot_s, slot_t, noff);
   const bool feedw = a.feed_w != nullptr;
   const double cs = a.sc->cs, ct = a.sc->ct, cx = a.sc->cx;
   double m = feedw ? 0.0 : -INFINITY;
@@ -458,17 +458,38 @@ __global__ void __launch_bounds__(FD ? 512 : 256) step_kernel(StepArgs<TQ> a) {
       const char* src = reinterpret_cast<const char*>(rp);
       cp_async16(dst, src);
       cp_async16(dst + 16, src + 16);
-      cp_async8((uint32_t)__cvta_generic_to_shared(val_at(buf, 0, b)), a.z + jj[b]);
-      if (LS) cp_async8((uint32_t)__cvta_generic_to_shared(val_at(buf, 1, b)), a.g_s + jj[b]);
-      if (LT) cp_async8((uint32_t)__cvta_generic_to_shared(val_at(buf, 2, b)), a.g_t + jj[b]);
+      // precomputed draws (draws kernel) or the oracle feed
+      if (a.z) cp_async8((uint32_t)__cvta_generic_to_shared(val_at(buf, 0, b)), a.z + jj[b]);
+      if (LS && a.g_s) cp_async8((uint32_t)__cvta_generic_to_shared(val_at(buf, 1, b)), a.g_s + jj[b]);
+      if (LT && a.g_t) cp_async8((uint32_t)__cvta_generic_to_shared(val_at(buf, 2, b)), a.g_t + jj[b]);
     }
     asm volatile("cp.async.commit_group;");
+  };
+  // FD: a batch's draws (Philox block t, filtering.py:273,280,286) go straight
+  // to its stage slot; computed after the previous batch's arithmetic, while
+  // this batch's record gathers are in flight.  The resampling word goes to
+  // global memory for the next step's lookups.
+  auto draws_for = [&](int64_t bi, int buf) {
+#pragma unroll 1
+    for (int b = 0; b < STEP_SB; ++b) {
+      const int64_t j = bi * batch + b * (int64_t)nth + threadIdx.x;
+      if (bi >= nbatches || j >= a.n) continue;
+      const Philox4 P = philox_block(a.dr.seed, (uint64_t)(a.dr.gbase + j), (uint64_t)a.t);
+      a.dr.u3[j] = P.w[3];
+      if (!a.z) {
+        const double u0 = unit_open(P.w[0]);
+        *val_at(buf, 0, b) = noff >= 0 ? nt_eval_slot(noff, u0) : ndtri(u0);
+      }
+      if (LS && !a.g_s) *val_at(buf, 1, b) = gamma_draw_slot(a.dr.gs, slot_s, unit_open(P.w[1]));
+      if (LT && !a.g_t) *val_at(buf, 2, b) = gamma_draw_slot(a.dr.gt, slot_t, unit_open(P.w[2]));
+    }
   };
   int cur = 0;
   int64_t bi = blockIdx.x;
   uint64_t w3n[STEP_SB];
   load_w3(bi, w3n);
   if (bi < nbatches) issue(bi, 0, w3n);
+  if (FD) draws_for(bi, 0);
   load_w3(bi + gridDim.x, w3n);
   for (; bi < nbatches; bi += gridDim.x) {
     if (bi + gridDim.x < nbatches) {
@@ -542,16 +563,8 @@ __global__ void __launch_bounds__(FD ? 512 : 256) step_kernel(StepArgs<TQ> a) {
     s2s = fma(eds, ds, s2s);
     s1t += edt;
     s2t = fma(edt, dt, s2t);
-    if (fd) {
-      // next step's draws for this slot (filtering.py:273,280,286 at t+1)
-      const Philox4 P = philox_block(a.nd.seed, (uint64_t)(a.nd.gbase + j), (uint64_t)(a.t + 1));
-      a.nd.u3[j] = P.w[3];
-      const double u0 = unit_open(P.w[0]);
-      a.nd.z[j] = noff >= 0 ? nt_eval_slot(noff, u0) : ndtri(u0);
-      if (LS) a.nd.g_s[j] = gamma_draw_slot(a.nd.gs, slot_s, unit_open(P.w[1]));
-      if (LT) a.nd.g_t[j] = gamma_draw_slot(a.nd.gt, slot_t, unit_open(P.w[2]));
-    }
   }
+    if (FD) draws_for(bi + gridDim.x, cur ^ 1);
     cur ^= 1;
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
