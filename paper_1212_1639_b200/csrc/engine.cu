@@ -789,12 +789,6 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     a.u3 = e->du3.p + (size_t)((t - 1) % 3) * n;
     a.lk = lk;
     a.idx_out = (keep_idx && t > 1) ? e->idx.p : nullptr;
-    {
-      const size_t off = (size_t)(t % 3) * n;
-      a.z = fz ? row(fz, t) : e->dz.p + off;
-      a.g_s = fgs ? row(fgs, t) : e->dgs.p + off;
-      a.g_t = fgt ? row(fgt, t) : e->dgt.p + off;
-    }
     a.feed_w = row(fw, t);
     // the side stream's step t-2 work reads the buffers this step overwrites
     if (ntg && t > 2) CK(cudaStreamWaitEvent(st, e->ev_q[t & 1], 0));
