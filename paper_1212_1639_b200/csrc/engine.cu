@@ -678,11 +678,25 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   const bool share_tab = LS && LT && e->tab_s == e->tab_t && c.gamma_method == 0;
   const int ngt = c.gamma_method == 0 ? (LS ? 1 : 0) + (LT && !share_tab ? 1 : 0) : 0;
   const size_t draw_smem = ((size_t)ngt * GT_TABLE_DOUBLES + (e->ntab ? NT_TABLE_DOUBLES : 0)) * sizeof(double);
-  // The step kernel computes the next step's draws itself (FD): 512 threads,
-  // shared memory = the step's tables + the double-buffered gather stage.
-  constexpr int STEP_THREADS = 512;
-  const size_t step_smem = (size_t)(((draw_smem / 8) + 3) & ~size_t(3)) * 8 +
+  // Large N: the step kernel computes its own draws (FD: 512 threads; shared
+  // memory = the step's tables + the double-buffered gather stage).  Small
+  // N: a separate draws_kernel on its own stream runs one step ahead, beside
+  // the step kernel and the CDF (a short step kernel cannot hide the draws'
+  // arithmetic).  PF_FUSED_DRAWS=0/1 overrides.
+  static const int fused_env = [] {
+    const char* v = getenv("PF_FUSED_DRAWS");
+    return v ? atoi(v) : -1;
+  }();
+  const bool fused = c.gamma_method == 0 && e->ntab &&
+                     (fused_env >= 0 ? fused_env != 0 : n >= ((int64_t)1 << 22));
+  const int STEP_THREADS = fused ? 512 : 256;
+  const size_t step_smem = (fused ? (size_t)(((draw_smem / 8) + 3) & ~size_t(3)) * 8 : 0) +
                            (size_t)2 * STEP_SB * STEP_THREADS * (sizeof(Rec) + 3 * sizeof(double));
+  if (!fused) {
+    CK(e->dz.ensure(3 * (size_t)n));
+    CK(e->dgs.ensure(3 * (size_t)n));
+    CK(e->dgt.ensure(3 * (size_t)n));
+  }
   {
     static bool attr[8] = {false};
     if (!attr[MODE]) {
@@ -690,12 +704,17 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
                               (int)((2 * GT_TABLE_DOUBLES + NT_TABLE_DOUBLES) * sizeof(double))));
       CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)((2 * GT_TABLE_DOUBLES + NT_TABLE_DOUBLES + 4) * sizeof(double) +
-                                    2 * STEP_SB * STEP_THREADS * (sizeof(Rec) + 3 * sizeof(double)))));
+                                    2 * STEP_SB * 512 * (sizeof(Rec) + 3 * sizeof(double)))));
+      CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(2 * STEP_SB * 256 * (sizeof(Rec) + 3 * sizeof(double)))));
       attr[MODE] = true;
     }
   }
   int occ = 0, docc = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, step_kernel<MODE, TQ, true>, STEP_THREADS, step_smem));
+  if (fused)
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, step_kernel<MODE, TQ, true>, STEP_THREADS, step_smem));
+  else
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, step_kernel<MODE, TQ, false>, STEP_THREADS, step_smem));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&docc, draws_kernel<MODE>, 256, draw_smem));
   if (occ < 1) occ = 1;
   if (docc < 1) docc = 1;
@@ -721,7 +740,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     draws_kernel<MODE><<<draw_grid, 256, draw_smem, s_>>>(d);
     LAUNCHED();
   };
-  (void)launch_draws;  // the step kernel computes its own draws (sharded runs use draws_kernel)
+  if (!fused && T >= 1) launch_draws(1, st);
 
   int cur = 0;
   WSrc wsrc;
@@ -820,20 +839,38 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     a.z = fz ? row(fz, t) : nullptr;
     a.g_s = fgs ? row(fgs, t) : nullptr;
     a.g_t = fgt ? row(fgt, t) : nullptr;
+    if (!fused) {  // draws_kernel output of step t
+      const size_t off = (size_t)(t % 3) * n;
+      if (!a.z) a.z = e->dz.p + off;
+      if (!a.g_s) a.g_s = e->dgs.p + off;
+      if (!a.g_t) a.g_t = e->dgt.p + off;
+      if (t > 1) CK(cudaStreamWaitEvent(st, e->ev_draw, 0));
+    }
     if (rs.resident) {
       cudaEvent_t b0, b1;
       cudaEventCreate(&b0);
       cudaEventCreate(&b1);
       cudaEventRecord(b0, st);
-      step_kernel<MODE, TQ, true><<<step_grid, STEP_THREADS, step_smem, st>>>(a);
+      if (fused) step_kernel<MODE, TQ, true><<<step_grid, STEP_THREADS, step_smem, st>>>(a);
+      else step_kernel<MODE, TQ, false><<<step_grid, STEP_THREADS, step_smem, st>>>(a);
       cudaEventRecord(b1, st);
       step_evs.push_back({b0, b1});
     } else {
-      step_kernel<MODE, TQ, true><<<step_grid, STEP_THREADS, step_smem, st>>>(a);
+      if (fused) step_kernel<MODE, TQ, true><<<step_grid, STEP_THREADS, step_smem, st>>>(a);
+      else step_kernel<MODE, TQ, false><<<step_grid, STEP_THREADS, step_smem, st>>>(a);
     }
     LAUNCHED();
     ++step_launches;
     cur ^= 1;
+    if (!fused) {
+      CK(cudaEventRecord(e->ev_steps[t % 3], st));
+      if (t < T) {
+        // draws(t+1) reuse the buffers of step t-2, last read by step t-1
+        if (t >= 2) CK(cudaStreamWaitEvent(e->dstream, e->ev_steps[(t - 1) % 3], 0));
+        launch_draws(t + 1, e->dstream);
+        CK(cudaEventRecord(e->ev_draw, e->dstream));
+      }
+    }
     mark(PH_PROP);
     if (keep_idx && t > 1)
       CK(cudaMemcpyAsync(out->indices + (size_t)(t - 2) * n, e->idx.p, n * sizeof(int64_t),

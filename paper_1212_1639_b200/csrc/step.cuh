@@ -62,6 +62,16 @@ extern __shared__ double pf_gtab[];
 // 16 double-wide bank pairs instead of the 4 a 12-double segment stride
 // leaves (4x fewer shared-memory wavefronts).  Same coefficients and Horner
 // order as gt_eval on the global [seg][k] table, so the values are identical.
+PF_D double gamma_table_slot(int slot, double u) {
+  double t;
+  const int seg = gt_segment(u, &t);
+  const double* c = pf_gtab + slot * GT_TABLE_DOUBLES + seg;
+  double r = c[GT_DEG * GT_NSEG];
+#pragma unroll
+  for (int k = GT_DEG - 1; k >= 0; --k) r = fma(r, t, c[k * GT_NSEG]);
+  return r;
+}
+
 PF_D double gamma_draw_slot(const GammaSrc& g, int slot, double u) {
   if (slot < 0) return gamma_draw(g, u);
   double t;
@@ -476,12 +486,11 @@ __global__ void __launch_bounds__(FD ? 512 : 256) step_kernel(StepArgs<TQ> a) {
       if (bi >= nbatches || j >= a.n) continue;
       const Philox4 P = philox_block(a.dr.seed, (uint64_t)(a.dr.gbase + j), (uint64_t)a.t);
       a.dr.u3[j] = P.w[3];
-      if (!a.z) {
-        const double u0 = unit_open(P.w[0]);
-        *val_at(buf, 0, b) = noff >= 0 ? nt_eval_slot(noff, u0) : ndtri(u0);
-      }
-      if (LS && !a.g_s) *val_at(buf, 1, b) = gamma_draw_slot(a.dr.gs, slot_s, unit_open(P.w[1]));
-      if (LT && !a.g_t) *val_at(buf, 2, b) = gamma_draw_slot(a.dr.gt, slot_t, unit_open(P.w[2]));
+      // tables only (FD runs with gamma_method 0): no call into the
+      // accurate solvers, which would cost the kernel a stack frame
+      if (!a.z) *val_at(buf, 0, b) = nt_eval_slot(noff, unit_open(P.w[0]));
+      if (LS && !a.g_s) *val_at(buf, 1, b) = gamma_table_slot(slot_s, unit_open(P.w[1]));
+      if (LT && !a.g_t) *val_at(buf, 2, b) = gamma_table_slot(slot_t, unit_open(P.w[2]));
     }
   };
   int cur = 0;
