@@ -17,14 +17,14 @@ far larger than the 126 MB L2, so no explicit flush is needed.
            scipy, all host threads as Backend lanes) on a bounded sample.
 
 Multi-GPU (--gpus N under torchrun, N > 1): ONE filter of --n-shard (default
-2^27, BASELINE configs[3]) particles sharded over the N GPUs (pf_group_*:
-per-step exchange of one partial record and one subtree total per shard over
-NVLink P2P, cross-shard resampling reads).  Rank 0's process drives the N
-shards (one CUDA stream per GPU); the other ranks hold the barrier and
-report zero time, so the max over ranks is rank 0's device time.  Total work
-is fixed as N grows: scaling "strong".  --multi replicas instead runs an
+2^27, BASELINE configs[3]) particles sharded over the N GPUs, one process per
+GPU (distributed.py / pf_shard_*): per step an NCCL all-gather of one partial
+record and one subtree total per rank plus one barrier, all enqueued on the
+engine's stream, and cross-rank resampling reads through CUDA IPC (NVLink
+P2P).  value = N*T*K / max over ranks of the device time.  Total work is
+fixed as N grows: scaling "strong".  --multi replicas instead runs an
 independent N-particle filter per rank (weak scaling).  --shards G runs G
-shards on one GPU (the sharded code path, for checking it on one device).
+shards on one GPU from one process (pf_group_*, the same sharded kernels).
 """
 
 from __future__ import annotations
@@ -295,64 +295,65 @@ def main():
 
 
 def run_sharded(args, world, rank, local):
-    """One filter sharded over G shards: G = world GPUs (torchrun; rank 0
-    drives all of them) or --shards G on one GPU."""
-    import numpy as np
-
+    """One filter sharded over G shards: G = world GPUs, one process each
+    (torchrun; Backend(process_group=...)), or --shards G on one GPU from
+    one process (pf_group_*)."""
     import paper_1212_1639_b200 as P
     from paper_1212_1639_b200 import _lib
 
     G = world if world > 1 else args.shards
     n = args.n_shard if world > 1 else args.n
     t_len = args.t
-    devices = list(range(G)) if world > 1 else [local] * G
     _, y = P.simulate(P.TrendNoiseModel(), t_len, P.RngStream(0, P.rng.AUX_STREAM_BASE + 1))
-    tot_ms = 0.0
-    e2e_s = 0.0
-    launches = 0
-    clk_summary = None
-    if rank == 0:
-        lib = _lib.require_device()
-        backend = P.Backend("cuda", shards=G, devices=devices)
-        P.run_particle_learning(P.Priors(), y, n, seed=0, backend=backend, track_quantiles=False)
-        eng = next(iter(backend._engines.values()))
-        for _ in range(args.warmup):
-            P.run_particle_learning(P.Priors(), y, n, seed=0, backend=backend, track_quantiles=False)
+    lib = _lib.require_device()
+    if world > 1:
+        backend = P.Backend("cuda", device=local, process_group=True)
+        where = f"one process per GPU, {G} ranks (NCCL exchange, CUDA IPC peer reads)"
+    else:
+        backend = P.Backend("cuda", shards=G, devices=[local] * G)
+        where = f"{G} shards on GPU {local} (one process)"
+
+    def once():
+        return P.run_particle_learning(P.Priors(), y, n, seed=0, backend=backend, track_quantiles=False)
+
+    once()
+    eng = next(iter(backend._engines.values()))
+    for _ in range(args.warmup):
+        once()
     barrier(world)
-    if rank == 0:
-        k0 = lib.pf_launch_count()
-        with ClockSampler(local) as clk:
-            t0 = time.perf_counter()
-            for _ in range(args.steps):
-                out = P.run_particle_learning(P.Priors(), y, n, seed=0, backend=backend,
-                                              track_quantiles=False)
-                tot_ms += eng.last_timing()["total_ms"]
-                _ = out.param_posterior["sigma2"].mean[-1]
-            e2e_s = time.perf_counter() - t0
-        launches = lib.pf_launch_count() - k0
-        clk_summary = clk.summary()
-        backend.close()
+    tot_ms = 0.0
+    k0 = lib.pf_launch_count()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            out = once()
+            tot_ms += eng.last_timing()["total_ms"]
+            _ = out.param_posterior["sigma2"].mean[-1]
+        e2e_s = time.perf_counter() - t0
+    launches = lib.pf_launch_count() - k0
+    clk_summary = clk.summary()
+    backend.close()
     barrier(world)
     tot_ms = max_over_ranks(tot_ms, world)
     e2e_s = max_over_ranks(e2e_s, world)
+    launches = int(max_over_ranks(float(launches), world))
     if rank == 0:
         peak, peak_kind = _peaks()
-        value = n * t_len * args.steps / (tot_ms / 1e3)
+        per_gpu = ALG_BYTES_CYCLE * n * t_len / (tot_ms / args.steps / 1e3) / 1e9 / G
         line = {
             "metric": "particle-steps/sec (N*T/s), full particle-learning cycle",
-            "value": value, "unit": "particle-steps/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "value": n * t_len * args.steps / (tot_ms / 1e3), "unit": "particle-steps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
             "config": {"workload": f"PL trend+noise, Priors(), cutpoint, N=2^{n.bit_length() - 1} sharded "
                                    f"over {G} shards, T={t_len}, seed 0, track_quantiles=False",
-                       "N": n, "T": t_len, "parallelism": f"particle shards x{G} on devices {devices}",
+                       "N": n, "T": t_len, "parallelism": where,
                        "l2": "working set >> L2 (no flush needed)"},
             "e2e": {"value": n * t_len * args.steps / e2e_s, "unit": "particle-steps/s",
                     "h2d_bytes_per_step": 8 * t_len, "d2h_bytes_per_step": 8 * t_len * 15},
-            "roofline": {"bound": "hbm", "kernel": "whole cycle", "achieved":
-                         ALG_BYTES_CYCLE * n * t_len / (tot_ms / args.steps / 1e3) / 1e9 / G,
-                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s per GPU",
-                         "frac": ALG_BYTES_CYCLE * n * t_len / (tot_ms / args.steps / 1e3) / 1e9 / G / peak,
+            "roofline": {"bound": "hbm", "kernel": "whole cycle", "achieved": per_gpu, "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s per GPU", "frac": per_gpu / peak,
                          "traffic": None, "alg_bytes_per_particle": ALG_BYTES_CYCLE},
             "cpu_baseline": None,
             "gpu_launches": launches,

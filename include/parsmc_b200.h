@@ -166,6 +166,46 @@ int pf_group_run(pf_group* g, const double* y, int64_t t_len, pf_outputs* out);
 int pf_group_last_timing(pf_group* g, double* total_ms);
 int pf_group_destroy(pf_group* g);
 
+/* ------------------------- sharded run, one process per GPU (torchrun) --- */
+/* The same sharded filter with one OS process per GPU: rank r of world
+ * (1, 2, 4, 8) owns slots [r N/world, (r+1) N/world) on cfg->device.  The
+ * caller owns the process group and drives, per step t = 1..T:
+ *   pf_shard_phase(s, 1, t)   ancestors + step kernel -> partial record
+ *   all-gather PF_XCHG_PARTIAL (in place, one slot per rank)
+ *   pf_shard_phase(s, 2, t)   combine + local tree reduce -> subtree total
+ *   all-gather PF_XCHG_TOTAL
+ *   pf_shard_phase(s, 3, t)   top tree, cut table / q, quantile classification
+ *   barrier (any collective)
+ *   pf_shard_phase(s, 4, t)   rank 0: exact weighted-quantile resolve
+ * then pf_shard_finish.  The collectives may run on pf_shard_stream (NCCL:
+ * no host sync) or through host memory (pf_shard_exchange_host, gloo).
+ * Data-dependent peer reads go through CUDA IPC: every rank exports
+ * pf_shard_ipc_handle_bytes() of handles and opens all ranks' handles
+ * (rank-major) once, after create.  Results are bit-identical to
+ * pf_engine_run; rank 0's pf_outputs receive the summaries, every rank its
+ * own slots of indices (T x N/world) and final particles.  Replaces the same
+ * _run_loop (filtering.py:200-374) as pf_group_run. */
+typedef struct pf_shard pf_shard;
+enum { PF_XCHG_PARTIAL = 0, PF_XCHG_TOTAL = 1 };
+int pf_shard_create(const pf_config* cfg, int32_t rank, int32_t world, pf_shard** out);
+/* Same n, precision, device and tracked outputs (seed, priors may change). */
+int pf_shard_reconfigure(pf_shard* s, const pf_config* cfg);
+int32_t pf_shard_ipc_handle_bytes(void);
+int pf_shard_ipc_handles(pf_shard* s, void* handles);
+int pf_shard_open_peers(pf_shard* s, const void* all_handles);
+/* Device pointer of an exchange array (world slots) and its slot size. */
+int pf_shard_exchange(pf_shard* s, int32_t which, void** dptr, int64_t* slot_bytes);
+/* to_host != 0: synchronise and copy this rank's slot to host; else copy
+ * all world slots from host to the device array. */
+int pf_shard_exchange_host(pf_shard* s, int32_t which, int32_t to_host, void* host);
+int pf_shard_stream(pf_shard* s, void** stream);
+int pf_shard_synchronize(pf_shard* s);
+int pf_shard_begin(pf_shard* s, const double* y, int64_t t_len, pf_outputs* out);
+int pf_shard_phase(pf_shard* s, int32_t phase, int64_t t);
+int pf_shard_finish(pf_shard* s);
+int pf_shard_last_timing(pf_shard* s, double* total_ms);
+int pf_shard_destroy(pf_shard* s);
+
 /* ------------------------------------------------- kernel level (L2) --- */
 /* All kernel-level entries take HOST pointers and run synchronously on the
  * current device; they exist for parity tests and for the reference's

@@ -95,6 +95,20 @@ SIGNATURES = {
     "pf_group_run": (C.c_int, [C.c_void_p, _dp, C.c_int64, C.POINTER(PfOutputs)]),
     "pf_group_last_timing": (C.c_int, [C.c_void_p, _dp]),
     "pf_group_destroy": (C.c_int, [C.c_void_p]),
+    "pf_shard_create": (C.c_int, [C.POINTER(PfConfig), C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    "pf_shard_reconfigure": (C.c_int, [C.c_void_p, C.POINTER(PfConfig)]),
+    "pf_shard_ipc_handle_bytes": (C.c_int32, []),
+    "pf_shard_ipc_handles": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "pf_shard_open_peers": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "pf_shard_exchange": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p), _i64p]),
+    "pf_shard_exchange_host": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    "pf_shard_stream": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "pf_shard_synchronize": (C.c_int, [C.c_void_p]),
+    "pf_shard_begin": (C.c_int, [C.c_void_p, _dp, C.c_int64, C.POINTER(PfOutputs)]),
+    "pf_shard_phase": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64]),
+    "pf_shard_finish": (C.c_int, [C.c_void_p]),
+    "pf_shard_last_timing": (C.c_int, [C.c_void_p, _dp]),
+    "pf_shard_destroy": (C.c_int, [C.c_void_p]),
     "pf_philox_block": (C.c_int, [C.c_uint64, _u64p, C.c_int64, C.c_uint64, _u64p]),
     "pf_philox4x64": (C.c_int, [_u64p, _u64p, C.c_int64, _u64p]),
     "pf_uniforms_at": (C.c_int, [C.c_uint64, _u64p, _u64p, C.c_int64, _dp]),

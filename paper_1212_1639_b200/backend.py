@@ -37,9 +37,15 @@ class Backend:
     devices : sequence of int, optional
         Device of each shard (default: all on ``device``); distinct devices
         must have peer access (NVLink / NVSwitch).
+    process_group : torch.distributed group or True, optional
+        One process per GPU: every rank of the group calls the same function
+        with the same arguments (SPMD) and owns ``n / world`` consecutive
+        particle slots on ``device``; all ranks return the full outputs
+        (``distributed.py``).  ``True`` means the default group.
     """
 
-    def __init__(self, mode="cuda", lanes=1, min_chunk=4096, device=0, shards=1, devices=None):
+    def __init__(self, mode="cuda", lanes=1, min_chunk=4096, device=0, shards=1, devices=None,
+                 process_group=None):
         if mode not in MODES:
             raise ValueError(f"unknown backend mode: {mode!r}")
         if lanes < 1:
@@ -57,6 +63,18 @@ class Backend:
         self.device = int(device)
         self.shards = shards
         self.devices = devices if devices is not None else [self.device] * shards
+        self.process_group = None
+        if process_group is not None and process_group is not False:
+            if shards != 1 or devices is not None:
+                raise ValueError("process_group and shards/devices are exclusive")
+            import torch.distributed as dist
+
+            if not dist.is_initialized():
+                raise ValueError("process_group needs an initialised torch.distributed process group")
+            self.process_group = None if process_group is True else process_group
+            self.world = dist.get_world_size(self.process_group)
+            self.rank = dist.get_rank(self.process_group)
+        self.distributed = process_group is not None and process_group is not False
         self._engines = {}
 
     def split(self, n):
@@ -98,8 +116,9 @@ class Backend:
             pass
 
     def __repr__(self):
+        tail = f", rank={self.rank}/{self.world}" if self.distributed else ""
         return (f"Backend(mode={self.mode!r}, lanes={self.lanes}, device={self.device}, "
-                f"shards={self.shards})")
+                f"shards={self.shards}{tail})")
 
 
 def device_available():

@@ -1206,6 +1206,7 @@ RunFn pick_run(int mode) {
 }  // namespace
 
 #include "group.cuh"
+#include "dist.cuh"
 
 // ================================================================ C ABI ===
 extern "C" {
@@ -1498,6 +1499,250 @@ int pf_group_destroy(pf_group* g) {
   if (g->xtot) cudaFree(g->xtot);
   if (g->evM) cudaEventDestroy(g->evM);
   delete g;
+  return PF_OK;
+}
+
+// --------------------------------------- sharded run, one process per GPU ---
+int pf_shard_destroy(pf_shard* s);
+
+int pf_shard_create(const pf_config* cfg, int32_t rank, int32_t world, pf_shard** out) {
+  if (!cfg || !out) return set_err(PF_ERR_VALUE, "null argument");
+  *out = nullptr;
+  const int64_t n = cfg->n;
+  if (n < 1) return set_err(PF_ERR_VALUE, "particle count must be >= 1");
+  if (!is_pow2(n)) return set_err(PF_ERR_NOT_POWER_OF_TWO, "particle count must be a power of two, got " + std::to_string(n));
+  if (world < 1 || world > PF_MAX_SHARDS || !is_pow2(world)) return set_err(PF_ERR_VALUE, "world size must be 1, 2, 4 or 8");
+  if (rank < 0 || rank >= world) return set_err(PF_ERR_VALUE, "rank out of range");
+  if (n / world < 4096) return set_err(PF_ERR_VALUE, "sharded runs need at least 4096 particles per shard");
+  if (cfg->resampler != PF_RESAMPLE_CUTPOINT)
+    return set_err(PF_ERR_NOT_IMPLEMENTED, "sharded runs use the cut-point resampler");
+  if (n > ((int64_t)1 << 31)) return set_err(PF_ERR_VALUE, "particle count above 2^31");
+  if (pf_device_count() < 1) return set_err(PF_ERR_CUDA, "no CUDA device visible");
+  pf_shard* s = new pf_shard();
+  s->cfg = *cfg;
+  s->rank = rank;
+  s->world = world;
+  s->ns = n / world;
+  s->lg = ilog2(s->ns);
+  pf_config cs = *cfg;
+  cs.n = s->ns;
+  int rc = pf_engine_create(&cs, &s->e);
+  if (rc != PF_OK) {
+    delete s;
+    return rc;
+  }
+  pf_engine* e = s->e;
+  CK(cudaSetDevice(cfg->device));
+  const size_t esz = cfg->precision == PF_DTYPE_F32 ? 4 : 8;
+  cudaError_t err;
+  auto fail_alloc = [&](cudaError_t er) {
+    pf_shard_destroy(s);
+    return set_err(er == cudaErrorMemoryAllocation ? PF_ERR_OUT_OF_MEMORY : PF_ERR_CUDA,
+                   std::string("shard allocation: ") + cudaGetErrorString(er));
+  };
+  if ((err = cudaMalloc((void**)&s->gcut, (size_t)(n + 1) * sizeof(int32_t))) ||
+      (err = cudaMalloc(&s->gq, (size_t)s->ns * esz)) ||
+      (err = cudaMalloc((void**)&s->lend, PF_MAX_SHARDS * sizeof(int64_t))) ||
+      (err = cudaMalloc((void**)&s->xrec, PF_MAX_SHARDS * sizeof(Partial))) ||
+      (err = cudaMalloc(&s->xtot, PF_MAX_SHARDS * sizeof(double))) || (err = e->keys.ensure((size_t)6 * s->ns)))
+    return fail_alloc(err);
+  const bool LS = cfg->learn && cfg->learn_sigma2, LT = cfg->learn && cfg->learn_tau2;
+  const int ntg = (cfg->track_quantiles ? 3 : 0) + (LS ? 5 : 0) + (LT ? 5 : 0);
+  if (rank == 0 && ntg) {
+    const uint32_t qcap = (uint32_t)std::max<int64_t>(4096, n / 4);
+    const int cls_grid = (int)std::min<int64_t>(cdf_plan(s->ns).tiles, (int64_t)sm_count() * 2);
+    const int fb_grid = grid_for(s->ns, 256, sm_count() * 2);
+    const size_t parts = (size_t)std::max<int64_t>((int64_t)world * std::max(cls_grid, fb_grid), sm_count() * 8);
+    if ((err = e->qtg.ensure(Q_MAXT)) || (err = e->qsh.ensure(2)) || (err = e->qcand.ensure((size_t)ntg * qcap)) ||
+        (err = e->qscratch.ensure((size_t)ntg * qcap)) || (err = e->qpart.ensure(parts * (Q_SLOTS + 1))) ||
+        (err = e->qhist.ensure((size_t)Q_MAXT * Q_SUB)) || (err = e->qfhist.ensure((size_t)Q_MAXT * Q_FB)) ||
+        (err = e->qunres.ensure(4)) || (err = e->qlidx.ensure((size_t)Q_MAXT * Q_LIST)) ||
+        (err = e->qlw.ensure((size_t)Q_MAXT * Q_LIST)))
+      return fail_alloc(err);
+  }
+  CK(e->rec[0].ensure(s->ns));
+  CK(e->rec[1].ensure(s->ns));
+  CK(e->lw.ensure(2 * s->ns));
+  CK(e->mbuf.ensure(2));
+  s->p_cut.assign(world, nullptr);
+  s->p_q.assign(world, nullptr);
+  s->p_rec[0].assign(world, nullptr);
+  s->p_rec[1].assign(world, nullptr);
+  s->p_keys.assign(world, nullptr);
+  s->p_lw.assign(world, nullptr);
+  s->p_mbuf.assign(world, nullptr);
+  *out = s;
+  return PF_OK;
+}
+
+// The buffers other ranks read, in handle order (XH_*); null where absent.
+static void shard_exports(pf_shard* s, void* ptrs[XH_COUNT]) {
+  pf_engine* e = s->e;
+  void* p[XH_COUNT] = {e->rec[0].p, e->rec[1].p, s->gcut, s->gq, e->keys.p, e->lw.p, e->mbuf.p,
+                       e->qtg.p, e->qsh.p, e->qcand.p, e->qpart.p, e->qhist.p, e->qfhist.p, e->qunres.p};
+  for (int k = 0; k < XH_COUNT; ++k) ptrs[k] = p[k];
+}
+
+int32_t pf_shard_ipc_handle_bytes(void) { return (int32_t)(XH_COUNT * sizeof(cudaIpcMemHandle_t)); }
+
+int pf_shard_ipc_handles(pf_shard* s, void* handles) {
+  if (!s || !handles) return set_err(PF_ERR_VALUE, "null argument");
+  CK(cudaSetDevice(s->cfg.device));
+  void* p[XH_COUNT];
+  shard_exports(s, p);
+  auto* h = reinterpret_cast<cudaIpcMemHandle_t*>(handles);
+  for (int k = 0; k < XH_COUNT; ++k) {
+    memset(&h[k], 0, sizeof(cudaIpcMemHandle_t));
+    if (p[k]) CK(cudaIpcGetMemHandle(&h[k], p[k]));
+  }
+  return PF_OK;
+}
+
+int pf_shard_open_peers(pf_shard* s, const void* all_handles) {
+  if (!s || !all_handles) return set_err(PF_ERR_VALUE, "null argument");
+  CK(cudaSetDevice(s->cfg.device));
+  const auto* h = reinterpret_cast<const cudaIpcMemHandle_t*>(all_handles);
+  static const cudaIpcMemHandle_t zero = {};
+  for (int r = 0; r < s->world; ++r) {
+    void* p[XH_COUNT];
+    if (r == s->rank) {
+      shard_exports(s, p);
+    } else {
+      for (int k = 0; k < XH_COUNT; ++k) {
+        p[k] = nullptr;
+        const cudaIpcMemHandle_t& hk = h[(size_t)r * XH_COUNT + k];
+        if (!memcmp(&hk, &zero, sizeof(zero))) continue;
+        // only rank 0's quantile state is read remotely
+        if (k >= XH_QTG && r != 0) continue;
+        CK(cudaIpcOpenMemHandle(&p[k], hk, cudaIpcMemLazyEnablePeerAccess));
+        s->opened.push_back(p[k]);
+      }
+    }
+    s->p_rec[0][r] = (const Rec*)p[XH_REC0];
+    s->p_rec[1][r] = (const Rec*)p[XH_REC1];
+    s->p_cut[r] = (const int32_t*)p[XH_CUT];
+    s->p_q[r] = p[XH_Q];
+    s->p_keys[r] = (const uint32_t*)p[XH_KEYS];
+    s->p_lw[r] = (const double*)p[XH_LW];
+    s->p_mbuf[r] = (const double*)p[XH_MBUF];
+    if (r == 0) {
+      s->q_tg = (QTarget*)p[XH_QTG];
+      s->q_sh = (QShared*)p[XH_QSH];
+      s->q_cand = (QCand*)p[XH_QCAND];
+      s->q_part = (double*)p[XH_QPART];
+      s->q_hist = (unsigned long long*)p[XH_QHIST];
+      s->q_fhist = (unsigned long long*)p[XH_QFHIST];
+      s->q_unres = (unsigned int*)p[XH_QUNRES];
+    }
+  }
+  for (int r = 0; r < s->world; ++r)
+    if (!s->p_rec[0][r] || !s->p_rec[1][r] || !s->p_cut[r] || !s->p_q[r] || !s->p_keys[r] || !s->p_lw[r] ||
+        !s->p_mbuf[r])
+      return set_err(PF_ERR_VALUE, "missing peer buffer handle (rank " + std::to_string(r) + ")");
+  return PF_OK;
+}
+
+int pf_shard_exchange(pf_shard* s, int32_t which, void** dptr, int64_t* slot_bytes) {
+  if (!s) return set_err(PF_ERR_VALUE, "null shard");
+  if (which == PF_XCHG_PARTIAL) {
+    if (dptr) *dptr = s->xrec;
+    if (slot_bytes) *slot_bytes = (int64_t)sizeof(Partial);
+  } else if (which == PF_XCHG_TOTAL) {
+    if (dptr) *dptr = s->xtot;
+    if (slot_bytes) *slot_bytes = s->cfg.precision == PF_DTYPE_F32 ? 4 : 8;
+  } else {
+    return set_err(PF_ERR_VALUE, "exchange id");
+  }
+  return PF_OK;
+}
+
+int pf_shard_stream(pf_shard* s, void** stream) {
+  if (!s || !stream) return set_err(PF_ERR_VALUE, "null argument");
+  *stream = (void*)s->e->st;
+  return PF_OK;
+}
+
+int pf_shard_exchange_host(pf_shard* s, int32_t which, int32_t to_host, void* host) {
+  if (!s || !host) return set_err(PF_ERR_VALUE, "null argument");
+  void* d = nullptr;
+  int64_t sb = 0;
+  int rc = pf_shard_exchange(s, which, &d, &sb);
+  if (rc != PF_OK) return rc;
+  CK(cudaSetDevice(s->cfg.device));
+  if (to_host) {
+    CK(cudaMemcpyAsync(host, (char*)d + (size_t)s->rank * sb, sb, cudaMemcpyDeviceToHost, s->e->st));
+  } else {
+    CK(cudaMemcpyAsync(d, host, (size_t)s->world * sb, cudaMemcpyHostToDevice, s->e->st));
+  }
+  CK(cudaStreamSynchronize(s->e->st));
+  return PF_OK;
+}
+
+int pf_shard_synchronize(pf_shard* s) {
+  if (!s) return set_err(PF_ERR_VALUE, "null shard");
+  CK(cudaSetDevice(s->cfg.device));
+  CK(cudaStreamSynchronize(s->e->st));
+  return PF_OK;
+}
+
+int pf_shard_begin(pf_shard* s, const double* y, int64_t t_len, pf_outputs* out) {
+  if (!s) return set_err(PF_ERR_VALUE, "null shard");
+  if (t_len < 0) return set_err(PF_ERR_VALUE, "negative series length");
+  for (int64_t i = 0; i < t_len; ++i)
+    if (!std::isfinite(y[i])) return set_err(PF_ERR_NON_FINITE_WEIGHT, "observations contain NaN or infinity");
+  if (out && out->hist_states)
+    return set_err(PF_ERR_NOT_IMPLEMENTED, "store_particles is not supported by sharded runs");
+  if (!s->p_cut.size() || !s->p_cut[0]) return set_err(PF_ERR_VALUE, "pf_shard_open_peers has not been called");
+  CK(cudaSetDevice(s->cfg.device));
+  return pick_shard_fns(shard_mode(s->cfg)).begin(s, y, t_len, out);
+}
+
+int pf_shard_phase(pf_shard* s, int32_t phase, int64_t t) {
+  if (!s) return set_err(PF_ERR_VALUE, "null shard");
+  if (phase < 1 || phase > 4) return set_err(PF_ERR_VALUE, "phase must be 1..4");
+  if (t < 1 || t > s->T) return set_err(PF_ERR_VALUE, "step out of range");
+  CK(cudaSetDevice(s->cfg.device));
+  return pick_shard_fns(shard_mode(s->cfg)).phase[phase - 1](s, t);
+}
+
+int pf_shard_finish(pf_shard* s) {
+  if (!s) return set_err(PF_ERR_VALUE, "null shard");
+  CK(cudaSetDevice(s->cfg.device));
+  return pick_shard_fns(shard_mode(s->cfg)).finish(s);
+}
+
+int pf_shard_reconfigure(pf_shard* s, const pf_config* cfg) {
+  if (!s || !cfg) return set_err(PF_ERR_VALUE, "null argument");
+  const pf_config& o = s->cfg;
+  if (cfg->n != o.n || cfg->precision != o.precision || cfg->device != o.device ||
+      cfg->resampler != o.resampler || cfg->track_quantiles != o.track_quantiles ||
+      (cfg->learn && cfg->learn_sigma2) != (o.learn && o.learn_sigma2) ||
+      (cfg->learn && cfg->learn_tau2) != (o.learn && o.learn_tau2))
+    return set_err(PF_ERR_VALUE, "reconfigure cannot change n, precision, device, resampler or the tracked outputs");
+  s->cfg = *cfg;
+  pf_config cs = *cfg;
+  cs.n = s->ns;
+  return pf_engine_reconfigure(s->e, &cs);
+}
+
+int pf_shard_last_timing(pf_shard* s, double* total_ms) {
+  if (!s) return set_err(PF_ERR_VALUE, "null shard");
+  if (total_ms) *total_ms = s->e->last_total_ms;
+  return PF_OK;
+}
+
+int pf_shard_destroy(pf_shard* s) {
+  if (!s) return PF_OK;
+  cudaSetDevice(s->cfg.device);
+  if (s->e && s->e->st) cudaStreamSynchronize(s->e->st);
+  for (void* p : s->opened) cudaIpcCloseMemHandle(p);
+  if (s->gcut) cudaFree(s->gcut);
+  if (s->gq) cudaFree(s->gq);
+  if (s->lend) cudaFree(s->lend);
+  if (s->xrec) cudaFree(s->xrec);
+  if (s->xtot) cudaFree(s->xtot);
+  pf_engine_destroy(s->e);
+  delete s;
   return PF_OK;
 }
 

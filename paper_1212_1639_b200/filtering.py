@@ -198,7 +198,20 @@ def _run_loop(model, priors, y, n, seed, backend, resampler, precision, store_pa
     try:
         cfg, ls, lt = _build_config(model, priors, n, seed, precision, flags, backend.device, resampler)
         shards = getattr(backend, "shards", 1)
-        if shards > 1:
+        if getattr(backend, "distributed", False):
+            if store_particles:
+                raise NotImplementedError("store_particles is not supported by sharded runs")
+            if resampler != "cutpoint":
+                raise NotImplementedError("sharded runs use the cut-point resampler")
+            if noise is not None:
+                raise NotImplementedError("oracle feeds are not supported by sharded runs")
+            key = ("rank", n, precision, backend.device, bool(track_quantiles), learn, ls, lt)
+
+            def factory():
+                from .distributed import ShardRank
+
+                return ShardRank(cfg, backend.process_group)
+        elif shards > 1:
             if store_particles:
                 raise NotImplementedError("store_particles is not supported by sharded runs")
             if resampler != "cutpoint":
@@ -221,7 +234,10 @@ def _run_loop(model, priors, y, n, seed, backend, resampler, precision, store_pa
         if noise is not None:
             feed = {k: np.ascontiguousarray(np.asarray(v, dtype=np.float64))
                     for k, v in noise.items() if v is not None}
-        eng.run(y, out, feed)
+        if getattr(backend, "distributed", False):
+            eng.run_arrays(np.ascontiguousarray(y, dtype=np.float64), arrays, n)
+        else:
+            eng.run(y, out, feed)
     finally:
         if own:
             backend.close()
