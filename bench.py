@@ -99,11 +99,15 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def dist_setup():
+def dist_setup(force=False):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or force:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         import torch
         import torch.distributed as dist
 
@@ -125,7 +129,9 @@ def max_over_ranks(x, world):
 
 
 def barrier(world):
-    if world > 1:
+    import torch.distributed as dist
+
+    if world > 1 or dist.is_initialized():
         import torch.distributed as dist
 
         dist.barrier()
@@ -200,8 +206,10 @@ def main():
     ap.add_argument("--multi", default="shard", choices=["shard", "replicas"])
     ap.add_argument("--n-shard", type=int, default=1 << 27)
     ap.add_argument("--shards", type=int, default=1)
+    ap.add_argument("--process-group", action="store_true",
+                    help="run the one-process-per-GPU sharded path even with one rank")
     args = ap.parse_args()
-    world, rank, local = dist_setup()
+    world, rank, local = dist_setup(force=args.process_group)
     if args.impl == "reference":
         run_reference_arm(args, world, rank)
         return
@@ -211,7 +219,7 @@ def main():
     import paper_1212_1639_b200 as P
     from paper_1212_1639_b200 import _lib
 
-    if (world > 1 and args.multi == "shard") or args.shards > 1:
+    if (world > 1 and args.multi == "shard") or args.shards > 1 or args.process_group:
         return run_sharded(args, world, rank, local)
     lib = _lib.require_device()
     n, t_len = args.n, args.t
@@ -304,9 +312,10 @@ def run_sharded(args, world, rank, local):
     G = world if world > 1 else args.shards
     n = args.n_shard if world > 1 else args.n
     t_len = args.t
+    spmd = world > 1 or args.process_group
     _, y = P.simulate(P.TrendNoiseModel(), t_len, P.RngStream(0, P.rng.AUX_STREAM_BASE + 1))
     lib = _lib.require_device()
-    if world > 1:
+    if spmd:
         backend = P.Backend("cuda", device=local, process_group=True)
         where = f"one process per GPU, {G} ranks (NCCL exchange, CUDA IPC peer reads)"
     else:
@@ -360,7 +369,7 @@ def run_sharded(args, world, rank, local):
             "clocks": clk_summary,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if spmd:
         import torch.distributed as dist
 
         dist.destroy_process_group()

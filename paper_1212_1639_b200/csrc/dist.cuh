@@ -57,6 +57,7 @@ struct pf_shard {
   uint32_t qcap = 0;
   int cls_grid = 0;
   int qm = 0;
+  bool fused = false;  // draws computed inside the step kernel (FD)
   pf_outputs* out = nullptr;
 };
 
@@ -149,7 +150,14 @@ struct ShardOps {
     CK(cudaEventRecord(e->ev0, e->st));
     init_kernel<MODE><<<grid_for(ns, 256), 256, 0, e->st>>>(a);
     LAUNCHED();
-    if (T >= 1) return draws(s, 1);
+    // Fused draws (as the engine's large-N path): the step kernel evaluates
+    // its own normal / gamma draws from the per-step tables in shared memory.
+    static const int fused_env = [] {
+      const char* v = getenv("PF_FUSED_DRAWS");
+      return v ? atoi(v) : -1;
+    }();
+    s->fused = c.gamma_method == 0 && e->ntab && fused_env != 0;
+    if (T >= 1 && !s->fused) return draws(s, 1);
     return PF_OK;
   }
 
@@ -186,12 +194,28 @@ struct ShardOps {
     const pf_config& c = s->cfg;
     const int64_t ns = s->ns;
     const int par = (int)(t & 1);
-    const size_t step_smem = (size_t)2 * STEP_SB * 256 * (sizeof(Rec) + 3 * sizeof(double));
-    CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)step_smem));
+    const bool FDm = s->fused;
+    const int threads = FDm ? 512 : 256;
+    const bool share_tab = LS && LT && e->tab_s == e->tab_t && c.gamma_method == 0;
+    const int ngt = c.gamma_method == 0 ? (LS ? 1 : 0) + (LT && !share_tab ? 1 : 0) : 0;
+    const size_t draw_smem = ((size_t)ngt * GT_TABLE_DOUBLES + (e->ntab ? NT_TABLE_DOUBLES : 0)) * sizeof(double);
+    const size_t step_smem = (FDm ? (size_t)(((draw_smem / 8) + 3) & ~size_t(3)) * 8 : 0) +
+                             (size_t)2 * STEP_SB * threads * (sizeof(Rec) + 3 * sizeof(double));
+    static bool attr[8] = {false};
+    if (!attr[MODE]) {
+      CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)((2 * GT_TABLE_DOUBLES + NT_TABLE_DOUBLES + 4) * sizeof(double) +
+                                    2 * STEP_SB * 512 * (sizeof(Rec) + 3 * sizeof(double)))));
+      CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(2 * STEP_SB * 256 * (sizeof(Rec) + 3 * sizeof(double)))));
+      attr[MODE] = true;
+    }
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, step_kernel<MODE, TQ, false>, 256, step_smem));
-    const int64_t nb = (ns + STEP_SB * 256 - 1) / (STEP_SB * 256);
+    if (FDm)
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, step_kernel<MODE, TQ, true>, threads, step_smem));
+    else
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, step_kernel<MODE, TQ, false>, threads, step_smem));
+    const int64_t nb = (ns + STEP_SB * threads - 1) / (STEP_SB * threads);
     const int grid = (int)std::min<int64_t>(nb, (int64_t)sm_count() * std::max(occ, 1));
     StepArgs<TQ> a;
     memset(&a, 0, sizeof(a));
@@ -236,11 +260,26 @@ struct ShardOps {
       a.slk.q[h] = (const TQ*)s->p_q[h];
       a.recs[h] = s->p_rec[s->cur][h];
     }
-    step_kernel<MODE, TQ, false><<<grid, 256, step_smem, e->st>>>(a);
-    LAUNCHED();
-    if (t < s->T) {
-      int rc = draws(s, t + 1);
-      if (rc != PF_OK) return rc;
+    if (FDm) {
+      a.dr.n = ns;
+      a.dr.t = t;
+      a.dr.seed = c.seed;
+      a.dr.gs = gamma_src(e, true, t);
+      a.dr.gt = gamma_src(e, false, t);
+      a.dr.ntab = e->ntab;
+      a.dr.u3 = e->du3.p + (size_t)par * ns;  // resampling words of step t
+      a.dr.fail = e->fail.p;
+      a.dr.gbase = (int64_t)s->rank * ns;
+      a.z = a.g_s = a.g_t = nullptr;
+      step_kernel<MODE, TQ, true><<<grid, threads, step_smem, e->st>>>(a);
+      LAUNCHED();
+    } else {
+      step_kernel<MODE, TQ, false><<<grid, threads, step_smem, e->st>>>(a);
+      LAUNCHED();
+      if (t < s->T) {
+        int rc = draws(s, t + 1);
+        if (rc != PF_OK) return rc;
+      }
     }
     if (s->out && s->out->indices && t > 1)
       CK(cudaMemcpyAsync(s->out->indices + (size_t)(t - 2) * ns, e->idx.p, ns * sizeof(int64_t),

@@ -84,3 +84,13 @@ def test_process_group_single_precision(gpu, tmp_path):
     n, t_len = 1 << 14, 10
     d = _launch(tmp_path, 2, "--particles", str(n), "--series-len", str(t_len), "--kind", "single")
     _check(_single("single", n, t_len, 5), d, 0)
+
+
+def test_process_group_nccl_path(gpu, tmp_path):
+    # NCCL refuses two ranks on one GPU; a one-rank NCCL group still runs the
+    # stream-ordered path (in-place all-gathers on the engine's stream, the
+    # IPC-free own-rank tables, the device-side barrier).
+    n, t_len = 1 << 14, 12
+    d = _launch(tmp_path, 1, "--particles", str(n), "--series-len", str(t_len), "--backend", "nccl", "--runs", "2")
+    for r in range(2):
+        _check(_single("learning", n, t_len, 5 + r), d, r)
