@@ -1250,11 +1250,21 @@ int pf_engine_create(const pf_config* cfg, pf_engine** out) {
     return rc;
   };
   cudaError_t err;
-  if ((err = cudaStreamCreateWithFlags(&e->st, cudaStreamNonBlocking))) return bail(err);
+  // Stream priorities: the critical path (step kernel, CDF) outranks the
+  // side stream's quantile work, so when both have CTAs waiting the block
+  // scheduler places the critical path's first.  PF_STREAM_PRIO=0 disables.
+  static const int prio_env = [] {
+    const char* v = getenv("PF_STREAM_PRIO");
+    return v ? atoi(v) : 1;
+  }();
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (!prio_env) prio_lo = prio_hi = 0;
+  if ((err = cudaStreamCreateWithPriority(&e->st, cudaStreamNonBlocking, prio_hi))) return bail(err);
   // The step kernel's reads are random 32-byte records; do not let L2
   // promote each miss into a 64/128-byte DRAM fetch.
   cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32);
-  if ((err = cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking))) return bail(err);
+  if ((err = cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking, prio_lo))) return bail(err);
   if ((err = cudaStreamCreateWithFlags(&e->dstream, cudaStreamNonBlocking)) ||
       (err = cudaEventCreateWithFlags(&e->ev_draw, cudaEventDisableTiming)) ||
       (err = cudaEventCreateWithFlags(&e->ev_step, cudaEventDisableTiming)) ||
