@@ -99,6 +99,8 @@ template <typename T>
 __global__ void __launch_bounds__(CDF_THREADS)
 cdf_reduce_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ chunk_tot,
                   const int64_t* __restrict__ fail) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (fail && *fail) return;
   __shared__ T wt[CDF_THREADS / 32];
   __shared__ T tt[64];
@@ -135,6 +137,8 @@ template <typename T>
 __global__ void __launch_bounds__(1024)
 cdf_top_kernel(const T* __restrict__ chunk_tot, int64_t G, T* __restrict__ node,
                T* __restrict__ carry, T* __restrict__ total_out, int64_t* fail, int64_t step) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (fail && *fail) return;
   extern __shared__ unsigned char smem_raw[];
   T* fw = reinterpret_cast<T*>(smem_raw);  // forward levels, 2G-1 nodes
@@ -263,6 +267,8 @@ PF_D uint32_t strata_f(T q, int64_t L, double unitB /* 2^B */) {
 __global__ void __launch_bounds__(256)
 group_build_kernel(const int32_t* __restrict__ cut, int64_t ngroups, Grp* __restrict__ grp,
                    const int64_t* __restrict__ fail) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (fail && *fail) return;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups;
        g += (int64_t)gridDim.x * blockDim.x) {
@@ -295,6 +301,8 @@ cdf_expand_kernel(WSrc src, int64_t n, int R, const T* __restrict__ tile_tot,
                   const T* __restrict__ total_p, T* __restrict__ q_out,
                   int32_t* __restrict__ cut_out, const int64_t* __restrict__ fail,
                   RankOut ro = RankOut(), int64_t gbase = 0) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (fail && *fail) return;
   __shared__ T wt[CDF_THREADS / 32];
   __shared__ T wmax[CDF_THREADS / 32];

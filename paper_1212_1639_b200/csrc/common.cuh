@@ -41,6 +41,24 @@ PF_HD int ilog2(int64_t n) {
   return k;
 }
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the
+// programmatic-stream-serialization attribute may start while its stream
+// predecessor is still draining.  pdl_wait() blocks until every prerequisite
+// grid has completed and its memory is visible -- it must precede any read
+// of a predecessor's output (and any write a predecessor could still read).
+// pdl_launch_dependents() lets the next kernel in the stream be scheduled
+// early.  Both are no-ops for kernels launched without the attribute.
+PF_D void pdl_wait() {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 900
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+PF_D void pdl_launch_dependents() {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 900
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
 // numpy's np.max propagates NaN: keep a NaN from either side.
 PF_D double nan_max(double a, double b) { return (a > b || a != a) ? a : b; }
 

@@ -70,6 +70,39 @@ struct DevBuf {
   }
 };
 
+// Launch on the critical-path stream with programmatic stream serialization
+// (PDL): the kernel may be scheduled while its predecessor drains; its
+// pdl_wait() (common.cuh) orders every dependent access.  PF_PDL is a mask
+// of the launches that use it (1 step kernel, 2 K2, 4 K3, 8 K4, 16 group
+// build); 0 disables.  Measured at N = 2^24 (profiles/r01_pdl_ab.txt): only
+// the top-tree launch gains (its single CTA is resident before K2 drains);
+// early-resident K4 / group / step CTAs cost the concurrent quantile work
+// more than the hidden launch latency saves.
+enum { PDL_STEP = 1, PDL_K2 = 2, PDL_K3 = 4, PDL_K4 = 8, PDL_GRP = 16 };
+int pdl_enabled() {
+  static const int on = [] {
+    const char* v = getenv("PF_PDL");
+    return v ? atoi(v) : (int)PDL_K3;
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(int which, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = (pdl_enabled() & which) ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 int grid_for(int64_t n, int block, int cap = 148 * 16) {
   int64_t g = (n + block - 1) / block;
   if (g < 1) g = 1;
@@ -269,8 +302,8 @@ int launch_cdf(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t* fai
     LAUNCHED();
     return PF_OK;
   }
-  cdf_reduce_kernel<T><<<(int)p.chunks, CDF_THREADS, 0, st>>>(src, p.R, (T*)b.tile_tot.p,
-                                                              (T*)b.chunk_tot.p, fail);
+  CK(launch_pdl(PDL_K2, cdf_reduce_kernel<T>, dim3((int)p.chunks), dim3(CDF_THREADS), 0, st, src, p.R, (T*)b.tile_tot.p,
+                (T*)b.chunk_tot.p, (const int64_t*)fail));
   LAUNCHED();
   return launch_cdf_tail<T>(b, src, n, q, cut, fail, step, st, so);
 }
@@ -292,14 +325,16 @@ int launch_cdf_tail(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t
                             4 * CDF_MAX_CHUNKS * (int)sizeof(T)));
     attr_set[sizeof(T) == 8] = true;
   }
-  cdf_top_kernel<T><<<1, 1024, smem, st>>>(ct, p.chunks, nd, cr, total, fail, step);
+  CK(launch_pdl(PDL_K3, cdf_top_kernel<T>, dim3(1), dim3(1024), smem, st, (const T*)ct, p.chunks, nd, cr, total, fail, step));
   LAUNCHED();
   if (so.on) {
-    cdf_expand_kernel<T, true><<<(int)p.chunks, CDF_THREADS, 0, st>>>(src, n, p.R, tt, nd, cr, total, q, cut,
-                                                                    fail, so.ro);
+    CK(launch_pdl(PDL_K4, cdf_expand_kernel<T, true>, dim3((int)p.chunks), dim3(CDF_THREADS), 0, st, src, n, p.R,
+                  (const T*)tt, (const T*)nd, (const T*)cr, (const T*)total, q, cut, (const int64_t*)fail, so.ro,
+                  (int64_t)0));
     LAUNCHED();
     const int64_t ng = n / GRP_STRATA;
-    group_build_kernel<<<grid_for(ng, 256, 148 * 8), 256, 0, st>>>(so.ro.cut, ng, so.grp, fail);
+    CK(launch_pdl(PDL_GRP, group_build_kernel, dim3(grid_for(ng, 256, 148 * 8)), dim3(256), 0, st,
+                  (const int32_t*)so.ro.cut, ng, so.grp, (const int64_t*)fail));
   } else
     cdf_expand_kernel<T, false><<<(int)p.chunks, CDF_THREADS, 0, st>>>(src, n, p.R, tt, nd, cr, total, q, cut,
                                                                      fail);
@@ -851,13 +886,13 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       cudaEventCreate(&b0);
       cudaEventCreate(&b1);
       cudaEventRecord(b0, st);
-      if (fused) step_kernel<MODE, TQ, true><<<step_grid, STEP_THREADS, step_smem, st>>>(a);
-      else step_kernel<MODE, TQ, false><<<step_grid, STEP_THREADS, step_smem, st>>>(a);
+      if (fused) CK(launch_pdl(PDL_STEP, step_kernel<MODE, TQ, true>, dim3(step_grid), dim3(STEP_THREADS), step_smem, st, a));
+      else CK(launch_pdl(PDL_STEP, step_kernel<MODE, TQ, false>, dim3(step_grid), dim3(STEP_THREADS), step_smem, st, a));
       cudaEventRecord(b1, st);
       step_evs.push_back({b0, b1});
     } else {
-      if (fused) step_kernel<MODE, TQ, true><<<step_grid, STEP_THREADS, step_smem, st>>>(a);
-      else step_kernel<MODE, TQ, false><<<step_grid, STEP_THREADS, step_smem, st>>>(a);
+      if (fused) CK(launch_pdl(PDL_STEP, step_kernel<MODE, TQ, true>, dim3(step_grid), dim3(STEP_THREADS), step_smem, st, a));
+      else CK(launch_pdl(PDL_STEP, step_kernel<MODE, TQ, false>, dim3(step_grid), dim3(STEP_THREADS), step_smem, st, a));
     }
     LAUNCHED();
     ++step_launches;

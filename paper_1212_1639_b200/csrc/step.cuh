@@ -393,9 +393,12 @@ PF_D void cp_async8(uint32_t dst, const void* src) {
 template <int MODE, typename TQ, bool FD = false>
 __global__ void __launch_bounds__(FD ? 512 : 256) step_kernel(StepArgs<TQ> a) {
   constexpr bool LS = MODE & M_LS, LT = MODE & M_LT, SINGLE = MODE & M_SINGLE;
-  if (*a.fail) return;
+  // the step's tables are constant over the run: stage them while the
+  // previous kernel (group build / K4) drains, then wait for its outputs
   int slot_s = -1, slot_t = -1, noff = -1, tab_doubles = 0;
   if (FD) tab_doubles = stage_tables<LS, LT>(a.dr.gs, a.dr.gt, a.dr.ntab, slot_s, slot_t, noff);
+  pdl_wait();
+  if (*a.fail) return;
   const bool feedw = a.feed_w != nullptr;
   const double cs = a.sc->cs, ct = a.sc->ct, cx = a.sc->cx;
   double m = feedw ? 0.0 : -INFINITY;
@@ -577,6 +580,7 @@ __global__ void __launch_bounds__(FD ? 512 : 256) step_kernel(StepArgs<TQ> a) {
     cur ^= 1;
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
+  pdl_launch_dependents();  // only the CTA reductions remain
 
   // ---- CTA reduction with rescaling to the CTA max
   __shared__ double red[16][8];
