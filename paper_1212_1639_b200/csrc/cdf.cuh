@@ -94,11 +94,115 @@ PF_D void thread_tree8(const T (&v)[8], T (&l1)[4], T (&l2)[2], T& l3) {
   l3 = l2[0] + l2[1];
 }
 
+// ------------------------------------------------------------------ K3 ---
+// The top of the adder tree over the G chunk totals (prefix_sum.py:46-91):
+// forward levels, backward pass down to the G chunk node values, and the
+// exclusive running max of the nodes (the carry into each chunk).  One CTA;
+// its scratch (fw: 2G, b0/b1: G each) is shared memory (cdf_top_kernel) or
+// global memory reached through L2 (K2's last CTA, below).
+struct SmemIO {
+  template <typename T>
+  PF_D static T ld(const T* p) { return *p; }
+  template <typename T>
+  PF_D static void st(T* p, T v) { *p = v; }
+};
+struct GlobalIO {  // L1-bypassing: the scratch is rewritten every step
+  template <typename T>
+  PF_D static T ld(const T* p) { return __ldcg(p); }
+  template <typename T>
+  PF_D static void st(T* p, T v) { __stcg(p, v); }
+};
+
+template <typename T, typename IO>
+PF_D void top_tree_body(const T* __restrict__ chunk_tot, int64_t G, T* fw, T* b0, T* b1, T* __restrict__ node,
+                        T* __restrict__ carry, T* __restrict__ total_out, int64_t* fail, int64_t step) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int64_t i = tid; i < G; i += nt) IO::st(fw + i, __ldcg(chunk_tot + i));
+  __syncthreads();
+  int64_t off = 0, len = G;
+  while (len > 1) {
+    for (int64_t i = tid; i < len / 2; i += nt) IO::st(fw + off + len + i, (T)(IO::ld(fw + off + 2 * i) + IO::ld(fw + off + 2 * i + 1)));
+    __syncthreads();
+    off += len;
+    len >>= 1;
+  }
+  const T total = IO::ld(fw + off);
+  // backward: level offsets from the top down
+  T* par = b0;
+  T* chi = b1;
+  if (tid == 0) IO::st(par, total);
+  __syncthreads();
+  int64_t plen = 1;
+  int64_t loff = off;  // offset of the parent level in fw
+  while (plen < G) {
+    const int64_t clen = plen * 2;
+    const int64_t coff = loff - clen;
+    for (int64_t i = tid; i < clen; i += nt) {
+      const T p = IO::ld(par + (i >> 1));
+      IO::st(chi + i, (i & 1) ? p : (T)(p - IO::ld(fw + coff + i + 1)));
+    }
+    __syncthreads();
+    T* tmp = par;
+    par = chi;
+    chi = tmp;
+    plen = clen;
+    loff = coff;
+  }
+  // par[0..G) = chunk node values.  Exclusive running max -> carry
+  // (max is exact, so any scan order gives the reference's
+  // np.maximum.accumulate bits).
+  for (int64_t i = tid; i < G; i += nt) node[i] = IO::ld(par + i);
+  {
+    __shared__ T wm[32];
+    const int64_t per = (G + nt - 1) / nt;
+    const int64_t lo = tid * per;
+    const int64_t hi = lo + per < G ? lo + per : G;
+    T loc = (T)(-INFINITY);
+    for (int64_t i = lo; i < hi; ++i) loc = fmax(loc, IO::ld(par + i));
+    const int lane = tid & 31, warp = tid >> 5;
+    T incl = loc;
+    for (int o = 1; o < 32; o <<= 1) {
+      const T other = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl = fmax(incl, other);
+    }
+    if (lane == 31) wm[warp] = incl;
+    __syncthreads();
+    T pre = (T)(-INFINITY);
+    for (int w = 0; w < warp; ++w) pre = fmax(pre, wm[w]);
+    T ex = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane > 0) pre = fmax(pre, ex);
+    for (int64_t i = lo; i < hi; ++i) {
+      carry[i] = pre;
+      pre = fmax(pre, IO::ld(par + i));
+    }
+  }
+  if (tid == 0) {
+    *total_out = total;
+    if (!(total > (T)0) || !isfinite((double)total)) {
+      if (fail) atomicCAS((unsigned long long*)fail, 0ull, (unsigned long long)(-step));
+    }
+  }
+}
+
+// K2 + K3 fused: when top.ctr is set, the last CTA to finish its chunk runs
+// the top tree (no separate single-CTA launch, which a concurrent
+// side-stream kernel holding every SM's resources could delay).
+template <typename T>
+struct TopFuse {
+  unsigned int* ctr = nullptr;  // zero between launches; the last CTA resets it
+  T* scratch = nullptr;         // 4G
+  T* node = nullptr;
+  T* carry = nullptr;
+  T* total = nullptr;
+  int64_t* fail = nullptr;
+  int64_t step = 0;
+};
+
 // ------------------------------------------------------------------ K2 ---
 template <typename T>
 __global__ void __launch_bounds__(CDF_THREADS)
 cdf_reduce_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ chunk_tot,
-                  const int64_t* __restrict__ fail) {
+                  const int64_t* __restrict__ fail, TopFuse<T> top = TopFuse<T>()) {
   pdl_wait();
   pdl_launch_dependents();
   if (fail && *fail) return;
@@ -129,9 +233,22 @@ cdf_reduce_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ chu
       for (int i = 0; i < len / 2; ++i) tt[i] = tt[2 * i] + tt[2 * i + 1];
     chunk_tot[chunk] = tt[0];
   }
+  if (top.ctr) {
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last = atomicAdd(top.ctr, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int64_t G = gridDim.x;
+    top_tree_body<T, GlobalIO>(chunk_tot, G, top.scratch, top.scratch + 2 * G, top.scratch + 3 * G, top.node,
+                               top.carry, top.total, top.fail, top.step);
+    if (threadIdx.x == 0) *top.ctr = 0u;
+  }
 }
 
-// ------------------------------------------------------------------ K3 ---
 // One CTA of 1024 threads; dynamic smem = (2G + 2G) * sizeof(T).
 template <typename T>
 __global__ void __launch_bounds__(1024)
@@ -142,74 +259,7 @@ cdf_top_kernel(const T* __restrict__ chunk_tot, int64_t G, T* __restrict__ node,
   if (fail && *fail) return;
   extern __shared__ unsigned char smem_raw[];
   T* fw = reinterpret_cast<T*>(smem_raw);  // forward levels, 2G-1 nodes
-  T* b0 = fw + 2 * G;                       // backward ping
-  T* b1 = b0 + G;                           // backward pong
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (int64_t i = tid; i < G; i += nt) fw[i] = chunk_tot[i];
-  __syncthreads();
-  int64_t off = 0, len = G;
-  while (len > 1) {
-    for (int64_t i = tid; i < len / 2; i += nt) fw[off + len + i] = fw[off + 2 * i] + fw[off + 2 * i + 1];
-    __syncthreads();
-    off += len;
-    len >>= 1;
-  }
-  const T total = fw[off];
-  // backward: level offsets from the top down
-  T* par = b0;
-  T* chi = b1;
-  if (tid == 0) par[0] = total;
-  __syncthreads();
-  int64_t plen = 1;
-  int64_t loff = off;  // offset of the parent level in fw
-  while (plen < G) {
-    const int64_t clen = plen * 2;
-    const int64_t coff = loff - clen;
-    for (int64_t i = tid; i < clen; i += nt) {
-      const T p = par[i >> 1];
-      chi[i] = (i & 1) ? p : (T)(p - fw[coff + i + 1]);
-    }
-    __syncthreads();
-    T* tmp = par;
-    par = chi;
-    chi = tmp;
-    plen = clen;
-    loff = coff;
-  }
-  // par[0..G) = chunk node values.  Exclusive running max -> carry
-  // (max is exact, so any scan order gives the reference's
-  // np.maximum.accumulate bits).
-  for (int64_t i = tid; i < G; i += nt) node[i] = par[i];
-  {
-    __shared__ T wm[32];
-    const int64_t per = (G + nt - 1) / nt;
-    const int64_t lo = tid * per;
-    const int64_t hi = lo + per < G ? lo + per : G;
-    T loc = (T)(-INFINITY);
-    for (int64_t i = lo; i < hi; ++i) loc = fmax(loc, par[i]);
-    const int lane = tid & 31, warp = tid >> 5;
-    T incl = loc;
-    for (int o = 1; o < 32; o <<= 1) {
-      const T other = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl = fmax(incl, other);
-    }
-    if (lane == 31) wm[warp] = incl;
-    __syncthreads();
-    T pre = (T)(-INFINITY);
-    for (int w = 0; w < warp; ++w) pre = fmax(pre, wm[w]);
-    T ex = __shfl_up_sync(0xffffffffu, incl, 1);
-    if (lane > 0) pre = fmax(pre, ex);
-    for (int64_t i = lo; i < hi; ++i) {
-      carry[i] = pre;
-      pre = fmax(pre, par[i]);
-    }
-  }
-  if (tid == 0) {
-    *total_out = total;
-    if (!(total > (T)0) || !isfinite((double)total)) {
-      if (fail) atomicCAS((unsigned long long*)fail, 0ull, (unsigned long long)(-step));
-    }
-  }
+  top_tree_body<T, SmemIO>(chunk_tot, G, fw, fw + 2 * G, fw + 3 * G, node, carry, total_out, fail, step);
 }
 
 // ------------------------------------------------ stratum lookup tables ---

@@ -203,24 +203,33 @@ int weighted_quantiles_dev(QuantileScratch& s, const double* vals, WSrc w, int64
   return PF_OK;
 }
 
-// K2 with the region-form quantile windows, dispatched on the quantity mask.
-// Classification only (side stream): persistent over the n / 2048 tiles.
+// Window classification (side stream), dispatched on the quantity mask:
+// persistent over the n / (CLS_THR * 8) classification tiles.  Measured
+// (profiles/r01_classify_ab.txt): 128-thread CTAs that co-reside with the
+// step kernel only move the classification's issue cost into the step
+// kernel (+150 us/step); 256-thread CTAs over one wave stay ahead.
+constexpr int CLS_THR = 256;
 template <typename TQ, int QM>
 int launch_reduce_qr_m(int grid, WSrc src, int R, TQ* tt, TQ* ct, int64_t* fail, const QArgs& qa,
                        cudaStream_t st) {
   constexpr int NQ = (QM & 1) + ((QM >> 1) & 1) + ((QM >> 2) & 1);
-  const size_t smem = (size_t)NQ * (2 * Q_PER + 1) * CDF_THREADS * sizeof(double);
+  const size_t smem = (size_t)NQ * (2 * Q_PER + 1) * CLS_THR * sizeof(double);
+  auto kern = cdf_reduce_qr_kernel<TQ, QM, false, CLS_THR>;
   static int occ = 0;
   if (!occ) {
-    CK(cudaFuncSetAttribute(cdf_reduce_qr_kernel<TQ, QM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cdf_reduce_qr_kernel<TQ, QM, false>, CDF_THREADS,
-                                                     smem));
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, CLS_THR, smem));
     if (occ < 1) occ = 1;
   }
   (void)grid;
-  const int g = (int)std::min<int64_t>((int64_t)R, (int64_t)sm_count() * occ);
-  cdf_reduce_qr_kernel<TQ, QM, false><<<g, CDF_THREADS, smem, st>>>(src, R, tt, ct, fail, qa);
+  static const int env_grid = [] {
+    const char* v = getenv("PF_CLS_GRID");
+    return v ? atoi(v) : 0;
+  }();
+  const int64_t tiles = R * (int64_t)(CDF_THREADS / CLS_THR);  // R: K2 tiles
+  const int64_t want = env_grid > 0 ? std::min<int64_t>(env_grid, CDF_MAX_CHUNKS) : (int64_t)sm_count() * occ;
+  const int g = (int)std::min<int64_t>(tiles, want);
+  kern<<<g, CLS_THR, smem, st>>>(src, (int)tiles, tt, ct, fail, qa);
   LAUNCHED();
   return PF_OK;
 }
@@ -270,17 +279,28 @@ int launch_reduce_qr(int qm, int grid, WSrc src, int R, TQ* tt, TQ* ct, int64_t*
 // ---------------------------------------------------------------- CDF ---
 struct CdfBufs {
   CdfPlan plan;
-  DevBuf<unsigned char> tile_tot, chunk_tot, node, carry, total;
+  DevBuf<unsigned char> tile_tot, chunk_tot, node, carry, total, top_scratch;
+  DevBuf<unsigned int> top_ctr;  // K2's last-CTA counter (zero between launches)
   cudaError_t ensure(int64_t n, size_t esz) {
     plan = cdf_plan(n);
     cudaError_t e;
     if ((e = tile_tot.ensure(plan.tiles * esz)) || (e = chunk_tot.ensure(plan.chunks * esz)) ||
         (e = node.ensure(plan.chunks * esz)) || (e = carry.ensure(plan.chunks * esz)) ||
-        (e = total.ensure(2 * esz)))
+        (e = total.ensure(2 * esz)) || (e = top_scratch.ensure(4 * plan.chunks * esz)) || (e = top_ctr.ensure(1)))
       return e;
-    return cudaSuccess;
+    return cudaMemset(top_ctr.p, 0, sizeof(unsigned int));
   }
 };
+
+// PF_FUSE_TOP=0: separate single-CTA top-tree launch (K3) instead of K2's
+// last CTA.
+bool fuse_top() {
+  static const bool on = [] {
+    const char* v = getenv("PF_FUSE_TOP");
+    return v ? atoi(v) != 0 : true;
+  }();
+  return on;
+}
 
 struct StrataOut {
   RankOut ro{nullptr, nullptr, nullptr, 0};
@@ -288,9 +308,19 @@ struct StrataOut {
   bool on = false;
 };
 
+// PF_CHAIN_DEBUG: events after each CDF-chain launch (resident diagnostics)
+std::vector<cudaEvent_t>* g_chain_rec = nullptr;
+void chain_mark(cudaStream_t st) {
+  if (!g_chain_rec) return;
+  cudaEvent_t ev;
+  cudaEventCreate(&ev);
+  cudaEventRecord(ev, st);
+  g_chain_rec->push_back(ev);
+}
+
 template <typename T>
 int launch_cdf_tail(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t* fail, int64_t step,
-                    cudaStream_t st, StrataOut so = StrataOut());
+                    cudaStream_t st, StrataOut so = StrataOut(), bool top_done = false);
 
 template <typename T>
 int launch_cdf(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t* fail, int64_t step,
@@ -302,16 +332,28 @@ int launch_cdf(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t* fai
     LAUNCHED();
     return PF_OK;
   }
+  TopFuse<T> top;
+  const bool fused = fuse_top();
+  if (fused) {
+    top.ctr = b.top_ctr.p;
+    top.scratch = (T*)b.top_scratch.p;
+    top.node = (T*)b.node.p;
+    top.carry = (T*)b.carry.p;
+    top.total = total;
+    top.fail = fail;
+    top.step = step;
+  }
   CK(launch_pdl(PDL_K2, cdf_reduce_kernel<T>, dim3((int)p.chunks), dim3(CDF_THREADS), 0, st, src, p.R, (T*)b.tile_tot.p,
-                (T*)b.chunk_tot.p, (const int64_t*)fail));
+                (T*)b.chunk_tot.p, (const int64_t*)fail, top));
   LAUNCHED();
-  return launch_cdf_tail<T>(b, src, n, q, cut, fail, step, st, so);
+  chain_mark(st);
+  return launch_cdf_tail<T>(b, src, n, q, cut, fail, step, st, so, fused);
 }
 
 // K3 + K4 (after K2, or after the quantile-fused K2).
 template <typename T>
 int launch_cdf_tail(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t* fail, int64_t step,
-                    cudaStream_t st, StrataOut so) {
+                    cudaStream_t st, StrataOut so, bool top_done) {
   const CdfPlan& p = b.plan;
   T* total = (T*)b.total.p;
   T* tt = (T*)b.tile_tot.p;
@@ -325,13 +367,18 @@ int launch_cdf_tail(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t
                             4 * CDF_MAX_CHUNKS * (int)sizeof(T)));
     attr_set[sizeof(T) == 8] = true;
   }
-  CK(launch_pdl(PDL_K3, cdf_top_kernel<T>, dim3(1), dim3(1024), smem, st, (const T*)ct, p.chunks, nd, cr, total, fail, step));
-  LAUNCHED();
+  if (!top_done) {
+    CK(launch_pdl(PDL_K3, cdf_top_kernel<T>, dim3(1), dim3(1024), smem, st, (const T*)ct, p.chunks, nd, cr, total,
+                  fail, step));
+    LAUNCHED();
+  }
+  chain_mark(st);
   if (so.on) {
     CK(launch_pdl(PDL_K4, cdf_expand_kernel<T, true>, dim3((int)p.chunks), dim3(CDF_THREADS), 0, st, src, n, p.R,
                   (const T*)tt, (const T*)nd, (const T*)cr, (const T*)total, q, cut, (const int64_t*)fail, so.ro,
                   (int64_t)0));
     LAUNCHED();
+    chain_mark(st);
     const int64_t ng = n / GRP_STRATA;
     CK(launch_pdl(PDL_GRP, group_build_kernel, dim3(grid_for(ng, 256, 148 * 8)), dim3(256), 0, st,
                   (const int32_t*)so.ro.cut, ng, so.grp, (const int64_t*)fail));
@@ -551,9 +598,12 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   const int64_t n = e->n, T = rs.T;
   cudaStream_t st = e->st;
   pf_outputs* out = rs.out;
-  const bool want_fq = out ? (out->filtered_quantiles != nullptr) : (c.track_quantiles != 0);
-  const bool want_sq = LS;
-  const bool want_tq = LT;
+  // PF_SKIP_QUANTILES=1: diagnostic only (measures the weighted-quantile
+  // cost; the quantile outputs are then left unwritten)
+  static const bool skip_q = getenv("PF_SKIP_QUANTILES") != nullptr;
+  const bool want_fq = !skip_q && (out ? (out->filtered_quantiles != nullptr) : (c.track_quantiles != 0));
+  const bool want_sq = LS && !skip_q;
+  const bool want_tq = LT && !skip_q;
   const bool keep_idx = out && out->indices;
   const bool keep_final = out && (out->final_states || out->final_sigma2);
   const bool store = out && out->hist_states;
@@ -664,6 +714,11 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   };
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> step_evs, sort_evs;
   if (rs.resident) step_evs.reserve((size_t)T);
+  // PF_CHAIN_DEBUG=1 (resident runs): per-step split of the critical path
+  // into step kernel / CDF chain / gap before the next step kernel (stderr)
+  static const bool chain_dbg = getenv("PF_CHAIN_DEBUG") != nullptr;
+  std::vector<cudaEvent_t> chain_evs, chain_sub;
+  g_chain_rec = (chain_dbg && rs.resident) ? &chain_sub : nullptr;
 
   CK(cudaEventRecord(e->ev0, st));
   if (timing) ev_record();
@@ -1011,10 +1066,14 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       q_step_end_kernel<<<1, 1024, 0, ss>>>(qa, 1);
       g_launches.fetch_add(2);
       CK(cudaEventRecord(e->ev_q[t & 1], ss));
-    } else {
-      if ((rc = launch_cdf<TQ>(e->cdf, wsrc, n, qv, e->cut.p, e->fail.p, t, st, so)) != PF_OK) return rc;
     }
     mark(PH_CDF);
+    if (chain_dbg && rs.resident) {  // diagnostics: end of the step's CDF chain
+      cudaEvent_t ce;
+      cudaEventCreate(&ce);
+      cudaEventRecord(ce, st);
+      chain_evs.push_back(ce);
+    }
 
     // ---- store: post-resample snapshot of step t
     if (store) {
@@ -1186,10 +1245,45 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       float k = 0;
       cudaEventElapsedTime(&k, pr.first, pr.second);
       acc += k;
+    }
+    e->last_step_ms = step_evs.empty() ? 0.0 : acc / step_evs.size();
+    if (chain_dbg && chain_evs.size() == step_evs.size() && chain_evs.size() > 2) {
+      double ch = 0, gap = 0;
+      int cnt = 0;
+      for (size_t i = 1; i + 1 < chain_evs.size(); ++i) {
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, step_evs[i].second, chain_evs[i]);
+        cudaEventElapsedTime(&b, chain_evs[i], step_evs[i + 1].first);
+        ch += a;
+        gap += b;
+        ++cnt;
+      }
+      fprintf(stderr, "[chain] step %.4f ms  cdf chain %.4f ms  gap %.4f ms (avg over %d steps)\n",
+              acc / step_evs.size(), ch / cnt, gap / cnt, cnt);
+      if (chain_sub.size() != 3 * chain_evs.size())
+        fprintf(stderr, "[chain] %zu sub-events for %zu steps\n", chain_sub.size(), chain_evs.size());
+      if (chain_sub.size() == 3 * chain_evs.size()) {  // K2 | K3 | K4 | group segments
+        double seg[4] = {0, 0, 0, 0};
+        for (size_t i = 1; i + 1 < chain_evs.size(); ++i) {
+          cudaEvent_t p[5] = {step_evs[i].second, chain_sub[3 * i], chain_sub[3 * i + 1], chain_sub[3 * i + 2],
+                              chain_evs[i]};
+          for (int k = 0; k < 4; ++k) {
+            float d = 0;
+            cudaEventElapsedTime(&d, p[k], p[k + 1]);
+            seg[k] += d;
+          }
+        }
+        fprintf(stderr, "[chain] K2 %.4f  K3 %.4f  K4 %.4f  group %.4f ms\n", seg[0] / cnt, seg[1] / cnt,
+                seg[2] / cnt, seg[3] / cnt);
+      }
+    }
+    for (auto ce : chain_sub) cudaEventDestroy(ce);
+    g_chain_rec = nullptr;
+    for (auto ce : chain_evs) cudaEventDestroy(ce);
+    for (auto& pr : step_evs) {
       cudaEventDestroy(pr.first);
       cudaEventDestroy(pr.second);
     }
-    e->last_step_ms = step_evs.empty() ? 0.0 : acc / step_evs.size();
   }
   if (out) {
     for (int k = 0; k < 7; ++k) out->phase_ns[k] = 0;

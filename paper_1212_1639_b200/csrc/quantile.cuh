@@ -476,10 +476,16 @@ PF_D void q_flush_compact(const QArgs& qa, QAgg& agg) {
   __syncthreads();
 }
 
-template <typename T, int QM, bool TREE>
-__global__ void __launch_bounds__(CDF_THREADS)
+// THR threads per CTA; a "tile" here is THR * CDF_V consecutive particles
+// (TREE requires THR == CDF_THREADS: the tile is K2's).  The classification-
+// only launch uses THR = 128 with <= 64 registers and ~35 KB of shared
+// memory, so a CTA fits beside a resident step-kernel CTA and the side
+// stream's classification overlaps the step kernel instead of the CDF chain.
+template <typename T, int QM, bool TREE, int THR = CDF_THREADS>
+__global__ void __launch_bounds__(THR, 65536 / (64 * THR))
 cdf_reduce_qr_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ chunk_tot,
                      const int64_t* __restrict__ fail, QArgs qa) {
+  static_assert(!TREE || THR == CDF_THREADS, "the fused tree pass uses K2's tiles");
   if (fail && *fail) return;
   constexpr int NR = 2 * Q_PER + 1;
   __shared__ T wt[CDF_THREADS / 32];
@@ -491,7 +497,7 @@ cdf_reduce_qr_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ 
   double* rsum = pf_gtab;
   auto RS = [&](int q, int r) -> double& {
     const int qi = __popc((unsigned)QM & ((1u << q) - 1u));
-    return rsum[(qi * NR + r) * CDF_THREADS + threadIdx.x];
+    return rsum[(qi * NR + r) * THR + threadIdx.x];
   };
   __shared__ uint32_t sb[Q_MAXQ][16];  // sorted bounds padded to 15 (+1) for the binary search
   q_agg_init(agg);
@@ -514,7 +520,7 @@ cdf_reduce_qr_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ 
   const int nloop = TREE ? R : (int)((R - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x);
   for (int r = 0; r < nloop; ++r) {
     const int64_t tile = TREE ? chunk * R + r : (int64_t)blockIdx.x + (int64_t)r * gridDim.x;
-    const int64_t base = tile * CDF_TILE + threadIdx.x * CDF_V;
+    const int64_t base = tile * (THR * CDF_V) + threadIdx.x * CDF_V;
     T v[CDF_V], l1[4], l2[2], g;
     load_tile_weights<T>(src, base, M, v);
     uint32_t key[Q_MAXQ][CDF_V];
