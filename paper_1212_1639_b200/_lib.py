@@ -21,6 +21,8 @@ from .errors import (
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libparsmc_b200.so")
+# PARSMC_B200_LIB: load a variant build instead (A/B experiments; scripts/)
+LIB_PATH = os.environ.get("PARSMC_B200_LIB", LIB_PATH)
 
 PF_OK = 0
 PF_ERR_ALL_WEIGHTS_ZERO = 1

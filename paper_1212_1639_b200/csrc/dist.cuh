@@ -195,7 +195,7 @@ struct ShardOps {
     const int64_t ns = s->ns;
     const int par = (int)(t & 1);
     const bool FDm = s->fused;
-    const int threads = FDm ? 512 : 256;
+    const int threads = FDm ? FD_THREADS : 256;
     const bool share_tab = LS && LT && e->tab_s == e->tab_t && c.gamma_method == 0;
     const int ngt = c.gamma_method == 0 ? (LS ? 1 : 0) + (LT && !share_tab ? 1 : 0) : 0;
     const size_t draw_smem = ((size_t)ngt * GT_TABLE_DOUBLES + (e->ntab ? NT_TABLE_DOUBLES : 0)) * sizeof(double);
@@ -205,7 +205,7 @@ struct ShardOps {
     if (!attr[MODE]) {
       CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)((2 * GT_TABLE_DOUBLES + NT_TABLE_DOUBLES + 4) * sizeof(double) +
-                                    2 * STEP_SB * 512 * (sizeof(Rec) + 3 * sizeof(double)))));
+                                    2 * STEP_SB * FD_THREADS * (sizeof(Rec) + 3 * sizeof(double)))));
       CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(2 * STEP_SB * 256 * (sizeof(Rec) + 3 * sizeof(double)))));
       attr[MODE] = true;

@@ -779,7 +779,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   }();
   const bool fused = c.gamma_method == 0 && e->ntab &&
                      (fused_env >= 0 ? fused_env != 0 : n >= ((int64_t)1 << 22));
-  const int STEP_THREADS = fused ? 512 : 256;
+  const int STEP_THREADS = fused ? FD_THREADS : 256;
   const size_t step_smem = (fused ? (size_t)(((draw_smem / 8) + 3) & ~size_t(3)) * 8 : 0) +
                            (size_t)2 * STEP_SB * STEP_THREADS * (sizeof(Rec) + 3 * sizeof(double));
   if (!fused) {
@@ -794,7 +794,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
                               (int)((2 * GT_TABLE_DOUBLES + NT_TABLE_DOUBLES) * sizeof(double))));
       CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)((2 * GT_TABLE_DOUBLES + NT_TABLE_DOUBLES + 4) * sizeof(double) +
-                                    2 * STEP_SB * 512 * (sizeof(Rec) + 3 * sizeof(double)))));
+                                    2 * STEP_SB * FD_THREADS * (sizeof(Rec) + 3 * sizeof(double)))));
       CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(2 * STEP_SB * 256 * (sizeof(Rec) + 3 * sizeof(double)))));
       attr[MODE] = true;

@@ -23,7 +23,14 @@
 namespace pf {
 
 constexpr double LOG_TWO_PI = 1.8378770664093453;  // math.log(2*math.pi), models.py:20
-constexpr int STEP_SB = 2;  // slots per thread per pipeline stage (double buffered)
+#ifndef PF_STEP_SB
+#define PF_STEP_SB 2
+#endif
+#ifndef PF_FD_THREADS
+#define PF_FD_THREADS 512
+#endif
+constexpr int STEP_SB = PF_STEP_SB;  // slots per thread per pipeline stage (double buffered)
+constexpr int FD_THREADS = PF_FD_THREADS;  // CTA width of the fused-draws step kernel
 
 // Order-preserving 32-bit image of a double (float32 rounded down, sign
 // folded): the quantile keys of quantile.cuh.
@@ -391,7 +398,7 @@ PF_D void cp_async8(uint32_t dst, const void* src) {
 // instead of a separate compute-bound draws kernel and a round trip of the
 // draws through HBM.
 template <int MODE, typename TQ, bool FD = false>
-__global__ void __launch_bounds__(FD ? 512 : 256) step_kernel(StepArgs<TQ> a) {
+__global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs<TQ> a) {
   constexpr bool LS = MODE & M_LS, LT = MODE & M_LT, SINGLE = MODE & M_SINGLE;
   // the step's tables are constant over the run: stage them while the
   // previous kernel (group build / K4) drains, then wait for its outputs
@@ -583,7 +590,7 @@ __global__ void __launch_bounds__(FD ? 512 : 256) step_kernel(StepArgs<TQ> a) {
   pdl_launch_dependents();  // only the CTA reductions remain
 
   // ---- CTA reduction with rescaling to the CTA max
-  __shared__ double red[16][8];
+  __shared__ double red[32][8];
   __shared__ double mblk;
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
