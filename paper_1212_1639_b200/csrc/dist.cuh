@@ -410,6 +410,7 @@ struct ShardOps {
       g_launches.fetch_add(4);
       if (round == 0) {
         for (int attempt = 0; attempt < 2; ++attempt) {
+          if (int r_ = fb_hist_smem()) return r_;
           q_fallback_prep_kernel<<<1, 32, 0, ss>>>(qa, attempt, e->fail.p);
           for (int h = 0; h < s->world; ++h) {  // every rank's particles (IPC reads)
             QArgs q2 = qa;
@@ -420,7 +421,7 @@ struct ShardOps {
             q2.pbase = h * fb_grid;
             q2.ptotal = s->world * fb_grid;
             q2.gbase = (uint32_t)((int64_t)h * ns);
-            q_fallback_hist_kernel<<<fb_grid, 256, 0, ss>>>(q2, s->p_lw[h] + (size_t)par * ns, 0,
+            q_fallback_hist_kernel<<<fb_grid, 256, QFB_SMEM_BYTES, ss>>>(q2, s->p_lw[h] + (size_t)par * ns, 0,
                                                             s->p_mbuf[h] + par, ns, SINGLE, attempt, e->fail.p);
           }
           q_fallback_select_kernel<<<ntg, 1024, 0, ss>>>(qa, attempt, e->fail.p);

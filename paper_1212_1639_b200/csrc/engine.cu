@@ -308,6 +308,31 @@ struct StrataOut {
   bool on = false;
 };
 
+// The fallback histogram kernel's shared-memory histograms exceed the 48 KB
+// default: opt in once per device.
+int fb_hist_smem() {
+  static bool done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !done[dev]) {
+    CK(cudaFuncSetAttribute(q_fallback_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, QFB_SMEM_BYTES));
+    done[dev] = true;
+  }
+  return PF_OK;
+}
+
+// One full wave of the fallback histogram kernel (a partial second wave
+// would cost a whole pass's latency for a third of the work).
+int fb_hist_grid(int64_t n) {
+  static int occ = 0;
+  if (!occ) {
+    if (fb_hist_smem() != PF_OK) return 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, q_fallback_hist_kernel, 256, QFB_SMEM_BYTES);
+    if (occ < 1) occ = 1;
+  }
+  return grid_for(n, 256, sm_count() * occ);
+}
+
 // PF_CHAIN_DEBUG: events after each CDF-chain launch (resident diagnostics)
 std::vector<cudaEvent_t>* g_chain_rec = nullptr;
 void chain_mark(cudaStream_t st) {
@@ -1052,7 +1077,8 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
           // misses: bounded re-window (attempt 0), whole side (attempt 1)
           for (int attempt = 0; attempt < 2; ++attempt) {
             q_fallback_prep_kernel<<<1, 32, 0, ss>>>(qa, attempt, e->fail.p);
-            q_fallback_hist_kernel<<<fb_grid, 256, 0, ss>>>(qa, lwp, wsrc.mode, wsrc.M, n, SINGLE, attempt,
+            if ((rc = fb_hist_smem()) != PF_OK) return rc;
+            q_fallback_hist_kernel<<<fb_hist_grid(n), 256, QFB_SMEM_BYTES, ss>>>(qa, lwp, wsrc.mode, wsrc.M, n, SINGLE, attempt,
                                                             e->fail.p);
             q_fallback_select_kernel<<<ntg, 1024, 0, ss>>>(qa, attempt, e->fail.p);
             g_launches.fetch_add(3);

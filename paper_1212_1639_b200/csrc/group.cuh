@@ -394,7 +394,8 @@ int run_group(pf_group* g, const double* y, int64_t T, pf_outputs* out) {
         g_launches.fetch_add(4);
         if (round == 0) {
           for (int attempt = 0; attempt < 2; ++attempt) {
-            q_fallback_prep_kernel<<<1, 32, 0, ss>>>(qa, attempt, e0->fail.p);
+            if ((rc = fb_hist_smem()) != PF_OK) return rc;
+          q_fallback_prep_kernel<<<1, 32, 0, ss>>>(qa, attempt, e0->fail.p);
             for (int s = 0; s < G; ++s) {  // every shard's particles (peer reads)
               pf_engine* e = g->sh[s];
               QArgs q2 = qa;
@@ -405,7 +406,7 @@ int run_group(pf_group* g, const double* y, int64_t T, pf_outputs* out) {
               q2.pbase = s * fb_grid;
               q2.ptotal = G * fb_grid;
               q2.gbase = (uint32_t)((int64_t)s * ns);
-              q_fallback_hist_kernel<<<fb_grid, 256, 0, ss>>>(q2, e->lw.p + (size_t)par * ns, 0, e->mbuf.p + par, ns,
+              q_fallback_hist_kernel<<<fb_grid, 256, QFB_SMEM_BYTES, ss>>>(q2, e->lw.p + (size_t)par * ns, 0, e->mbuf.p + par, ns,
                                                               SINGLE, attempt, e0->fail.p);
             }
             q_fallback_select_kernel<<<ntg, 1024, 0, ss>>>(qa, attempt, e0->fail.p);

@@ -129,9 +129,15 @@ PF_D void window_of(const QTarget& t, double mean, double sd, uint32_t* lo, uint
   *hi = key_ru(c + t.h * sd);
 }
 
+// floor((key - lo) nb / (hi - lo + 1)) for lo <= key <= hi, nb <= 4096, in
+// fp64: the numerator (< 2^44) and denominator (<= 2^32) are exact, and a
+// non-integer quotient (< 2^12) lies at least 2^-32 from an integer -- far
+// beyond the division's 2^-41 absolute rounding -- so the truncation is the
+// exact integer quotient (a 64-bit integer division costs ~4x the issue).
 PF_D uint32_t sub_bin(uint32_t key, uint32_t lo, uint32_t hi, int nb) {
-  const uint64_t span = (uint64_t)(hi - lo) + 1;
-  return (uint32_t)(((uint64_t)(key - lo) * (uint64_t)nb) / span);
+  const double num = (double)(key - lo) * (double)nb;
+  const double den = (double)((uint64_t)(hi - lo) + 1);
+  return (uint32_t)(num / den);
 }
 
 // Exact value of quantity q for particle idx at step t (resolve side).
@@ -941,34 +947,97 @@ __global__ void q_fallback_prep_kernel(QArgs qa, int attempt, const int64_t* fai
 }
 
 // F1: full pass over the particles for targets in fallback: fixed-point
-// histogram of the interval + fp64 weight below it.
+// histogram of the interval + fp64 weight below it.  The first QFB_SMEM_T
+// targets in fallback accumulate in a per-CTA shared-memory histogram
+// (flushed once per CTA): a whole-side interval holds millions of particles,
+// and global atomics on 4096 bins would serialise on them.  A bin is two
+// 32-bit words with an explicit carry (64-bit shared atomics are CAS loops
+// on this architecture; 32-bit adds are native): the low word's adder that
+// wraps it adds the carry to the high word, so the pair holds the exact
+// 64-bit sum.  Integer sums: the same bins in any order.
+constexpr int QFB_SMEM_T = 2;
+constexpr int QFB_SMEM_BYTES = QFB_SMEM_T * Q_FB * 8;
 __global__ void __launch_bounds__(256)
 q_fallback_hist_kernel(QArgs qa, const double* __restrict__ lw, int wmode, const double* Mp, int64_t n,
                        int single, int attempt, const int64_t* fail) {
   if (*fail || !qa.sh->fb_active[attempt]) return;
   __shared__ uint32_t ilo[Q_MAXT], ihi[Q_MAXT];
-  __shared__ int act[Q_MAXT];
+  __shared__ int act[Q_MAXT], tq[Q_MAXT], slot[Q_MAXT];
   __shared__ bool last;
-  if (threadIdx.x < qa.ntarget) {
-    const QTarget& t = qa.tg[threadIdx.x];
-    act[threadIdx.x] = t.status == QS_FB;
-    ilo[threadIdx.x] = t.ilo;
-    ihi[threadIdx.x] = t.ihi;
+  extern __shared__ uint32_t shist[];  // [QFB_SMEM_T][Q_FB][lo, hi]
+  if (threadIdx.x == 0) {
+    int ns = 0;
+    for (int k = 0; k < Q_MAXT; ++k) {
+      const bool on = k < qa.ntarget && qa.tg[k].status == QS_FB;
+      act[k] = on;
+      tq[k] = on ? qa.tg[k].q : 0;
+      ilo[k] = on ? qa.tg[k].ilo : 0u;
+      ihi[k] = on ? qa.tg[k].ihi : 0u;
+      slot[k] = (on && ns < QFB_SMEM_T) ? ns++ : -1;
+    }
   }
+  for (int i = threadIdx.x; i < 2 * QFB_SMEM_T * Q_FB; i += blockDim.x) shist[i] = 0u;
   __syncthreads();
   const double M = wmode == 0 ? *Mp : 0.0;
   double acc[Q_MAXT];
+#pragma unroll
   for (int k = 0; k < Q_MAXT; ++k) acc[k] = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double w = wmode == 0 ? exp(lw[i] - M) : lw[i];
-    if (single) w = (double)(float)w;
-    for (int k = 0; k < qa.ntarget; ++k) {
+  // FU particles per thread per iteration with all their loads issued up
+  // front (memory-level parallelism); each thread still visits its particles
+  // in the order i, i + stride, i + 2 stride, ... so the fp64 below-interval
+  // sums are the same as a one-at-a-time loop's.
+  constexpr int FU = 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += FU * stride) {
+    double w[FU];
+    bool ok[FU];
+#pragma unroll
+    for (int u = 0; u < FU; ++u) {
+      const int64_t i = i0 + u * stride;
+      ok[u] = i < n;
+      w[u] = ok[u] ? lw[i] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < FU; ++u) {
+      double x = wmode == 0 ? exp(w[u] - M) : w[u];
+      if (single) x = (double)(float)x;
+      w[u] = ok[u] ? x : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < Q_MAXT; ++k) {
       if (!act[k]) continue;
-      const uint32_t key = qa.keys[qa.tg[k].q][i];
-      if (key < ilo[k]) acc[k] += w;
-      else if (key <= ihi[k])
-        atomicAdd(&qa.fhist[(size_t)k * Q_FB + sub_bin(key, ilo[k], ihi[k], Q_FB)],
-                  (unsigned long long)llrint(w * qa.fx_scale));
+      const uint32_t* kq = qa.keys[tq[k]];
+      uint32_t key[FU];
+#pragma unroll
+      for (int u = 0; u < FU; ++u) key[u] = ok[u] ? kq[i0 + u * stride] : 0xFFFFFFFFu;
+#pragma unroll
+      for (int u = 0; u < FU; ++u) {
+        if (!ok[u] || key[u] > ihi[k]) continue;
+        if (key[u] < ilo[k]) {
+          acc[k] += w[u];
+        } else {
+          const unsigned long long v = (unsigned long long)llrint(w[u] * qa.fx_scale);
+          const uint32_t b = sub_bin(key[u], ilo[k], ihi[k], Q_FB);
+          if (slot[k] >= 0) {
+            uint32_t* cell = shist + 2 * (slot[k] * Q_FB + b);
+            const uint32_t vlo = (uint32_t)v;
+            const uint32_t old = atomicAdd(cell, vlo);
+            const uint32_t vhi = (uint32_t)(v >> 32) + (old + vlo < old ? 1u : 0u);
+            if (vhi) atomicAdd(cell + 1, vhi);
+          } else {
+            atomicAdd(&qa.fhist[(size_t)k * Q_FB + b], v);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int k = 0; k < Q_MAXT; ++k) {
+    if (slot[k] < 0) continue;
+    for (int b = threadIdx.x; b < Q_FB; b += blockDim.x) {
+      const uint32_t* cell = shist + 2 * (slot[k] * Q_FB + b);
+      const unsigned long long v = ((unsigned long long)cell[1] << 32) | cell[0];
+      if (v) atomicAdd(&qa.fhist[(size_t)k * Q_FB + b], v);
     }
   }
   // deterministic combine of the below-interval sums
@@ -1053,19 +1122,38 @@ __global__ void __launch_bounds__(256) q_fallback_fill_kernel(QArgs qa, const do
                                                               const double* Mp, int64_t n, int single,
                                                               const int64_t* fail) {
   if (*fail || !qa.sh->fb_active[0]) return;
+  __shared__ int act[Q_MAXT], tq[Q_MAXT];
+  __shared__ uint32_t klo[Q_MAXT], khi[Q_MAXT];
+  if (threadIdx.x < Q_MAXT) {
+    const int k = threadIdx.x;
+    const bool on = k < qa.ntarget && qa.tg[k].status == QS_REFILL;
+    act[k] = on;
+    tq[k] = on ? qa.tg[k].q : 0;
+    klo[k] = on ? qa.tg[k].klo : 1u;
+    khi[k] = on ? qa.tg[k].khi : 0u;
+  }
+  __syncthreads();
   const double M = wmode == 0 ? *Mp : 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    for (int k = 0; k < qa.ntarget; ++k) {
-      QTarget& t = qa.tg[k];
-      if (t.status != QS_REFILL) continue;
-      const uint32_t key = qa.keys[t.q][i];
-      if (key >= t.klo && key <= t.khi) {
+  constexpr int FU = 4;  // particles per thread per iteration, loads up front
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += FU * stride) {
+#pragma unroll
+    for (int k = 0; k < Q_MAXT; ++k) {
+      if (!act[k]) continue;
+      const uint32_t* kq = qa.keys[tq[k]];
+      uint32_t key[FU];
+#pragma unroll
+      for (int u = 0; u < FU; ++u) key[u] = i0 + u * stride < n ? kq[i0 + u * stride] : 0u;
+#pragma unroll
+      for (int u = 0; u < FU; ++u) {
+        const int64_t i = i0 + u * stride;
+        if (i >= n || key[u] < klo[k] || key[u] > khi[k]) continue;
         double w = wmode == 0 ? exp(lw[i] - M) : lw[i];
         if (single) w = (double)(float)w;
-        const uint32_t pos = atomicAdd(&t.count, 1u);
+        const uint32_t pos = atomicAdd(&qa.tg[k].count, 1u);
         if (pos < qa.cap) {
           QCand c;
-          c.key = key;
+          c.key = key[u];
           c.idx = qa.gbase + (uint32_t)i;
           c.w = w;
           qa.cand[(size_t)k * qa.cap + pos] = c;
