@@ -201,14 +201,14 @@ struct ShardOps {
     const size_t draw_smem = ((size_t)ngt * GT_TABLE_DOUBLES + (e->ntab ? NT_TABLE_DOUBLES : 0)) * sizeof(double);
     const size_t step_smem = (FDm ? (size_t)(((draw_smem / 8) + 3) & ~size_t(3)) * 8 : 0) +
                              (size_t)2 * STEP_SB * threads * (sizeof(Rec) + 3 * sizeof(double));
-    static bool attr[8] = {false};
-    if (!attr[MODE]) {
+    static DevOnce attr;
+    if (attr.pending()) {
       CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)((2 * GT_TABLE_DOUBLES + NT_TABLE_DOUBLES + 4) * sizeof(double) +
                                     2 * STEP_SB * FD_THREADS * (sizeof(Rec) + 3 * sizeof(double)))));
       CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(2 * STEP_SB * 256 * (sizeof(Rec) + 3 * sizeof(double)))));
-      attr[MODE] = true;
+      attr.mark();
     }
     int occ = 0;
     if (FDm)

@@ -110,6 +110,24 @@ int grid_for(int64_t n, int block, int cap = 148 * 16) {
   return (int)g;
 }
 
+// Per-device "done" flags for one-time kernel attribute setup: function
+// attributes live in each device's context, so a process that runs engines
+// on several devices must set them on every one.  Set first, mark after
+// (a concurrent caller may set an attribute twice, never launch without it).
+struct DevOnce {
+  std::atomic<bool> done[64] = {};
+  bool pending() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d < 0 || d >= 64 || !done[d].load(std::memory_order_acquire);
+  }
+  void mark() {
+    int d = 0;
+    cudaGetDevice(&d);
+    if (d >= 0 && d < 64) done[d].store(true, std::memory_order_release);
+  }
+};
+
 int sm_count() {
   static int sms = 0;
   if (!sms) {
@@ -216,10 +234,13 @@ int launch_reduce_qr_m(int grid, WSrc src, int R, TQ* tt, TQ* ct, int64_t* fail,
   const size_t smem = (size_t)NQ * (2 * Q_PER + 1) * CLS_THR * sizeof(double);
   auto kern = cdf_reduce_qr_kernel<TQ, QM, false, CLS_THR>;
   static int occ = 0;
-  if (!occ) {
+  static DevOnce attr;
+  if (attr.pending()) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, CLS_THR, smem));
-    if (occ < 1) occ = 1;
+    int o = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, CLS_THR, smem));
+    occ = o < 1 ? 1 : o;
+    attr.mark();
   }
   (void)grid;
   static const int env_grid = [] {
@@ -311,12 +332,10 @@ struct StrataOut {
 // The fallback histogram kernel's shared-memory histograms exceed the 48 KB
 // default: opt in once per device.
 int fb_hist_smem() {
-  static bool done[64] = {false};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev >= 0 && dev < 64 && !done[dev]) {
+  static DevOnce attr;
+  if (attr.pending()) {
     CK(cudaFuncSetAttribute(q_fallback_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, QFB_SMEM_BYTES));
-    done[dev] = true;
+    attr.mark();
   }
   return PF_OK;
 }
@@ -386,11 +405,11 @@ int launch_cdf_tail(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t
   T* nd = (T*)b.node.p;
   T* cr = (T*)b.carry.p;
   const size_t smem = 4 * p.chunks * sizeof(T);
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[sizeof(T) == 8]) {
+  static DevOnce attr_set;
+  if (attr_set.pending()) {
     CK(cudaFuncSetAttribute(cdf_top_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             4 * CDF_MAX_CHUNKS * (int)sizeof(T)));
-    attr_set[sizeof(T) == 8] = true;
+    attr_set.mark();
   }
   if (!top_done) {
     CK(launch_pdl(PDL_K3, cdf_top_kernel<T>, dim3(1), dim3(1024), smem, st, (const T*)ct, p.chunks, nd, cr, total,
@@ -813,8 +832,8 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     CK(e->dgt.ensure(3 * (size_t)n));
   }
   {
-    static bool attr[8] = {false};
-    if (!attr[MODE]) {
+    static DevOnce attr;  // per MODE / TQ instantiation
+    if (attr.pending()) {
       CK(cudaFuncSetAttribute(draws_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)((2 * GT_TABLE_DOUBLES + NT_TABLE_DOUBLES) * sizeof(double))));
       CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -822,7 +841,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
                                     2 * STEP_SB * FD_THREADS * (sizeof(Rec) + 3 * sizeof(double)))));
       CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(2 * STEP_SB * 256 * (sizeof(Rec) + 3 * sizeof(double)))));
-      attr[MODE] = true;
+      attr.mark();
     }
   }
   int occ = 0, docc = 0;
@@ -1061,11 +1080,11 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       vs.learn_t = LT;
       double *ox = e->o_fq.p, *os = e->o_sq.p, *ot = e->o_tq.p;
       const int hgrid = std::max(1, std::min(64, (int)((n / 64 + 255) / 256)));
-      static bool resolve_attr = false;
-      if (!resolve_attr) {
+      static DevOnce resolve_attr;
+      if (resolve_attr.pending()) {
         CK(cudaFuncSetAttribute(q_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 Q_RESOLVE_SMEM));
-        resolve_attr = true;
+        resolve_attr.mark();
       }
       for (int round = 0; round < 2; ++round) {
         q_hist_kernel<<<dim3(hgrid, ntg), 256, 0, ss>>>(qa, e->fail.p, round);

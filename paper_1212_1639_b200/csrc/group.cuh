@@ -380,10 +380,10 @@ int run_group(pf_group* g, const double* y, int64_t T, pf_outputs* out) {
       vs.learn_t = LT;
       double *ox = e0->o_fq.p, *os = e0->o_sq.p, *ot = e0->o_tq.p;
       const int hgrid = std::max(1, std::min(64, (int)((N / 64 + 255) / 256)));
-      static bool resolve_attr = false;
-      if (!resolve_attr) {
+      static DevOnce resolve_attr;
+      if (resolve_attr.pending()) {
         CK(cudaFuncSetAttribute(q_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Q_RESOLVE_SMEM));
-        resolve_attr = true;
+        resolve_attr.mark();
       }
       const int fb_grid = grid_for(ns, 256, sms * 2);
       for (int round = 0; round < 2; ++round) {
