@@ -488,6 +488,10 @@ cdf_expand_kernel(WSrc src, int64_t n, int R, const T* __restrict__ tile_tot,
       uint4* fp = reinterpret_cast<uint4*>(ro.f32 + base);
       fp[0] = make_uint4(fx[0], fx[1], fx[2], fx[3]);
       fp[1] = make_uint4(fx[4], fx[5], fx[6], fx[7]);
+      if (q_out) {  // sharded runs keep q for the boundary lookups
+#pragma unroll
+        for (int i = 0; i < CDF_V; ++i) q_out[base + i] = qv[i];
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < CDF_V; ++i) q_out[base + i] = qv[i];
@@ -945,6 +949,84 @@ PF_D void ancestors_of(const Lookup<TQ>& L, const uint64_t (&w3)[SB], const bool
 #pragma unroll
   for (int b = 0; b < SB; ++b)
     if (ok[b]) anc[b] = cutpoint_lookup<TQ>(L.q, L.cut, L.n, unit_open(w3[b]));
+}
+
+// ------------------------------------------- sharded rank-table lookup ---
+// The rank tables of a sharded run, per shard g: grp over the GLOBAL stratum
+// groups (entries valid only for groups whose 8 strata and closing cut lie
+// in g's stratum range [L_end[g-1], L_end[g]); boundary groups carry pad = 1
+// and take the cut/q walk), fq / f32 over g's own particles.  A lookup reads
+// the owner shard's tables (peer memory when it is another GPU) and counts
+// in the owner's run exactly as ancestor_of does on one device.
+constexpr uint32_t GRP_BOUNDARY = 1u;
+
+struct ShardRank {
+  const Grp* grp[PF_MAX_SHARDS];      // [N / 8] per shard (global groups)
+  const uint8_t* fq[PF_MAX_SHARDS];   // [N / G (+16)] per shard
+  const uint32_t* f32[PF_MAX_SHARDS];
+  int B;                              // 53 - log2(N)
+  int on;
+};
+
+// One thread per global group that intersects this shard's stratum range.
+__global__ void __launch_bounds__(256)
+group_build_shard_kernel(const int32_t* __restrict__ cut, const int64_t* __restrict__ lend, int shard, int G,
+                         int64_t n, Grp* __restrict__ grp, const int64_t* __restrict__ fail) {
+  pdl_wait();
+  if (fail && *fail) return;
+  const int64_t lo = shard ? __ldcg(&lend[shard - 1]) : 0, hi = __ldcg(&lend[shard]);
+  const int64_t g0 = lo / GRP_STRATA, g1 = (hi + GRP_STRATA - 1) / GRP_STRATA;
+  for (int64_t gi = g0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < g1;
+       gi += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = gi * GRP_STRATA;
+    const bool full = s >= lo && (s + GRP_STRATA < hi || (shard == G - 1 && s + GRP_STRATA <= n));
+    Grp r;
+    r.pad = full ? 0u : GRP_BOUNDARY;
+    r.base = GRP_OVERFLOW;
+    r.cum = 0;
+    if (full) {
+      const int32_t* c = cut + s;
+      const uint32_t base = (uint32_t)c[0];
+      uint64_t cum = 0;
+      bool over = false;
+#pragma unroll
+      for (int i = 0; i < GRP_STRATA; ++i) {
+        const uint32_t e = (uint32_t)(c[i + 1] - (int32_t)base);
+        over |= e > 255u;
+        cum |= (uint64_t)(e & 255u) << (8 * i);
+      }
+      r.base = base | (over ? GRP_OVERFLOW : 0u);
+      r.cum = cum;
+    }
+    grp[gi] = r;
+  }
+}
+
+template <typename TQ>
+PF_D int64_t sharded_lookup_rank(const ShardLookup<TQ>& SL, const ShardRank& R, uint64_t w3) {
+  const uint64_t K = ((w3 >> 12) << 1) | 1ull;  // u = K 2^-53
+  const uint64_t s0 = K >> R.B;
+  int g = 0;
+  while (g < SL.G - 1 && __ldcg(&SL.lend[g]) <= (int64_t)s0) ++g;
+  const uint64_t pol = l2_policy_last();
+  const Grp gr = ld_grp(R.grp[g] + s0 / GRP_STRATA, pol);
+  if (gr.pad & GRP_BOUNDARY) return sharded_lookup<TQ>(SL, w3);
+  // the owner's tables, addressed by global particle index
+  const int64_t gb = (int64_t)g << SL.lg;
+  Lookup<TQ> L;
+  L.anc = nullptr;
+  L.q = nullptr;
+  L.cut = SL.cut[g];
+  L.grp = R.grp[g];
+  L.fq = R.fq[g] - gb;
+  L.f32 = R.f32[g] - gb;
+  L.B = R.B;
+  L.n = SL.n;
+  const uint32_t r = (uint32_t)(K & ((1ull << R.B) - 1ull));
+  int64_t first;
+  int cnt;
+  stratum_run(L, gr, s0, first, cnt);
+  return run_count(L, first, cnt, r, pol);
 }
 
 }  // namespace pf

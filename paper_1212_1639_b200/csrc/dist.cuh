@@ -32,6 +32,15 @@ struct pf_shard {
   int32_t* gcut = nullptr;  // full-size cut table, this rank's strata written
   void* gq = nullptr;       // q of this rank's particles
   int64_t* lend = nullptr;  // [PF_MAX_SHARDS]
+  // rank tables (N >= 2^21): grp over the global stratum groups, fq / f32
+  // over this rank's particles
+  bool rank_on = false;
+  Grp* sgrp = nullptr;
+  uint8_t* sfq = nullptr;
+  uint32_t* sf32 = nullptr;
+  std::vector<const Grp*> p_grp;
+  std::vector<const uint8_t*> p_fq;
+  std::vector<const uint32_t*> p_f32;
   // peers' buffers (IPC-mapped; own entries point at local memory)
   std::vector<const int32_t*> p_cut;
   std::vector<const void*> p_q;
@@ -64,8 +73,8 @@ struct pf_shard {
 namespace {
 
 // Exported buffers, in handle order.
-enum { XH_REC0, XH_REC1, XH_CUT, XH_Q, XH_KEYS, XH_LW, XH_MBUF, XH_QTG, XH_QSH, XH_QCAND, XH_QPART, XH_QHIST,
-       XH_QFHIST, XH_QUNRES, XH_COUNT };
+enum { XH_REC0, XH_REC1, XH_CUT, XH_Q, XH_KEYS, XH_LW, XH_MBUF, XH_GRP, XH_FQ, XH_F32, XH_QTG, XH_QSH, XH_QCAND,
+       XH_QPART, XH_QHIST, XH_QFHIST, XH_QUNRES, XH_COUNT };
 
 template <int MODE, typename TQ>
 struct ShardOps {
@@ -259,7 +268,14 @@ struct ShardOps {
       a.slk.cut[h] = s->p_cut[h];
       a.slk.q[h] = (const TQ*)s->p_q[h];
       a.recs[h] = s->p_rec[s->cur][h];
+      if (s->rank_on) {
+        a.srk.grp[h] = s->p_grp[h];
+        a.srk.fq[h] = s->p_fq[h];
+        a.srk.f32[h] = s->p_f32[h];
+      }
     }
+    a.srk.B = 53 - ilog2(c.n);
+    a.srk.on = s->rank_on && t > 1;
     if (FDm) {
       a.dr.n = ns;
       a.dr.t = t;
@@ -355,9 +371,19 @@ struct ShardOps {
     w.src = e->lw.p + (size_t)par * ns;
     w.M = e->mbuf.p + par;
     w.mode = 0;
-    cdf_expand_kernel<TQ, false><<<(int)plan.chunks, CDF_THREADS, 0, e->st>>>(
-        w, N, plan.R, (TQ*)b.tile_tot.p, (TQ*)b.node.p, (TQ*)b.carry.p, (TQ*)b.total.p, (TQ*)s->gq, s->gcut,
-        e->fail.p, RankOut(), (int64_t)s->rank * ns);
+    if (s->rank_on) {
+      RankOut ro{s->gcut, s->sfq, s->sf32, 53 - ilog2(N)};
+      cdf_expand_kernel<TQ, true><<<(int)plan.chunks, CDF_THREADS, 0, e->st>>>(
+          w, N, plan.R, (TQ*)b.tile_tot.p, (TQ*)b.node.p, (TQ*)b.carry.p, (TQ*)b.total.p, (TQ*)s->gq, s->gcut,
+          e->fail.p, ro, (int64_t)s->rank * ns);
+      LAUNCHED();
+      group_build_shard_kernel<<<grid_for(ns / GRP_STRATA, 256, sm_count() * 8), 256, 0, e->st>>>(
+          s->gcut, s->lend, s->rank, s->world, N, s->sgrp, e->fail.p);
+    } else {
+      cdf_expand_kernel<TQ, false><<<(int)plan.chunks, CDF_THREADS, 0, e->st>>>(
+          w, N, plan.R, (TQ*)b.tile_tot.p, (TQ*)b.node.p, (TQ*)b.carry.p, (TQ*)b.total.p, (TQ*)s->gq, s->gcut,
+          e->fail.p, RankOut(), (int64_t)s->rank * ns);
+    }
     LAUNCHED();
     if (s->ntg) {
       QArgs q2 = qargs(s, par);

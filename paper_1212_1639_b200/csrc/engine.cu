@@ -1379,6 +1379,18 @@ RunFn pick_run(int mode) {
 
 }  // namespace
 
+namespace {
+// Sharded runs use per-shard rank tables for N >= 2^21 (the single-device
+// strata threshold: F then fits 32 bits).  PF_SHARD_RANK=0 keeps the cut/q walk.
+bool shard_rank_enabled(int64_t n) {
+  static const int env = [] {
+    const char* v = getenv("PF_SHARD_RANK");
+    return v ? atoi(v) : 1;
+  }();
+  return env != 0 && n >= ((int64_t)1 << STRATA_MIN_LOG2N);
+}
+}  // namespace
+
 #include "group.cuh"
 #include "dist.cuh"
 
@@ -1558,6 +1570,7 @@ int pf_group_create(const pf_config* cfg, int32_t nshards, const int32_t* device
   g->G = G;
   g->ns = n / G;
   g->lg = ilog2(g->ns);
+  g->rank_on = shard_rank_enabled(n);
   for (int s = 0; s < G; ++s) {
     const int d = devices ? devices[s] : 0;
     if (d < 0 || d >= ndev) {
@@ -1610,6 +1623,25 @@ int pf_group_create(const pf_config* cfg, int32_t nshards, const int32_t* device
     g->gcut.push_back(cut);
     g->gq.push_back(q);
     g->lend.push_back(le);
+    {
+      const int32_t nn = (int32_t)n;  // cut[N] = N closes the last group
+      cudaMemcpy(cut + n, &nn, sizeof(nn), cudaMemcpyHostToDevice);
+    }
+    if (g->rank_on) {
+      Grp* gp = nullptr;
+      uint8_t* fq = nullptr;
+      uint32_t* f32 = nullptr;
+      if ((err = cudaMalloc((void**)&gp, (size_t)(n / GRP_STRATA) * sizeof(Grp))) ||
+          (err = cudaMalloc((void**)&fq, (size_t)g->ns + 16)) ||
+          (err = cudaMalloc((void**)&f32, (size_t)g->ns * sizeof(uint32_t)))) {
+        pf_group_destroy(g);
+        return set_err(err == cudaErrorMemoryAllocation ? PF_ERR_OUT_OF_MEMORY : PF_ERR_CUDA,
+                       std::string("shard rank tables: ") + cudaGetErrorString(err));
+      }
+      g->sgrp.push_back(gp);
+      g->sfq.push_back(fq);
+      g->sf32.push_back(f32);
+    }
     cudaEvent_t ev[5];
     for (auto& x : ev) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
     g->evA.push_back(ev[0]);
@@ -1672,6 +1704,11 @@ int pf_group_destroy(pf_group* g) {
     cudaFree(g->gcut[s]);
     cudaFree(g->gq[s]);
     cudaFree(g->lend[s]);
+    if (s < g->sgrp.size()) {
+      cudaFree(g->sgrp[s]);
+      cudaFree(g->sfq[s]);
+      cudaFree(g->sf32[s]);
+    }
     cudaEventDestroy(g->evA[s]);
     cudaEventDestroy(g->evB[s]);
     cudaEventDestroy(g->evC[s]);
@@ -1730,6 +1767,15 @@ int pf_shard_create(const pf_config* cfg, int32_t rank, int32_t world, pf_shard*
       (err = cudaMalloc((void**)&s->xrec, PF_MAX_SHARDS * sizeof(Partial))) ||
       (err = cudaMalloc(&s->xtot, PF_MAX_SHARDS * sizeof(double))) || (err = e->keys.ensure((size_t)6 * s->ns)))
     return fail_alloc(err);
+  {
+    const int32_t nn = (int32_t)n;  // cut[N] = N closes the last stratum group
+    if ((err = cudaMemcpy(s->gcut + n, &nn, sizeof(nn), cudaMemcpyHostToDevice))) return fail_alloc(err);
+  }
+  s->rank_on = shard_rank_enabled(n);
+  if (s->rank_on && ((err = cudaMalloc((void**)&s->sgrp, (size_t)(n / GRP_STRATA) * sizeof(Grp))) ||
+                     (err = cudaMalloc((void**)&s->sfq, (size_t)s->ns + 16)) ||
+                     (err = cudaMalloc((void**)&s->sf32, (size_t)s->ns * sizeof(uint32_t)))))
+    return fail_alloc(err);
   const bool LS = cfg->learn && cfg->learn_sigma2, LT = cfg->learn && cfg->learn_tau2;
   const int ntg = (cfg->track_quantiles ? 3 : 0) + (LS ? 5 : 0) + (LT ? 5 : 0);
   if (rank == 0 && ntg) {
@@ -1755,6 +1801,9 @@ int pf_shard_create(const pf_config* cfg, int32_t rank, int32_t world, pf_shard*
   s->p_keys.assign(world, nullptr);
   s->p_lw.assign(world, nullptr);
   s->p_mbuf.assign(world, nullptr);
+  s->p_grp.assign(world, nullptr);
+  s->p_fq.assign(world, nullptr);
+  s->p_f32.assign(world, nullptr);
   *out = s;
   return PF_OK;
 }
@@ -1763,6 +1812,7 @@ int pf_shard_create(const pf_config* cfg, int32_t rank, int32_t world, pf_shard*
 static void shard_exports(pf_shard* s, void* ptrs[XH_COUNT]) {
   pf_engine* e = s->e;
   void* p[XH_COUNT] = {e->rec[0].p, e->rec[1].p, s->gcut, s->gq, e->keys.p, e->lw.p, e->mbuf.p,
+                       s->sgrp, s->sfq, s->sf32,
                        e->qtg.p, e->qsh.p, e->qcand.p, e->qpart.p, e->qhist.p, e->qfhist.p, e->qunres.p};
   for (int k = 0; k < XH_COUNT; ++k) ptrs[k] = p[k];
 }
@@ -1809,6 +1859,9 @@ int pf_shard_open_peers(pf_shard* s, const void* all_handles) {
     s->p_keys[r] = (const uint32_t*)p[XH_KEYS];
     s->p_lw[r] = (const double*)p[XH_LW];
     s->p_mbuf[r] = (const double*)p[XH_MBUF];
+    s->p_grp[r] = (const Grp*)p[XH_GRP];
+    s->p_fq[r] = (const uint8_t*)p[XH_FQ];
+    s->p_f32[r] = (const uint32_t*)p[XH_F32];
     if (r == 0) {
       s->q_tg = (QTarget*)p[XH_QTG];
       s->q_sh = (QShared*)p[XH_QSH];
@@ -1821,7 +1874,7 @@ int pf_shard_open_peers(pf_shard* s, const void* all_handles) {
   }
   for (int r = 0; r < s->world; ++r)
     if (!s->p_rec[0][r] || !s->p_rec[1][r] || !s->p_cut[r] || !s->p_q[r] || !s->p_keys[r] || !s->p_lw[r] ||
-        !s->p_mbuf[r])
+        !s->p_mbuf[r] || (s->rank_on && (!s->p_grp[r] || !s->p_fq[r] || !s->p_f32[r])))
       return set_err(PF_ERR_VALUE, "missing peer buffer handle (rank " + std::to_string(r) + ")");
   return PF_OK;
 }
@@ -1925,6 +1978,9 @@ int pf_shard_destroy(pf_shard* s) {
   if (s->lend) cudaFree(s->lend);
   if (s->xrec) cudaFree(s->xrec);
   if (s->xtot) cudaFree(s->xtot);
+  if (s->sgrp) cudaFree(s->sgrp);
+  if (s->sfq) cudaFree(s->sfq);
+  if (s->sf32) cudaFree(s->sf32);
   pf_engine_destroy(s->e);
   delete s;
   return PF_OK;

@@ -32,6 +32,12 @@ struct pf_group {
   std::vector<int32_t*> gcut;
   std::vector<void*> gq;
   std::vector<int64_t*> lend;
+  // per shard rank tables (N >= 2^21): grp over the global stratum groups,
+  // fq / f32 over the shard's particles
+  bool rank_on = false;
+  std::vector<Grp*> sgrp;
+  std::vector<uint8_t*> sfq;
+  std::vector<uint32_t*> sf32;
   std::vector<cudaEvent_t> evA, evB, evC, evK, evD;
   cudaEvent_t evM = nullptr;  // shard 0's combine (quantile windows) done
   double last_ms = 0;
@@ -277,7 +283,14 @@ int run_group(pf_group* g, const double* y, int64_t T, pf_outputs* out) {
         a.slk.cut[h] = g->gcut[h];
         a.slk.q[h] = (const TQ*)g->gq[h];
         a.recs[h] = g->sh[h]->rec[cur].p;
+        if (g->rank_on) {
+          a.srk.grp[h] = g->sgrp[h];
+          a.srk.fq[h] = g->sfq[h];
+          a.srk.f32[h] = g->sf32[h];
+        }
       }
+      a.srk.B = 53 - ilog2(N);
+      a.srk.on = g->rank_on && t > 1;
       step_kernel<MODE, TQ><<<step_grid, 256, step_smem, st>>>(a);
       LAUNCHED();
       CK(cudaEventRecord(g->evA[s], st));
@@ -335,9 +348,19 @@ int run_group(pf_group* g, const double* y, int64_t T, pf_outputs* out) {
       w.src = e->lw.p + (size_t)par * ns;
       w.M = e->mbuf.p + par;
       w.mode = 0;
-      cdf_expand_kernel<TQ, false><<<(int)plan.chunks, CDF_THREADS, 0, e->st>>>(
-          w, N, plan.R, (TQ*)b.tile_tot.p, (TQ*)b.node.p, (TQ*)b.carry.p, (TQ*)b.total.p, (TQ*)g->gq[s],
-          g->gcut[s], e->fail.p, RankOut(), (int64_t)s * ns);
+      if (g->rank_on) {
+        RankOut ro{g->gcut[s], g->sfq[s], g->sf32[s], 53 - ilog2(N)};
+        cdf_expand_kernel<TQ, true><<<(int)plan.chunks, CDF_THREADS, 0, e->st>>>(
+            w, N, plan.R, (TQ*)b.tile_tot.p, (TQ*)b.node.p, (TQ*)b.carry.p, (TQ*)b.total.p, (TQ*)g->gq[s],
+            g->gcut[s], e->fail.p, ro, (int64_t)s * ns);
+        LAUNCHED();
+        group_build_shard_kernel<<<grid_for(ns / GRP_STRATA, 256, sms * 8), 256, 0, e->st>>>(
+            g->gcut[s], g->lend[s], s, G, N, g->sgrp[s], e->fail.p);
+      } else {
+        cdf_expand_kernel<TQ, false><<<(int)plan.chunks, CDF_THREADS, 0, e->st>>>(
+            w, N, plan.R, (TQ*)b.tile_tot.p, (TQ*)b.node.p, (TQ*)b.carry.p, (TQ*)b.total.p, (TQ*)g->gq[s],
+            g->gcut[s], e->fail.p, RankOut(), (int64_t)s * ns);
+      }
       LAUNCHED();
       CK(cudaEventRecord(g->evC[s], e->st));
       if (ntg) {

@@ -214,6 +214,7 @@ struct StepArgs {
   int shard;
   DrawArgs dr;           // FD: this step's draws are computed here (tables, seed, u3 out)
   ShardLookup<TQ> slk;   // sharded run (slk.G > 0): cross-shard lookup
+  ShardRank srk;         // sharded run: per-shard rank tables (srk.on)
   const Rec* recs[PF_MAX_SHARDS];  // sharded run: every shard's records of step t-1
 };
 
@@ -453,7 +454,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
       if (a.slk.G > 0) {
 #pragma unroll
         for (int b = 0; b < STEP_SB; ++b)
-          if (ok[b]) anc[b] = sharded_lookup<TQ>(a.slk, w3[b]);
+          if (ok[b]) anc[b] = a.srk.on ? sharded_lookup_rank<TQ>(a.slk, a.srk, w3[b]) : sharded_lookup<TQ>(a.slk, w3[b]);
       } else if (a.lk.anc) {  // baseline resamplers: ancestors precomputed
 #pragma unroll
         for (int b = 0; b < STEP_SB; ++b)

@@ -94,3 +94,12 @@ def test_process_group_nccl_path(gpu, tmp_path):
     d = _launch(tmp_path, 1, "--particles", str(n), "--series-len", str(t_len), "--backend", "nccl", "--runs", "2")
     for r in range(2):
         _check(_single("learning", n, t_len, 5 + r), d, r)
+
+
+def test_process_group_rank_tables(gpu, tmp_path):
+    # N >= 2^21: the ranks' lookups use the per-shard rank tables (owner
+    # shard's grp / fq / f32 through the IPC mappings), boundary groups the
+    # cut / q walk -- still bit-identical to one device.
+    n, t_len = 1 << 21, 6
+    d = _launch(tmp_path, 2, "--particles", str(n), "--series-len", str(t_len))
+    _check(_single("learning", n, t_len, 5), d, 0)
