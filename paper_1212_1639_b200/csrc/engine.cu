@@ -959,6 +959,8 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     a.fail = e->fail.p;
     a.xrec = nullptr;
     a.shard = 0;
+    static const int dbg_identity = getenv("PF_DEBUG_IDENTITY_ANC") ? 1 : 0;  // timing diagnostics only
+    a.dbg_identity = dbg_identity;
     // this step's draws are computed in the step kernel (tables of step t);
     // only the resampling word goes to memory (for step t+1's lookups)
     memset(&a.dr, 0, sizeof(a.dr));

@@ -215,6 +215,7 @@ struct StepArgs {
   DrawArgs dr;           // FD: this step's draws are computed here (tables, seed, u3 out)
   ShardLookup<TQ> slk;   // sharded run (slk.G > 0): cross-shard lookup
   ShardRank srk;         // sharded run: per-shard rank tables (srk.on)
+  int dbg_identity;      // diagnostics only (PF_DEBUG_IDENTITY_ANC): skip the lookup, ancestor = slot
   const Rec* recs[PF_MAX_SHARDS];  // sharded run: every shard's records of step t-1
 };
 
@@ -450,7 +451,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
       ok[b] = jj[b] < a.n;
       anc[b] = jj[b];
     }
-    if (a.t > 1) {
+    if (a.t > 1 && !a.dbg_identity) {
       if (a.slk.G > 0) {
 #pragma unroll
         for (int b = 0; b < STEP_SB; ++b)
