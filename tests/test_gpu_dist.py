@@ -103,3 +103,10 @@ def test_process_group_rank_tables(gpu, tmp_path):
     n, t_len = 1 << 21, 6
     d = _launch(tmp_path, 2, "--particles", str(n), "--series-len", str(t_len))
     _check(_single("learning", n, t_len, 5), d, 0)
+
+
+def test_process_group_degeneracy_raises_on_every_rank(gpu, tmp_path):
+    # the reference's AllWeightsZeroError(step=t) (filtering.py:294-296),
+    # raised identically by every rank (all see the same partial records)
+    d = _launch(tmp_path, 2, "--particles", str(1 << 13), "--kind", "degenerate")
+    assert list(d["steps"]) == [2, 2]

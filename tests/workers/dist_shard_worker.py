@@ -18,7 +18,7 @@ def main():
     ap.add_argument("--backend", default="gloo")
     ap.add_argument("--particles", type=int, default=1 << 14)
     ap.add_argument("--series-len", type=int, default=16)
-    ap.add_argument("--kind", default="learning", choices=["learning", "filter", "single"])
+    ap.add_argument("--kind", default="learning", choices=["learning", "filter", "single", "degenerate"])
     ap.add_argument("--same-gpu", action="store_true")
     ap.add_argument("--runs", type=int, default=1)
     a = ap.parse_args()
@@ -29,6 +29,22 @@ def main():
     rank = dist.get_rank()
     _, y = P.simulate(P.TrendNoiseModel(), a.series_len, P.RngStream(1, P.rng.AUX_STREAM_BASE + 1))
     res = {}
+    if a.kind == "degenerate":
+        # every rank must raise the reference's AllWeightsZeroError(step=2)
+        with P.Backend("cuda", device=dev, process_group=True) as b:
+            try:
+                P.run_particle_filter(P.TrendNoiseModel(sigma2=1e-300, tau2=0.1), [0.0, 1e200], a.particles,
+                                      seed=1, backend=b)
+                step = -1
+            except P.AllWeightsZeroError as e:
+                step = e.step
+        steps = [None] * dist.get_world_size()
+        dist.all_gather_object(steps, step)
+        if rank == 0:
+            np.savez(a.out, steps=np.array(steps))
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     with P.Backend("cuda", device=dev, process_group=True) as b:
         for r in range(a.runs):
             seed = 5 + r
