@@ -16,15 +16,16 @@ far larger than the 126 MB L2, so no explicit flush is needed.
   --impl reference  times the reference's CPU algorithm (oracle port, numpy +
            scipy, all host threads as Backend lanes) on a bounded sample.
 
-Multi-GPU (--gpus N under torchrun, N > 1): ONE filter of --n-shard (default
-2^27, BASELINE configs[3]) particles sharded over the N GPUs, one process per
-GPU (distributed.py / pf_shard_*): per step an NCCL all-gather of one partial
-record and one subtree total per rank plus one barrier, all enqueued on the
-engine's stream, and cross-rank resampling reads through CUDA IPC (NVLink
-P2P).  value = N*T*K / max over ranks of the device time.  Total work is
-fixed as N grows: scaling "strong".  --multi replicas instead runs an
-independent N-particle filter per rank (weak scaling).  --shards G runs G
-shards on one GPU from one process (pf_group_*, the same sharded kernels).
+Multi-GPU (--gpus N under torchrun, N > 1): ONE filter of --n-shard particles
+(default N x 2^24, so 2^24 per GPU as at N = 1; N = 8 is BASELINE configs[3],
+2^27) sharded over the N GPUs, one process per GPU (distributed.py /
+pf_shard_*): per step an NCCL all-gather of one partial record and one
+subtree total per rank plus one barrier, all enqueued on the engine's stream,
+and cross-rank resampling reads through CUDA IPC (NVLink P2P).  value =
+N_particles*T*K / max over ranks of the device time.  Work per GPU is fixed
+as N grows: scaling "weak" (pass --n-shard for a fixed total, "strong").
+--multi replicas instead runs an independent filter per rank.  --shards G
+runs G shards on one GPU from one process (pf_group_*, the same kernels).
 """
 
 from __future__ import annotations
@@ -204,7 +205,8 @@ def main():
     ap.add_argument("--ref-t", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--multi", default="shard", choices=["shard", "replicas"])
-    ap.add_argument("--n-shard", type=int, default=1 << 27)
+    ap.add_argument("--n-shard", type=int, default=None,
+                    help="particles of the sharded filter (default: world x --n, weak scaling)")
     ap.add_argument("--shards", type=int, default=1)
     ap.add_argument("--process-group", action="store_true",
                     help="run the one-process-per-GPU sharded path even with one rank")
@@ -310,7 +312,8 @@ def run_sharded(args, world, rank, local):
     from paper_1212_1639_b200 import _lib
 
     G = world if world > 1 else args.shards
-    n = args.n_shard if world > 1 else args.n
+    fixed_total = args.n_shard is not None
+    n = (args.n_shard if fixed_total else world * args.n) if world > 1 else args.n
     t_len = args.t
     spmd = world > 1 or args.process_group
     _, y = P.simulate(P.TrendNoiseModel(), t_len, P.RngStream(0, P.rng.AUX_STREAM_BASE + 1))
@@ -353,7 +356,8 @@ def run_sharded(args, world, rank, local):
             "metric": "particle-steps/sec (N*T/s), full particle-learning cycle",
             "value": n * t_len * args.steps / (tot_ms / 1e3), "unit": "particle-steps/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if (world > 1 and fixed_total) else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": f"PL trend+noise, Priors(), cutpoint, N=2^{n.bit_length() - 1} sharded "
                                    f"over {G} shards, T={t_len}, seed 0, track_quantiles=False",
