@@ -204,6 +204,9 @@ int pf_shard_begin(pf_shard* s, const double* y, int64_t t_len, pf_outputs* out)
 int pf_shard_phase(pf_shard* s, int32_t phase, int64_t t);
 int pf_shard_finish(pf_shard* s);
 int pf_shard_last_timing(pf_shard* s, double* total_ms);
+/* Unmap the peers' buffers.  Every rank should call it, then meet at a
+ * barrier, before any rank destroys (frees what its peers mapped). */
+int pf_shard_close_peers(pf_shard* s);
 int pf_shard_destroy(pf_shard* s);
 
 /* ------------------------------------------------- kernel level (L2) --- */

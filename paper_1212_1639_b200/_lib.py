@@ -110,6 +110,7 @@ SIGNATURES = {
     "pf_shard_phase": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64]),
     "pf_shard_finish": (C.c_int, [C.c_void_p]),
     "pf_shard_last_timing": (C.c_int, [C.c_void_p, _dp]),
+    "pf_shard_close_peers": (C.c_int, [C.c_void_p]),
     "pf_shard_destroy": (C.c_int, [C.c_void_p]),
     "pf_philox_block": (C.c_int, [C.c_uint64, _u64p, C.c_int64, C.c_uint64, _u64p]),
     "pf_philox4x64": (C.c_int, [_u64p, _u64p, C.c_int64, _u64p]),

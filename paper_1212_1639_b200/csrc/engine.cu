@@ -1970,6 +1970,15 @@ int pf_shard_last_timing(pf_shard* s, double* total_ms) {
   return PF_OK;
 }
 
+int pf_shard_close_peers(pf_shard* s) {
+  if (!s) return PF_OK;
+  cudaSetDevice(s->cfg.device);
+  if (s->e && s->e->st) cudaStreamSynchronize(s->e->st);
+  for (void* p : s->opened) cudaIpcCloseMemHandle(p);
+  s->opened.clear();
+  return PF_OK;
+}
+
 int pf_shard_destroy(pf_shard* s) {
   if (!s) return PF_OK;
   cudaSetDevice(s->cfg.device);

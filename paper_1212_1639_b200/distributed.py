@@ -251,7 +251,15 @@ class ShardRank:
         return {"total_ms": tot.value}
 
     def close(self):
+        """Unmap the peers, meet the other ranks, then free: no rank frees
+        memory a peer still maps."""
         if self.h:
+            self.lib.pf_shard_close_peers(self.h)
+            try:
+                if self.dist.is_initialized():
+                    self.dist.barrier(group=self.group)
+            except Exception:  # noqa: BLE001 -- teardown after a failed peer: free anyway
+                pass
             self.lib.pf_shard_destroy(self.h)
             self.h = C.c_void_p()
 
