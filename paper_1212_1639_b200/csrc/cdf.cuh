@@ -474,7 +474,16 @@ cdf_expand_kernel(WSrc src, int64_t n, int R, const T* __restrict__ tile_tot,
       qv[i] = qi;
       const int64_t L = (int64_t)ceil(qi * nf);
       int32_t* ct = STRATA ? ro.cut : cut_out;
-      for (int64_t kk = Lprev; kk < L; ++kk) ct[kk] = (int32_t)(gbase + base + i);
+      // strata [Lprev, L) start at this particle: usually 0, 1 or 2 of them,
+      // so the first two stores are predicated and only longer runs loop
+      const int32_t v = (int32_t)(gbase + base + i);
+      if (L > Lprev) {
+        ct[Lprev] = v;
+        if (L > Lprev + 1) {
+          ct[Lprev + 1] = v;
+          for (int64_t kk = Lprev + 2; kk < L; ++kk) ct[kk] = v;
+        }
+      }
       if (STRATA) {
         const uint32_t f = strata_f<T>(qi, L, unitB);
         fx[i] = f;
