@@ -259,6 +259,7 @@ struct ShardOps {
     a.out.t_sd = e->o_tsd.p;
     a.fail = e->fail.p;
     a.xrec = s->xrec;
+    a.ref_slack = 64.0;
     a.shard = s->rank;
     a.slk.G = s->world;
     a.slk.lg = s->lg;

@@ -961,6 +961,11 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     a.shard = 0;
     static const int dbg_identity = getenv("PF_DEBUG_IDENTITY_ANC") ? 1 : 0;  // timing diagnostics only
     a.dbg_identity = dbg_identity;
+    static const double ref_slack = [] {
+      const char* v = getenv("PF_MOMENT_SLACK");
+      return v ? atof(v) : 64.0;
+    }();
+    a.ref_slack = ref_slack;
     // this step's draws are computed in the step kernel (tables of step t);
     // only the resampling word goes to memory (for step t+1's lookups)
     memset(&a.dr, 0, sizeof(a.dr));

@@ -274,6 +274,7 @@ int run_group(pf_group* g, const double* y, int64_t T, pf_outputs* out) {
       a.out.t_sd = e->o_tsd.p;
       a.fail = e->fail.p;
       a.xrec = g->xrec;
+      a.ref_slack = 64.0;
       a.shard = s;
       a.slk.G = G;
       a.slk.lg = g->lg;

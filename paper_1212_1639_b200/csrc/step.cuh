@@ -216,6 +216,7 @@ struct StepArgs {
   ShardLookup<TQ> slk;   // sharded run (slk.G > 0): cross-shard lookup
   ShardRank srk;         // sharded run: per-shard rank tables (srk.on)
   int dbg_identity;      // diagnostics only (PF_DEBUG_IDENTITY_ANC): skip the lookup, ancestor = slot
+  double ref_slack;      // moment-reference slack (64; 0 = rescale at every new max)
   const Rec* recs[PF_MAX_SHARDS];  // sharded run: every shard's records of step t-1
 };
 
@@ -410,7 +411,12 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
   if (*a.fail) return;
   const bool feedw = a.feed_w != nullptr;
   const double cs = a.sc->cs, ct = a.sc->ct, cx = a.sc->cx;
+  // m: reference of this thread's moment sums (moved, with a rescale, only
+  // when a log-weight exceeds it by more than ref_slack = 64 -- e <= e^64
+  // keeps the fp64 sums far from overflow); mx: the true running max, the
+  // step's M.
   double m = feedw ? 0.0 : -INFINITY;
+  double mx = m;
   double s0 = 0, sx = 0, s2x = 0, s1s = 0, s2s = 0, s1t = 0, s2t = 0;
   bool bad = false;
 
@@ -560,7 +566,8 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
     } else {
       a.lw[j] = lw;
       if (!(lw == lw) || lw == INFINITY) bad = true;
-      if (lw > m) {
+      if (lw > mx) mx = lw;
+      if (lw > m + a.ref_slack) {
         const double sc = exp(m - lw);
         s0 *= sc; sx *= sc; s2x *= sc; s1s *= sc; s2s *= sc; s1t *= sc; s2t *= sc;
         m = lw;
@@ -596,7 +603,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
   __shared__ double mblk;
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double wm = warp_max(m);
+  double wm = warp_max(mx);
   if (lane == 0) red[warp][0] = wm;
   __syncthreads();
   if (threadIdx.x == 0) {
