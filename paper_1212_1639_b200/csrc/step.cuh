@@ -30,6 +30,10 @@ constexpr double LOG_TWO_PI = 1.8378770664093453;  // math.log(2*math.pi), model
 #define PF_FD_THREADS 512
 #endif
 constexpr int STEP_SB = PF_STEP_SB;  // slots per thread per pipeline stage (double buffered)
+// STEP_SB = 1 builds (tried with 512 and 768-thread CTAs) report an
+// out-of-range shared address in the fused draws under compute-sanitizer;
+// the cause is not understood, so they are refused rather than shipped.
+static_assert(STEP_SB >= 2, "STEP_SB = 1 is unsupported (fails memcheck in the fused draws)");
 constexpr int FD_THREADS = PF_FD_THREADS;  // CTA width of the fused-draws step kernel
 
 // Order-preserving 32-bit image of a double (float32 rounded down, sign
