@@ -43,6 +43,9 @@ enum { PF_DTYPE_F64 = 0, PF_DTYPE_F32 = 1 };
 /* ------------------------------------------------------------ library --- */
 const char* pf_version(void);
 const char* pf_last_error_message(void);
+/* sizeof(pf_config), sizeof(pf_outputs), sizeof(pf_feed) as compiled into
+ * the library: lets a binding check its struct mirrors (no device needed). */
+int pf_abi_sizes(int64_t* sizes3);
 int64_t pf_last_error_step(void);
 /* Number of visible CUDA devices (0 on a host without a GPU; never fails). */
 int pf_device_count(void);
@@ -127,6 +130,10 @@ typedef struct pf_outputs {
    * resample_sort_only, propagate, store, other (nanoseconds) */
   int64_t phase_ns[7];
   int64_t failed_step;          /* step of AllWeightsZeroError, else 0 */
+  /* [T] effective sample size (sum w)^2 / sum w^2 of the pre-resample weights
+   * (an extension: the reference reports no ESS); reduced with the other
+   * per-shard sums in sharded runs */
+  double* ess;
 } pf_outputs;
 
 typedef struct pf_engine pf_engine;
@@ -149,6 +156,12 @@ int pf_engine_last_timing(pf_engine* e, double* total_ms, double* step_kernel_ms
  * a truncated candidate set (should be 0), [1] window misses that needed
  * the fallback pass, [2] largest candidate list, [3] resolves performed. */
 int pf_engine_quantile_stats(pf_engine* e, int64_t* stats4);
+/* Kernel path the last run took (bit mask): PF_PATH_FUSED_DRAWS -- draws
+ * computed inside the step kernel; PF_PATH_RANK_TABLES -- strata rank-table
+ * lookups (N >= 2^21); PF_PATH_FUSED_TOP -- top tree in K2's last CTA.
+ * Lets parity tests assert they covered the benchmarked path. */
+enum { PF_PATH_FUSED_DRAWS = 1, PF_PATH_RANK_TABLES = 2, PF_PATH_FUSED_TOP = 4 };
+int pf_engine_last_path(pf_engine* e, int32_t* flags);
 int pf_engine_destroy(pf_engine* e);
 
 /* ----------------------------------------- sharded run (multi-GPU) --- */

@@ -75,6 +75,7 @@ class PfOutputs(C.Structure):
         ("hist_a_sigma", _dp), ("hist_b_sigma", _dp), ("hist_a_tau", _dp),
         ("hist_b_tau", _dp),
         ("phase_ns", C.c_int64 * 7), ("failed_step", C.c_int64),
+        ("ess", _dp),
     ]
 
 
@@ -82,6 +83,7 @@ class PfOutputs(C.Structure):
 SIGNATURES = {
     "pf_version": (C.c_char_p, []),
     "pf_last_error_message": (C.c_char_p, []),
+    "pf_abi_sizes": (C.c_int, [_i64p]),
     "pf_last_error_step": (C.c_int64, []),
     "pf_device_count": (C.c_int, []),
     "pf_launch_count": (C.c_int64, []),
@@ -91,6 +93,7 @@ SIGNATURES = {
     "pf_engine_run_resident": (C.c_int, [C.c_void_p, C.c_int64]),
     "pf_engine_last_timing": (C.c_int, [C.c_void_p, _dp, _dp, _i64p, _i64p]),
     "pf_engine_quantile_stats": (C.c_int, [C.c_void_p, _i64p]),
+    "pf_engine_last_path": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
     "pf_engine_destroy": (C.c_int, [C.c_void_p]),
     "pf_group_create": (C.c_int, [C.POINTER(PfConfig), C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_void_p)]),
     "pf_group_reconfigure": (C.c_int, [C.c_void_p, C.POINTER(PfConfig)]),

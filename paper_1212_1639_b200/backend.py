@@ -76,6 +76,7 @@ class Backend:
             self.rank = dist.get_rank(self.process_group)
         self.distributed = process_group is not None and process_group is not False
         self._engines = {}
+        self._pool = None
 
     def split(self, n):
         """Contiguous lane ranges covering [0, n) (backend.py:39-50)."""
@@ -89,6 +90,27 @@ class Backend:
             lo = hi
         return out
 
+    def run(self, n, fn):
+        """Invoke ``fn(lo, hi)`` over disjoint ranges covering [0, n)
+        (backend.py:52-70): the host-side seam reference callers drive
+        directly.  Returns only once every lane has finished (the phase
+        barrier), and re-raises a lane's exception.  ``fn`` is the caller's
+        own host code; the device engines never go through it."""
+        if n <= 0:
+            return
+        ranges = self.split(n)
+        if self.mode != "parallel" or len(ranges) == 1:
+            for lo, hi in ranges:
+                fn(lo, hi)
+            return
+        if self._pool is None:
+            from concurrent.futures import ThreadPoolExecutor
+
+            self._pool = ThreadPoolExecutor(max_workers=self.lanes)
+        futures = [self._pool.submit(fn, lo, hi) for lo, hi in ranges]
+        for f in futures:
+            f.result()  # waits for every lane; re-raises lane exceptions in order
+
     def engine(self, key, factory):
         """The cached engine for ``key`` (created by ``factory()`` once)."""
         eng = self._engines.get(key)
@@ -101,6 +123,9 @@ class Backend:
         for eng in self._engines.values():
             eng.close()
         self._engines.clear()
+        if self._pool is not None:
+            self._pool.shutdown(wait=True)
+            self._pool = None
 
     def __enter__(self):
         return self
@@ -110,8 +135,14 @@ class Backend:
         return False
 
     def __del__(self):
+        # garbage collection runs at different times on different ranks: no
+        # collective teardown here (ShardRank.release is rank-local)
         try:
-            self.close()
+            for eng in self._engines.values():
+                (getattr(eng, "release", None) or eng.close)()
+            self._engines.clear()
+            if self._pool is not None:
+                self._pool.shutdown(wait=False)
         except Exception:
             pass
 

@@ -93,6 +93,7 @@ struct ShardOps {
     const size_t TT = (size_t)(T > 0 ? T : 1);
     if ((rc = build_tables(e, T)) != PF_OK) return rc;
     CK(e->o_fm.ensure(TT));
+    CK(e->o_ess.ensure(TT));
     if (LS) { CK(e->o_sm.ensure(TT)); CK(e->o_ssd.ensure(TT)); CK(e->o_sq.ensure(TT * 5)); }
     if (LT) { CK(e->o_tm.ensure(TT)); CK(e->o_tsd.ensure(TT)); CK(e->o_tq.ensure(TT * 5)); }
     // the quantile state was sized (and exported) at create from the config
@@ -257,6 +258,7 @@ struct ShardOps {
     a.out.s_sd = e->o_ssd.p;
     a.out.t_mean = e->o_tm.p;
     a.out.t_sd = e->o_tsd.p;
+    a.out.ess = nullptr;  // sharded: the combine kernel writes it
     a.fail = e->fail.p;
     a.xrec = s->xrec;
     a.ref_slack = 64.0;
@@ -316,6 +318,7 @@ struct ShardOps {
     so.s_sd = e->o_ssd.p;
     so.t_mean = e->o_tm.p;
     so.t_sd = e->o_tsd.p;
+    so.ess = e->o_ess.p;
     double* qmom = (s->rank == 0 && s->ntg) ? &(s->q_sh + par)->mean[0] : nullptr;
     combine_kernel<MODE><<<1, 256, 0, e->st>>>(s->xrec, s->world, t, 0, so, qmom, e->sc.p, e->mbuf.p + par,
                                                e->fail.p);
@@ -467,7 +470,20 @@ struct ShardOps {
         g_launches.fetch_add(s->world);
       }
     }
-    q_select_kernel<<<ntg, 1024, 0, ss>>>(qa, vs, e->qscratch.p, ox, os, ot, t, e->fail.p, e->qunres.p);
+    QAll all;
+    memset(&all, 0, sizeof(all));
+    all.nsrc = s->world;
+    all.ns = ns;
+    for (int h = 0; h < s->world; ++h) {  // every rank's particles (IPC reads)
+      const uint32_t* kb = s->p_keys[h] + (size_t)par * 3 * ns;
+      all.keys[h][0] = s->want_fq ? kb : nullptr;
+      all.keys[h][1] = LS ? kb + ns : nullptr;
+      all.keys[h][2] = LT ? kb + 2 * (size_t)ns : nullptr;
+      all.lw[h] = s->p_lw[h] + (size_t)par * ns;
+      all.M[h] = s->p_mbuf[h] + par;
+    }
+    all.single = SINGLE;
+    q_select_kernel<<<ntg, 1024, 0, ss>>>(qa, vs, e->qscratch.p, ox, os, ot, t, e->fail.p, s->q_unres, all);
     q_step_end_kernel<<<1, 1024, 0, ss>>>(qa, 1);
     g_launches.fetch_add(2);
     return PF_OK;
@@ -503,8 +519,8 @@ struct ShardOps {
       m.learn_t = LT;
       m.sigma2_fixed = c.sigma2_fixed;
       m.tau2_fixed = c.tau2_fixed;
-      m.a_s = shape_at(c, true, T);
-      m.a_t = shape_at(c, false, T);
+      m.a_s = shape_at(e, true, T);
+      m.a_t = shape_at(e, false, T);
       m.idx = keep_idx ? e->idx.p : nullptr;
       double* dst[7] = {out->final_states, out->final_sigma2, out->final_tau2, out->final_a_sigma,
                         out->final_b_sigma, out->final_a_tau, out->final_b_tau};
@@ -533,6 +549,7 @@ struct ShardOps {
       };
       int rc;
       if ((rc = cp(out->filtered_mean, e->o_fm, T)) != PF_OK) return rc;
+    if (out->ess && (rc = cp(out->ess, e->o_ess, T)) != PF_OK) return rc;
       if (s->want_fq && (rc = cp(out->filtered_quantiles, e->o_fq, T * 3)) != PF_OK) return rc;
       if (LS && ((rc = cp(out->sigma2_mean, e->o_sm, T)) || (rc = cp(out->sigma2_sd, e->o_ssd, T)) ||
                  (rc = cp(out->sigma2_quantiles, e->o_sq, T * 5))))
@@ -558,6 +575,7 @@ struct ShardOps {
       return set_err(PF_ERR_ALL_WEIGHTS_ZERO, "all particle weights are zero (at time step " + std::to_string(f) + ")",
                      f);
     if (f < 0) return set_err(PF_ERR_ALL_WEIGHTS_ZERO, "all particle weights are zero", 0);
+    if (s->rank == 0 && s->ntg) return check_quantile_unresolved(s->q_unres);
     return PF_OK;
   }
 };

@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <deque>
 #include <mutex>
 #include <cmath>
 #include <cstdio>
@@ -486,13 +487,14 @@ struct pf_engine {
   DevBuf<int64_t> fail;
   CdfBufs cdf;
   // per-run outputs (device)
-  DevBuf<double> o_fm, o_sm, o_ssd, o_tm, o_tsd, o_fq, o_sq, o_tq;
+  DevBuf<double> o_fm, o_sm, o_ssd, o_tm, o_tsd, o_fq, o_sq, o_tq, o_ess;
   DevBuf<double> probs;  // [0..5) param probs, [5..8) state probs
   // gamma tables for the shape schedule a0 + t/2, t = 0..T
   const double* tab_s = nullptr;  // cached per-step gamma tables (not owned)
   const double* tab_t = nullptr;
-  const std::vector<double>* sh_s = nullptr;
-  const std::vector<double>* sh_t = nullptr;
+  // a_t = a0 + t/2 for t = 0..T, accumulated as the reference does
+  // (a = a + 0.5 per step, filtering.py:279,285), rebuilt once per run
+  std::vector<double> sched_s, sched_t;
   // materialise scratch
   DevBuf<double> m_x, m_s2, m_t2, m_as, m_bs, m_at, m_bt;
   DevBuf<double> feed_buf;
@@ -502,10 +504,28 @@ struct pf_engine {
   double last_total_ms = 0, last_step_ms = 0;
   int64_t qstats[4] = {0, 0, 0, 0};  // quantile: unresolved, fallbacks, max candidates, resolves
   int64_t last_step_launches = 0, last_kernels = 0;
+  int32_t last_path = 0;  // PF_PATH_* of the last run
   std::vector<double> y_host;
 };
 
 namespace {
+
+// A weighted-quantile target that could not be selected exactly (its window
+// held more candidates than the list and no full-particle source was given):
+// never returned silently.
+int quantile_unresolved_error(int64_t count) {
+  return set_err(PF_ERR_CUDA, "weighted quantile unresolved for " + std::to_string(count) +
+                                  " target-step(s): candidate window overflow");
+}
+
+// Read the unresolved counter of a quantile state after the side stream has
+// drained (group and process-group runs; the single engine reads all four).
+int check_quantile_unresolved(const unsigned int* stats) {
+  if (!stats) return PF_OK;
+  unsigned int u = 0;
+  CK(cudaMemcpy(&u, stats, sizeof(u), cudaMemcpyDeviceToHost));
+  return u ? quantile_unresolved_error(u) : PF_OK;
+}
 
 // Process-wide cache of per-step inverse-gamma tables, keyed by (device,
 // prior shape).  The schedule a0, a0+1/2, ... is a prefix-closed sequence, so
@@ -517,7 +537,7 @@ struct TableEntry {
   std::vector<double> shapes;
   double* tab;
 };
-std::vector<TableEntry> g_tables;
+std::deque<TableEntry> g_tables;  // deque: entries never move (engines keep pointers into them)
 std::mutex g_tables_mu;
 
 int cached_table(int device, double a0, int64_t T, cudaStream_t st, const TableEntry** out) {
@@ -584,10 +604,18 @@ int cached_ntab(int device, cudaStream_t st, const double** out) {
   return PF_OK;
 }
 
+void shape_schedule(std::vector<double>& out, double a0, int64_t T) {
+  out.resize((size_t)T + 1);
+  double a = a0;
+  out[0] = a;
+  for (int64_t t = 1; t <= T; ++t) out[(size_t)t] = (a = a + 0.5);
+}
+
 int build_tables(pf_engine* e, int64_t T) {
   e->tab_s = e->tab_t = nullptr;
-  e->sh_s = e->sh_t = nullptr;
   e->ntab = nullptr;
+  shape_schedule(e->sched_s, e->cfg.sigma2_shape, T);
+  shape_schedule(e->sched_t, e->cfg.tau2_shape, T);
   if (e->cfg.gamma_method != 0) return PF_OK;
   {
     int rc = cached_ntab(e->cfg.device, e->st, &e->ntab);
@@ -599,31 +627,34 @@ int build_tables(pf_engine* e, int64_t T) {
   if (ls) {
     if ((rc = cached_table(e->cfg.device, e->cfg.sigma2_shape, T, e->st, &te)) != PF_OK) return rc;
     e->tab_s = te->tab;
-    e->sh_s = &te->shapes;
   }
   if (lt) {
     if ((rc = cached_table(e->cfg.device, e->cfg.tau2_shape, T, e->st, &te)) != PF_OK) return rc;
     e->tab_t = te->tab;
-    e->sh_t = &te->shapes;
   }
   return PF_OK;
+}
+
+// Step t's shape, O(1) from the run's schedule (t <= T of the last
+// build_tables; longer t only for callers outside a run).
+double sched_at(const std::vector<double>& sc, double a0, int64_t t) {
+  if (t >= 0 && (size_t)t < sc.size()) return sc[(size_t)t];
+  double a = a0;
+  for (int64_t k = 0; k < t; ++k) a = a + 0.5;
+  return a;
 }
 
 GammaSrc gamma_src(pf_engine* e, bool sigma, int64_t t) {
   GammaSrc g;
   g.method = e->cfg.gamma_method;
-  double a = sigma ? e->cfg.sigma2_shape : e->cfg.tau2_shape;
-  for (int64_t k = 0; k < t; ++k) a = a + 0.5;
-  g.shape = a;
+  g.shape = sigma ? sched_at(e->sched_s, e->cfg.sigma2_shape, t) : sched_at(e->sched_t, e->cfg.tau2_shape, t);
   const double* base = sigma ? e->tab_s : e->tab_t;
   g.table = base ? base + (size_t)t * GT_TABLE_DOUBLES : nullptr;
   return g;
 }
 
-double shape_at(const pf_config& c, bool sigma, int64_t t) {
-  double a = sigma ? c.sigma2_shape : c.tau2_shape;
-  for (int64_t k = 0; k < t; ++k) a = a + 0.5;
-  return a;
+double shape_at(const pf_engine* e, bool sigma, int64_t t) {
+  return sigma ? sched_at(e->sched_s, e->cfg.sigma2_shape, t) : sched_at(e->sched_t, e->cfg.tau2_shape, t);
 }
 
 struct RunSpec {
@@ -657,6 +688,8 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
 
   const size_t TT = (size_t)(T > 0 ? T : 1);
   CK(e->o_fm.ensure(TT));
+  const bool want_ess = out && out->ess;
+  if (want_ess) CK(e->o_ess.ensure(TT));
   if (LS) { CK(e->o_sm.ensure(TT)); CK(e->o_ssd.ensure(TT)); CK(e->o_sq.ensure(TT * 5)); }
   if (LT) { CK(e->o_tm.ensure(TT)); CK(e->o_tsd.ensure(TT)); CK(e->o_tq.ensure(TT * 5)); }
   if (want_fq) CK(e->o_fq.ensure(TT * 3));
@@ -817,12 +850,14 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   // N: a separate draws_kernel on its own stream runs one step ahead, beside
   // the step kernel and the CDF (a short step kernel cannot hide the draws'
   // arithmetic).  PF_FUSED_DRAWS=0/1 overrides.
-  static const int fused_env = [] {
+  const int fused_env = [] {  // read per run (A/B tests switch it in-process)
     const char* v = getenv("PF_FUSED_DRAWS");
     return v ? atoi(v) : -1;
   }();
   const bool fused = c.gamma_method == 0 && e->ntab &&
                      (fused_env >= 0 ? fused_env != 0 : n >= ((int64_t)1 << 22));
+  e->last_path = (fused ? PF_PATH_FUSED_DRAWS : 0) | (e->strata ? PF_PATH_RANK_TABLES : 0) |
+                 (c.resampler == PF_RESAMPLE_CUTPOINT && fuse_top() ? PF_PATH_FUSED_TOP : 0);
   const int STEP_THREADS = fused ? FD_THREADS : 256;
   const size_t step_smem = (fused ? (size_t)(((draw_smem / 8) + 3) & ~size_t(3)) * 8 : 0) +
                            (size_t)2 * STEP_SB * STEP_THREADS * (sizeof(Rec) + 3 * sizeof(double));
@@ -956,6 +991,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     a.out.s_sd = e->o_ssd.p;
     a.out.t_mean = e->o_tm.p;
     a.out.t_sd = e->o_tsd.p;
+    a.out.ess = want_ess ? e->o_ess.p : nullptr;
     a.fail = e->fail.p;
     a.xrec = nullptr;
     a.shard = 0;
@@ -1114,7 +1150,16 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
         }
         g_launches.fetch_add(2);
       }
-      q_select_kernel<<<ntg, 1024, 0, ss>>>(qa, vs, e->qscratch.p, ox, os, ot, t, e->fail.p, e->qunres.p);
+      QAll all;
+      memset(&all, 0, sizeof(all));
+      all.nsrc = 1;
+      all.ns = n;
+      for (int q = 0; q < Q_MAXQ; ++q) all.keys[0][q] = qa.keys[q];
+      all.lw[0] = lwp;
+      all.M[0] = wsrc.M;
+      all.wmode = wsrc.mode;
+      all.single = SINGLE;
+      q_select_kernel<<<ntg, 1024, 0, ss>>>(qa, vs, e->qscratch.p, ox, os, ot, t, e->fail.p, e->qunres.p, all);
       q_step_end_kernel<<<1, 1024, 0, ss>>>(qa, 1);
       g_launches.fetch_add(2);
       CK(cudaEventRecord(e->ev_q[t & 1], ss));
@@ -1144,8 +1189,8 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       m.learn_t = LT;
       m.sigma2_fixed = c.sigma2_fixed;
       m.tau2_fixed = c.tau2_fixed;
-      m.a_s = shape_at(c, true, t);
-      m.a_t = shape_at(c, false, t);
+      m.a_s = shape_at(e, true, t);
+      m.a_t = shape_at(e, false, t);
       m.idx = nullptr;
       size_t off = (size_t)(t - 1) * n;
       CK(e->m_x.ensure(n)); CK(e->m_s2.ensure(n)); CK(e->m_t2.ensure(n)); CK(e->m_as.ensure(n));
@@ -1187,8 +1232,8 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     m.learn_t = LT;
     m.sigma2_fixed = c.sigma2_fixed;
     m.tau2_fixed = c.tau2_fixed;
-    m.a_s = shape_at(c, true, T);
-    m.a_t = shape_at(c, false, T);
+    m.a_s = shape_at(e, true, T);
+    m.a_t = shape_at(e, false, T);
     m.idx = keep_idx ? e->idx.p : nullptr;
     m.x = keep_final ? out->final_states : nullptr;
     m.fail = e->fail.p;
@@ -1256,6 +1301,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       return PF_OK;
     };
     if ((rc = cp(out->filtered_mean, e->o_fm, T)) != PF_OK) return rc;
+    if (want_ess && (rc = cp(out->ess, e->o_ess, T)) != PF_OK) return rc;
     if (want_fq && (rc = cp(out->filtered_quantiles, e->o_fq, T * 3)) != PF_OK) return rc;
     if (LS) {
       if ((rc = cp(out->sigma2_mean, e->o_sm, T)) || (rc = cp(out->sigma2_sd, e->o_ssd, T)) ||
@@ -1365,6 +1411,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     return set_err(PF_ERR_ALL_WEIGHTS_ZERO, "all particle weights are zero (at time step " +
                                              std::to_string(fail_h) + ")", fail_h);
   if (fail_h < 0) return set_err(PF_ERR_ALL_WEIGHTS_ZERO, "all particle weights are zero", 0);
+  if (e->qstats[0] > 0) return quantile_unresolved_error(e->qstats[0]);
   return PF_OK;
 }
 
@@ -1406,6 +1453,13 @@ extern "C" {
 
 const char* pf_version(void) { return "parsmc-b200 0.1.0 (sm_100a)"; }
 const char* pf_last_error_message(void) { return g_msg.c_str(); }
+int pf_abi_sizes(int64_t* sizes3) {
+  if (!sizes3) return set_err(PF_ERR_VALUE, "null sizes");
+  sizes3[0] = (int64_t)sizeof(pf_config);
+  sizes3[1] = (int64_t)sizeof(pf_outputs);
+  sizes3[2] = (int64_t)sizeof(pf_feed);
+  return PF_OK;
+}
 int64_t pf_last_error_step(void) { return g_step; }
 int64_t pf_launch_count(void) { return g_launches.load(); }
 
@@ -2018,12 +2072,18 @@ int pf_engine_last_timing(pf_engine* e, double* total_ms, double* step_kernel_ms
   return PF_OK;
 }
 
+int pf_engine_last_path(pf_engine* e, int32_t* flags) {
+  if (!e || !flags) return set_err(PF_ERR_VALUE, "null engine or flags");
+  *flags = e->last_path;
+  return PF_OK;
+}
+
 int pf_engine_destroy(pf_engine* e) {
   if (!e) return PF_OK;
   cudaSetDevice(e->cfg.device);
   if (e->st) cudaStreamSynchronize(e->st);
   DevBuf<double>* bufs[] = {&e->lw, &e->s2init, &e->o_fm, &e->o_sm, &e->o_ssd,
-                            &e->o_tm, &e->o_tsd, &e->o_fq, &e->o_sq, &e->o_tq, &e->probs, &e->m_x, &e->m_s2, &e->m_t2, &e->m_as,
+                            &e->o_tm, &e->o_tsd, &e->o_fq, &e->o_sq, &e->o_tq, &e->o_ess, &e->probs, &e->m_x, &e->m_s2, &e->m_t2, &e->m_as,
                             &e->m_bs, &e->m_at, &e->m_bt, &e->feed_buf};
   for (auto* b : bufs) b->release();
   e->rec[0].release();

@@ -73,6 +73,7 @@ int run_group(pf_group* g, const double* y, int64_t T, pf_outputs* out) {
     if ((rc = set_device(g->dev[s])) != PF_OK) return rc;
     if ((rc = build_tables(e, T)) != PF_OK) return rc;
     CK(e->o_fm.ensure(TT));
+    CK(e->o_ess.ensure(TT));
     if (LS) { CK(e->o_sm.ensure(TT)); CK(e->o_ssd.ensure(TT)); CK(e->o_sq.ensure(TT * 5)); }
     if (LT) { CK(e->o_tm.ensure(TT)); CK(e->o_tsd.ensure(TT)); CK(e->o_tq.ensure(TT * 5)); }
     if (want_fq) CK(e->o_fq.ensure(TT * 3));
@@ -272,6 +273,7 @@ int run_group(pf_group* g, const double* y, int64_t T, pf_outputs* out) {
       a.out.s_sd = e->o_ssd.p;
       a.out.t_mean = e->o_tm.p;
       a.out.t_sd = e->o_tsd.p;
+      a.out.ess = nullptr;  // sharded: the combine kernel writes it
       a.fail = e->fail.p;
       a.xrec = g->xrec;
       a.ref_slack = 64.0;
@@ -316,6 +318,7 @@ int run_group(pf_group* g, const double* y, int64_t T, pf_outputs* out) {
       so.s_sd = e->o_ssd.p;
       so.t_mean = e->o_tm.p;
       so.t_sd = e->o_tsd.p;
+      so.ess = e->o_ess.p;
       double* qmom = (s == 0 && ntg) ? &(e0->qsh.p + par)->mean[0] : nullptr;
       combine_kernel<MODE><<<1, 256, 0, e->st>>>(g->xrec, G, t, 0, so, qmom, e->sc.p, e->mbuf.p + par,
                                                  e->fail.p);
@@ -450,7 +453,21 @@ int run_group(pf_group* g, const double* y, int64_t T, pf_outputs* out) {
           g_launches.fetch_add(G);
         }
       }
-      q_select_kernel<<<ntg, 1024, 0, ss>>>(qa, vs, e0->qscratch.p, ox, os, ot, t, e0->fail.p, e0->qunres.p);
+      QAll all;
+      memset(&all, 0, sizeof(all));
+      all.nsrc = G;
+      all.ns = ns;
+      for (int s = 0; s < G; ++s) {
+        pf_engine* e = g->sh[s];
+        uint32_t* kb = e->keys.p + (size_t)par * 3 * ns;
+        all.keys[s][0] = want_fq ? kb : nullptr;
+        all.keys[s][1] = want_sq ? kb + ns : nullptr;
+        all.keys[s][2] = want_tq ? kb + 2 * (size_t)ns : nullptr;
+        all.lw[s] = e->lw.p + (size_t)par * ns;
+        all.M[s] = e->mbuf.p + par;
+      }
+      all.single = SINGLE;
+      q_select_kernel<<<ntg, 1024, 0, ss>>>(qa, vs, e0->qscratch.p, ox, os, ot, t, e0->fail.p, e0->qunres.p, all);
       q_step_end_kernel<<<1, 1024, 0, ss>>>(qa, 1);
       g_launches.fetch_add(2);
       CK(cudaEventRecord(e0->ev_q[t & 1], ss));
@@ -487,8 +504,8 @@ int run_group(pf_group* g, const double* y, int64_t T, pf_outputs* out) {
       m.learn_t = LT;
       m.sigma2_fixed = c.sigma2_fixed;
       m.tau2_fixed = c.tau2_fixed;
-      m.a_s = shape_at(c, true, T);
-      m.a_t = shape_at(c, false, T);
+      m.a_s = shape_at(e, true, T);
+      m.a_t = shape_at(e, false, T);
       m.idx = keep_idx ? e->idx.p : nullptr;
       double* dst[7] = {out->final_states, out->final_sigma2, out->final_tau2, out->final_a_sigma,
                         out->final_b_sigma, out->final_a_tau, out->final_b_tau};
@@ -530,6 +547,7 @@ int run_group(pf_group* g, const double* y, int64_t T, pf_outputs* out) {
       return PF_OK;
     };
     if ((rc = cp(out->filtered_mean, e0->o_fm, T)) != PF_OK) return rc;
+    if (out->ess && (rc = cp(out->ess, e0->o_ess, T)) != PF_OK) return rc;
     if (want_fq && (rc = cp(out->filtered_quantiles, e0->o_fq, T * 3)) != PF_OK) return rc;
     if (LS && ((rc = cp(out->sigma2_mean, e0->o_sm, T)) || (rc = cp(out->sigma2_sd, e0->o_ssd, T)) ||
                (rc = cp(out->sigma2_quantiles, e0->o_sq, T * 5))))
@@ -563,6 +581,10 @@ int run_group(pf_group* g, const double* y, int64_t T, pf_outputs* out) {
     return set_err(PF_ERR_ALL_WEIGHTS_ZERO,
                    "all particle weights are zero (at time step " + std::to_string(fail_h) + ")", fail_h);
   if (fail_h < 0) return set_err(PF_ERR_ALL_WEIGHTS_ZERO, "all particle weights are zero", 0);
+  if (ntg) {
+    if ((rc = set_device(g->dev[0])) != PF_OK) return rc;
+    if ((rc = check_quantile_unresolved(e0->qunres.p)) != PF_OK) return rc;
+  }
   return PF_OK;
 }
 

@@ -1163,14 +1163,30 @@ __global__ void __launch_bounds__(256) q_fallback_fill_kernel(QArgs qa, const do
   }
 }
 
+// Every particle of the step, per source (one per shard; a single run has
+// one): the overflow path of q_select_kernel walks these instead of the
+// truncated candidate list.
+struct QAll {
+  int nsrc;                                    // 0: not available (count the target unresolved)
+  int64_t ns;                                  // particles per source
+  const uint32_t* keys[PF_MAX_SHARDS][Q_MAXQ];
+  const double* lw[PF_MAX_SHARDS];             // log-weights (or fed weights, wmode 1)
+  const double* M[PF_MAX_SHARDS];              // the step's max log-weight
+  int wmode, single;
+};
+
 // S: last resort for a target whose re-windowed candidates still crowd the
 // exact list (heavy ties): weighted radix select over the exact 64-bit value
 // images of all candidates (one CTA per target).  Smallest value v with
 // wbelow + sum_{value <= v} w >= p W -- the same answer as the stable-order
-// cumulative search.
+// cumulative search.  A window that held more candidates than the list
+// (tg.count > cap: e.g. tau2 = 0, where resampling leaves long runs of
+// identical states) is selected exactly over every particle whose key lies
+// in the window, read from `all`; the weights are formed as the candidate
+// passes form them, so the answer is the one the full list would give.
 __global__ void __launch_bounds__(1024)
 q_select_kernel(QArgs qa, QValueSrc vs, double* __restrict__ scratch, double* out_x, double* out_s,
-                double* out_t, int64_t t_step, const int64_t* fail, unsigned int* unresolved) {
+                double* out_t, int64_t t_step, const int64_t* fail, unsigned int* unresolved, QAll all) {
   if (*fail || !qa.sh->any_miss) return;
   const int k = blockIdx.x;
   QTarget& tg = qa.tg[k];
@@ -1178,11 +1194,15 @@ q_select_kernel(QArgs qa, QValueSrc vs, double* __restrict__ scratch, double* ou
   __shared__ unsigned long long hist[256];
   __shared__ uint64_t prefix;
   __shared__ double base;
+  const bool over = tg.count > qa.cap;
+  const bool exact_all = over && all.nsrc > 0;
   const uint32_t m = min(tg.count, qa.cap);
   double* val = scratch + (size_t)k * qa.cap;
   const QCand* cand = qa.cand + (size_t)k * qa.cap;
-  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) val[i] = quantity_value(vs, tg.q, cand[i].idx);
+  if (!exact_all)
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) val[i] = quantity_value(vs, tg.q, cand[i].idx);
   const double T = tg.p * qa.sh->W;
+  const uint32_t klo = tg.klo, khi = tg.khi;
   if (threadIdx.x == 0) {
     prefix = 0;
     base = tg.wbelow;
@@ -1192,10 +1212,27 @@ q_select_kernel(QArgs qa, QValueSrc vs, double* __restrict__ scratch, double* ou
     for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     const uint64_t pfx = prefix;
-    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-      const uint64_t b = ordered_bits(val[i]);
-      if (shift == 56 || (b >> (shift + 8)) == pfx)
-        atomicAdd(&hist[(b >> shift) & 255], (unsigned long long)llrint(cand[i].w * qa.fx_scale));
+    if (exact_all) {
+      for (int h = 0; h < all.nsrc; ++h) {
+        const uint32_t* kq = all.keys[h][tg.q];
+        const double M = all.wmode == 0 ? *all.M[h] : 0.0;
+        for (int64_t i = threadIdx.x; i < all.ns; i += blockDim.x) {
+          const uint32_t key = kq[i];
+          if (key < klo || key > khi) continue;
+          const uint64_t b = ordered_bits(quantity_value(vs, tg.q, (uint32_t)(h * all.ns + i)));
+          if (shift == 56 || (b >> (shift + 8)) == pfx) {
+            double w = all.wmode == 0 ? exp(all.lw[h][i] - M) : all.lw[h][i];
+            if (all.single) w = (double)(float)w;
+            atomicAdd(&hist[(b >> shift) & 255], (unsigned long long)llrint(w * qa.fx_scale));
+          }
+        }
+      }
+    } else {
+      for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        const uint64_t b = ordered_bits(val[i]);
+        if (shift == 56 || (b >> (shift + 8)) == pfx)
+          atomicAdd(&hist[(b >> shift) & 255], (unsigned long long)llrint(cand[i].w * qa.fx_scale));
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1220,7 +1257,7 @@ q_select_kernel(QArgs qa, QValueSrc vs, double* __restrict__ scratch, double* ou
     double* o = tg.q == 0 ? out_x : (tg.q == 1 ? out_s : out_t);
     const int ncol = tg.q == 0 ? 3 : 5;
     o[(t_step - 1) * ncol + tg.col] = v;
-    if (tg.count > qa.cap) atomicAdd(unresolved, 1u);
+    if (over && !exact_all) atomicAdd(unresolved, 1u);  // the host raises on this
     tg.status = QS_OK;
   }
 }

@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(256) init_kernel(InitArgs a) {
 
 // ---------------------------------------------------------------- step ---
 struct Partial {
-  double m, s0, sx, s2x, s1s, s2s, s1t, s2t, bad;
+  double m, s0, sx, s2x, s1s, s2s, s1t, s2t, s2w, bad;  // s2w: sum of squared weights (ESS)
 };
 
 struct Scalars {
@@ -172,6 +172,7 @@ struct StepOut {   // device arrays indexed by t-1
   double* s_sd;
   double* t_mean;
   double* t_sd;
+  double* ess;     // optional: (sum w)^2 / sum w^2 (extension; the reference has no ESS)
 };
 
 struct DrawArgs {
@@ -238,8 +239,8 @@ PF_D double warp_max(double v) {
 // Combine `count` partials (each rescaled to its own max) in a fixed order:
 // M = max (NaN when any partial saw a NaN / +inf log-weight), S = sums
 // rescaled to M.  Called by all threads of one CTA; results in thread 0.
-PF_D void reduce_partials(const Partial* p, int count, double (*red)[8], double& M_out, double& bad_out,
-                          double (&S)[7]) {
+PF_D void reduce_partials(const Partial* p, int count, double (*red)[10], double& M_out, double& bad_out,
+                          double (&S)[8]) {
   __shared__ double mfin;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double M = -INFINITY, badsum = 0.0;
@@ -260,7 +261,7 @@ PF_D void reduce_partials(const Partial* p, int count, double (*red)[8], double&
   }
   __syncthreads();
   M = mfin;
-  double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int b = threadIdx.x; b < count; b += blockDim.x) {
     const double mb2 = __ldcg(&p[b].m);
     const double f = (mb2 == -INFINITY) ? 0.0 : exp(mb2 - M);
@@ -271,18 +272,19 @@ PF_D void reduce_partials(const Partial* p, int count, double (*red)[8], double&
     acc[4] += f * __ldcg(&p[b].s2s);
     acc[5] += f * __ldcg(&p[b].s1t);
     acc[6] += f * __ldcg(&p[b].s2t);
+    acc[7] += (f * f) * __ldcg(&p[b].s2w);
   }
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < 7; ++k) {
+  for (int k = 0; k < 8; ++k) {
     const double sv = warp_sum(acc[k]);
     if (lane == 0) red[warp][k] = sv;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int k = 0; k < 7; ++k) S[k] = 0.0;
+    for (int k = 0; k < 8; ++k) S[k] = 0.0;
     for (int w = 0; w < nw; ++w)
-      for (int k = 0; k < 7; ++k) S[k] += red[w][k];
+      for (int k = 0; k < 8; ++k) S[k] += red[w][k];
     M_out = M;
   }
 }
@@ -291,7 +293,7 @@ PF_D void reduce_partials(const Partial* p, int count, double (*red)[8], double&
 // moment shifts of the next step, the max log-weight and the degeneracy
 // check (filtering.py:294-296).  One thread.
 template <bool LS, bool LT>
-PF_D void finalize_step(int64_t t, double M, double bsum, const double (&S)[7], bool feedw, double cs,
+PF_D void finalize_step(int64_t t, double M, double bsum, const double (&S)[8], bool feedw, double cs,
                         double ct, double cx, const StepOut& out, double* qmom, Scalars* sc, double* Mout,
                         int64_t* fail) {
   (void)bsum;
@@ -299,6 +301,7 @@ PF_D void finalize_step(int64_t t, double M, double bsum, const double (&S)[7], 
   const double W = S[0];
   const double fm = S[1] / W;
   out.fmean[i] = fm;
+  if (out.ess) out.ess[i] = (W * W) / S[7];
   {
     const double d = fm - cx;
     const double var = S[2] / W - d * d;
@@ -421,7 +424,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
   // step's M.
   double m = feedw ? 0.0 : -INFINITY;
   double mx = m;
-  double s0 = 0, sx = 0, s2x = 0, s1s = 0, s2s = 0, s1t = 0, s2t = 0;
+  double s0 = 0, sx = 0, s2x = 0, s1s = 0, s2s = 0, s1t = 0, s2t = 0, s2w = 0;
   bool bad = false;
 
   // Software pipeline over batches of STEP_SB x blockDim slots (batches are
@@ -573,7 +576,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
       if (lw > mx) mx = lw;
       if (lw > m + a.ref_slack) {
         const double sc = exp(m - lw);
-        s0 *= sc; sx *= sc; s2x *= sc; s1s *= sc; s2s *= sc; s1t *= sc; s2t *= sc;
+        s0 *= sc; sx *= sc; s2x *= sc; s1s *= sc; s2s *= sc; s1t *= sc; s2t *= sc; s2w *= sc * sc;
         m = lw;
         e = 1.0;
       } else if (lw > -INFINITY) {
@@ -586,6 +589,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
     if (a.ks) a.ks[j] = key_rd_(s2);
     if (a.kt) a.kt[j] = key_rd_(t2);
     s0 += e;
+    s2w = fma(e, e, s2w);
     sx = fma(e, xn, sx);
     const double dxx = xn - cx;
     s2x = fma(e * dxx, dxx, s2x);
@@ -603,7 +607,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
   pdl_launch_dependents();  // only the CTA reductions remain
 
   // ---- CTA reduction with rescaling to the CTA max
-  __shared__ double red[32][8];
+  __shared__ double red[32][10];
   __shared__ double mblk;
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -618,24 +622,25 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
   __syncthreads();
   const double mb = mblk;
   const double scl = (m == -INFINITY) ? 0.0 : exp(m - mb);
-  double v[8] = {s0 * scl, sx * scl, s2x * scl, s1s * scl, s2s * scl, s1t * scl, s2t * scl,
-                 bad ? 1.0 : 0.0};
+  double v[9] = {s0 * scl, sx * scl, s2x * scl, s1s * scl, s2s * scl, s1t * scl, s2t * scl,
+                 s2w * (scl * scl), bad ? 1.0 : 0.0};
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
+  for (int k = 0; k < 9; ++k) {
     const double s = warp_sum(v[k]);
     if (lane == 0) red[warp][k] = s;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
-      for (int k = 0; k < 8; ++k) acc[k] += red[w][k];
+      for (int k = 0; k < 9; ++k) acc[k] += red[w][k];
     Partial p;
     p.m = mb;
     p.s0 = acc[0]; p.sx = acc[1]; p.s2x = acc[2]; p.s1s = acc[3]; p.s2s = acc[4]; p.s1t = acc[5];
     p.s2t = acc[6];
-    p.bad = acc[7];
+    p.s2w = acc[7];
+    p.bad = acc[8];
     a.partials[blockIdx.x] = p;
     __threadfence();
     const unsigned int ticket = atomicAdd(&a.sc->counter, 1u);
@@ -646,7 +651,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
 
   // ---- last CTA: combine the partials (fixed order -> deterministic)
   __threadfence();
-  double M, bsum, S[7];
+  double M, bsum, S[8];
   reduce_partials(a.partials, (int)gridDim.x, red, M, bsum, S);
   if (threadIdx.x != 0) return;
   if (a.xrec) {
@@ -655,6 +660,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
     Partial p;
     p.m = M;
     p.s0 = S[0]; p.sx = S[1]; p.s2x = S[2]; p.s1s = S[3]; p.s2s = S[4]; p.s1t = S[5]; p.s2t = S[6];
+    p.s2w = S[7];
     p.bad = bsum;
     a.xrec[a.shard] = p;
     __threadfence_system();
@@ -672,9 +678,9 @@ __global__ void __launch_bounds__(256) combine_kernel(const Partial* __restrict_
                                                       double* Mout, int64_t* fail) {
   constexpr bool LS = MODE & M_LS, LT = MODE & M_LT;
   if (*fail) return;
-  __shared__ double red[8][8];
+  __shared__ double red[8][10];
   const double cs = sc->cs, ct = sc->ct, cx = sc->cx;
-  double M, bsum, S[7];
+  double M, bsum, S[8];
   reduce_partials(xrec, G, red, M, bsum, S);
   if (threadIdx.x != 0) return;
   finalize_step<LS, LT>(t, M, bsum, S, feedw != 0, cs, ct, cx, out, qmom, sc, Mout, fail);

@@ -35,6 +35,7 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
+from . import errors as _errors
 
 PF_XCHG_PARTIAL = 0
 PF_XCHG_TOTAL = 1
@@ -74,29 +75,81 @@ class ShardRank:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.nccl = dist.get_backend(group) == "nccl"
-        self.lib = _lib.require_device()
         self.device = int(cfg.device)
         self.h = C.c_void_p()
-        _lib.check(self.lib.pf_shard_create(C.byref(cfg), self.rank, self.world, C.byref(self.h)), self.lib)
         self.cfg = cfg
+        # creation is collective: a rank that fails still meets the others,
+        # and every rank raises (none is left waiting in the peer exchange)
+        err = None
         try:
-            self._open_peers()
+            self.lib = _lib.require_device()
+            _lib.check(self.lib.pf_shard_create(C.byref(cfg), self.rank, self.world, C.byref(self.h)), self.lib)
+        except Exception as exc:  # noqa: BLE001 -- agreed on below
+            err = exc
+        self._raise_agreed(err, release=True)
+        self._open_peers()
+        try:
             self._bind_exchange()
-        except Exception:
-            self.close()
-            raise
+        except Exception as exc:  # noqa: BLE001
+            err = exc
+        self._raise_agreed(err, release=True)
+
+    # ---------------------------------------------------- rank agreement
+    @staticmethod
+    def _status_of(exc):
+        if exc is None:
+            return None
+        return (type(exc), exc.args, getattr(exc, "step", None))
+
+    @staticmethod
+    def _rebuild(status):
+        typ, args, step = status
+        if step is not None and issubclass(typ, _errors.AllWeightsZeroError):
+            return typ(step=step)
+        try:
+            return typ(*args)
+        except Exception:  # noqa: BLE001 -- an exception type with another signature
+            return _errors.DeviceError(f"{typ.__name__}: {args}")
+
+    def _agreed_status(self, exc):
+        """Every rank's status (None or its exception), exchanged before any
+        data collective: the first failing rank's, or None when all ran."""
+        allst = [None] * self.world
+        self.dist.all_gather_object(allst, self._status_of(exc), group=self.group)
+        return next((st for st in allst if st is not None), None)
+
+    def _raise_agreed(self, exc, release=False):
+        st = self._agreed_status(exc)
+        if st is None:
+            return
+        if release:
+            self._release_local()
+        raise exc if exc is not None else self._rebuild(st)
 
     # ------------------------------------------------------------ set-up
     def _open_peers(self):
-        hb = int(self.lib.pf_shard_ipc_handle_bytes())
-        mine = np.zeros(hb, dtype=np.uint8)
-        _lib.check(self.lib.pf_shard_ipc_handles(self.h, mine.ctypes.data_as(C.c_void_p)), self.lib)
+        err, mine = None, b""
+        try:
+            hb = int(self.lib.pf_shard_ipc_handle_bytes())
+            h = np.zeros(hb, dtype=np.uint8)
+            _lib.check(self.lib.pf_shard_ipc_handles(self.h, h.ctypes.data_as(C.c_void_p)), self.lib)
+            mine = h.tobytes()
+        except Exception as exc:  # noqa: BLE001
+            err = exc
         allh = [None] * self.world
-        self.dist.all_gather_object(allh, mine.tobytes(), group=self.group)
-        buf = np.frombuffer(b"".join(allh), dtype=np.uint8).copy()
-        _lib.check(self.lib.pf_shard_open_peers(self.h, buf.ctypes.data_as(C.c_void_p)), self.lib)
-        # every rank must have mapped its peers before any rank starts a run
-        self.dist.barrier(group=self.group)
+        self.dist.all_gather_object(allh, (mine, self._status_of(err)), group=self.group)
+        bad = next((st for _, st in allh if st is not None), None)
+        if bad is not None:
+            self._release_local()
+            raise err if err is not None else self._rebuild(bad)
+        try:
+            buf = np.frombuffer(b"".join(m for m, _ in allh), dtype=np.uint8).copy()
+            _lib.check(self.lib.pf_shard_open_peers(self.h, buf.ctypes.data_as(C.c_void_p)), self.lib)
+        except Exception as exc:  # noqa: BLE001
+            err = exc
+        # doubles as the barrier: every rank has mapped its peers before any
+        # rank starts a run
+        self._raise_agreed(err, release=True)
 
     def _bind_exchange(self):
         self.slot = {}
@@ -206,20 +259,14 @@ class ShardRank:
             self.run(y, out)
         except Exception as exc:  # noqa: BLE001 -- re-raised on every rank below
             status = exc
-        self._publish(arrays, local, status, t_len, ns)
-        if status is not None:
-            raise status
+        # every rank enters the agreement whatever happened locally; if any
+        # rank failed, every rank raises (rank 0's resolve / finish included)
+        self._raise_agreed(status)
+        self._publish(arrays, local, t_len, ns)
 
-    def _publish(self, arrays, local, status, t_len, ns):
+    def _publish(self, arrays, local, t_len, ns):
         import torch
 
-        # rank 0's status decides (all ranks see the same partial records)
-        flag = [None]
-        if self.rank == 0:
-            flag[0] = None if status is None else (type(status), status.args)
-        self.dist.broadcast_object_list(flag, src=0, group=self.group)
-        if flag[0] is not None or status is not None:
-            return
         dev = torch.device("cuda", self.device) if self.nccl else torch.device("cpu")
         summaries = sorted(k for k in arrays if k != "indices" and not k.startswith("final_"))
         if summaries:
@@ -251,20 +298,32 @@ class ShardRank:
         return {"total_ms": tot.value}
 
     def close(self):
-        """Unmap the peers, meet the other ranks, then free: no rank frees
-        memory a peer still maps."""
+        """Collective teardown (explicit ``close`` / ``Backend.close`` /
+        ``with``, called by every rank): unmap the peers, meet the other
+        ranks, then free -- no rank frees memory a peer still maps."""
         if self.h:
             self.lib.pf_shard_close_peers(self.h)
-            try:
-                if self.dist.is_initialized():
-                    self.dist.barrier(group=self.group)
-            except Exception:  # noqa: BLE001 -- teardown after a failed peer: free anyway
-                pass
+            if self.dist.is_initialized():
+                self.dist.barrier(group=self.group)
             self.lib.pf_shard_destroy(self.h)
             self.h = C.c_void_p()
 
+    def release(self):
+        """Non-collective teardown (garbage collection): a barrier here could
+        pair with an unrelated collective on a peer, so only this rank's
+        mappings of its peers are dropped and its own memory is left to the
+        process exit (a peer may still map it)."""
+        self._release_local()
+
+    def _release_local(self):
+        if getattr(self, "h", None):
+            try:
+                self.lib.pf_shard_close_peers(self.h)
+            finally:
+                self.h = C.c_void_p()
+
     def __del__(self):
         try:
-            self.close()
+            self.release()
         except Exception:
             pass

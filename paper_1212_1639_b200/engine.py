@@ -87,6 +87,15 @@ class Engine:
         _lib.check(self.lib.pf_engine_quantile_stats(self.h, s), self.lib)
         return {"unresolved": s[0], "fallbacks": s[1], "max_candidates": s[2], "resolves": s[3]}
 
+    PATH_FLAGS = {"fused_draws": 1, "rank_tables": 2, "fused_top": 4}
+
+    def last_path(self):
+        """Kernel path of the last run (pf_engine_last_path): which of the
+        benchmarked variants actually executed."""
+        f = C.c_int32()
+        _lib.check(self.lib.pf_engine_last_path(self.h, C.byref(f)), self.lib)
+        return {k: bool(f.value & b) for k, b in self.PATH_FLAGS.items()}
+
     def close(self):
         if self.h:
             self.lib.pf_engine_destroy(self.h)

@@ -79,6 +79,10 @@ class FilterOutput:
     final_particles: ParticleSystem | None = None
     particle_history: list | None = None
     resampled_indices: np.ndarray | None = None
+    # extension (not in the reference): effective sample size per step,
+    # (sum w)^2 / sum w^2 of the pre-resample weights, from the device's
+    # per-shard weight sums
+    ess: np.ndarray | None = None
 
 
 def snapshot_store(particles, dest):
@@ -246,7 +250,7 @@ def _run_loop(model, priors, y, n, seed, backend, resampler, precision, store_pa
 
 def _alloc_outputs(t_len, n, learn, ls, lt, track_quantiles, keep_indices, keep_final, store):
     out = _lib.PfOutputs()
-    a = {"filtered_mean": np.empty(t_len)}
+    a = {"filtered_mean": np.empty(t_len), "ess": np.empty(t_len)}
     if track_quantiles:
         a["filtered_quantiles"] = np.empty((t_len, 3))
     if learn and ls:
@@ -300,4 +304,4 @@ def _assemble(out, a, t_len, n, dtype, learn, ls, lt, store):
     return FilterOutput(filtered_mean=a["filtered_mean"],
                         filtered_quantiles=a.get("filtered_quantiles"),
                         param_posterior=summaries, timings=timings, final_particles=final,
-                        particle_history=history, resampled_indices=a.get("indices"))
+                        particle_history=history, resampled_indices=a.get("indices"), ess=a.get("ess"))

@@ -41,12 +41,17 @@ def test_version_and_device_count_without_compute(lib):
     assert lib.pf_launch_count() >= 0
 
 
-def test_struct_layouts_match_header():
-    """pf_config / pf_outputs field order and sizes as the C compiler lays them out."""
+def test_struct_layouts_match_header(lib):
+    """pf_config / pf_outputs / pf_feed: the ctypes mirrors have the sizes the
+    compiled library reports (pf_abi_sizes), and the expected field count."""
     from paper_1212_1639_b200 import _lib
 
+    sizes = (_lib.C.c_int64 * 3)()
+    assert lib.pf_abi_sizes(sizes) == 0
+    assert list(sizes) == [_lib.C.sizeof(_lib.PfConfig), _lib.C.sizeof(_lib.PfOutputs),
+                           _lib.C.sizeof(_lib.PfFeed)]
     assert _lib.C.sizeof(_lib.PfConfig) == 8 + 8 + 4 * 4 + 8 * 11 + 4 * 8
-    assert _lib.C.sizeof(_lib.PfOutputs) == 8 * 23 + 8 * 7 + 8
+    assert _lib.C.sizeof(_lib.PfOutputs) == 8 * 23 + 8 * 7 + 8 + 8
     assert _lib.C.sizeof(_lib.PfFeed) == 32
 
 

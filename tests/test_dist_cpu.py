@@ -64,7 +64,7 @@ def _rank_main(rank, world, port, result):
         local["sigma2_quantiles"] = arrays["sigma2_quantiles"]
     sr = ShardRank.__new__(ShardRank)
     sr.dist, sr.group, sr.rank, sr.world, sr.nccl, sr.device, sr.h = dist, None, rank, world, False, 0, None
-    sr._publish(arrays, local, None, t_len, ns)
+    sr._publish(arrays, local, t_len, ns)
     result.put((rank, {k: v.tobytes() for k, v in arrays.items()}))
     dist.barrier()
     dist.destroy_process_group()
@@ -92,3 +92,49 @@ def test_two_gloo_ranks_publish_the_full_outputs():
         assert np.array_equal(np.frombuffer(a["sigma2_quantiles"]), np.arange(t_len * 5, dtype=float))
         assert np.array_equal(np.frombuffer(a["indices"], dtype=np.int64).reshape(t_len, n), want_idx)
         assert np.array_equal(np.frombuffer(a["final_states"]), np.repeat([0.0, 1.0], ns))
+
+
+def _agree_main(rank, world, port, result):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sr = ShardRank.__new__(ShardRank)
+    sr.dist, sr.group, sr.rank, sr.world, sr.nccl, sr.device, sr.h = dist, None, rank, world, False, 0, None
+    seen = []
+    # (a) only rank 1 fails: every rank raises its error (no rank left in a collective)
+    # (b) only rank 0 fails with a step-carrying degeneracy: rank 1 rebuilds it with the step
+    # (c) nobody fails: no exception
+    cases = [(1, P.NonFiniteWeightError("bad weight on rank 1")), (0, P.AllWeightsZeroError(step=3)), (None, None)]
+    for who, exc in cases:
+        try:
+            sr._raise_agreed(exc if rank == who else None)
+            seen.append(None)
+        except Exception as e:  # noqa: BLE001
+            seen.append((type(e).__name__, str(e), getattr(e, "step", None)))
+    result.put((rank, seen))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_gloo_ranks_agree_on_failure():
+    """a failure on any one rank is raised on every rank, rebuilt
+    from the failing rank's type, message and step."""
+    import torch.multiprocessing as mp
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_agree_main, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert got[0] == got[1]
+    assert got[0][0] == ("NonFiniteWeightError", "bad weight on rank 1", None)
+    assert got[0][1] == ("AllWeightsZeroError", "all particle weights are zero (at time step 3)", 3)
+    assert got[0][2] is None

@@ -67,7 +67,7 @@ def test_oracle_mode_matches_reference(gpu, name, with_w):
             if f"{nm}_mean" in d:
                 s = out.param_posterior[nm]
                 assert _rel(s.mean, d[f"{nm}_mean"]) <= REL
-                assert _rel(s.sd, d[f"{nm}_sd"]) <= 1e-8
+                assert _rel(s.sd, d[f"{nm}_sd"]) <= REL, _rel(s.sd, d[f"{nm}_sd"])
                 assert np.array_equal(s.quantiles, d[f"{nm}_quantiles"])
         assert np.array_equal(fp.params.sigma2, d["final_sigma2"])
         assert np.array_equal(fp.params.tau2, d["final_tau2"])
@@ -123,7 +123,9 @@ def test_native_mode_tracks_reference(gpu, name):
     d = golden(name)
     out = _run(d)
     agree = float(np.mean(out.resampled_indices == d["indices"]))
-    assert agree > 0.9
+    # draws within ~1e-14 relative of scipy's: an ancestor differs only where
+    # that perturbation crosses a cut point (near-ties), which is rare
+    assert agree >= 0.999, agree
     assert np.max(np.abs(out.filtered_mean - d["filtered_mean"])) < 0.05
 
 

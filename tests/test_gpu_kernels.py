@@ -95,6 +95,7 @@ def test_gammaincinv_vs_scipy(gpu, method):
         got = prng.gammaincinv(float(a), u, method=method)
         rel = np.abs(got - d["gammaincinv"][k]) / d["gammaincinv"][k]
         worst = max(worst, float(rel.max()))
+    print(f"gammaincinv[{method}] worst relative error vs scipy: {worst:.3e}")
     assert worst <= 2e-13, worst
 
 
