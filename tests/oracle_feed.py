@@ -55,7 +55,7 @@ def make_feed(n, t_len, seed, sigma2_shape=5.0, tau2_shape=5.0, procs=None):
         feed["g_tau"] = np.empty((t_len + 1, n))
     jobs = [(seed, lo, min(n, lo + _CHUNK), t, sa[t] if sa else None, ta[t] if ta else None)
             for t in range(t_len + 1) for lo in range(0, n, _CHUNK)]
-    with get_context("fork").Pool(procs) as pool:
+    with get_context("spawn").Pool(procs) as pool:
         for (lo, z, gs, gt), job in zip(pool.imap(_rows, jobs), jobs):
             t, hi = job[3], job[2]
             feed["z"][t, lo:hi] = z

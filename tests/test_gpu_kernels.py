@@ -96,7 +96,10 @@ def test_gammaincinv_vs_scipy(gpu, method):
         rel = np.abs(got - d["gammaincinv"][k]) / d["gammaincinv"][k]
         worst = max(worst, float(rel.max()))
     print(f"gammaincinv[{method}] worst relative error vs scipy: {worst:.3e}")
-    assert worst <= 2e-13, worst
+    # measured on B200: 2.39e-14 (table), 2.33e-14 (accurate solver) -- the
+    # two agree with each other far closer than with scipy, whose own Halley
+    # stopping rule leaves ~1e-14 (profiles/r02_pytest_gpu.log)
+    assert worst <= 3e-14, worst
 
 
 # ------------------------------------------------------------ tree CDF ---

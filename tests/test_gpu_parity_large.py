@@ -96,10 +96,13 @@ def test_native_fused_draws_equal_draws_kernel(gpu, monkeypatch):
     assert np.array_equal(a.resampled_indices, c.resampled_indices)
     assert np.array_equal(a.final_particles.states, c.final_particles.states)
     assert np.array_equal(a.final_particles.params.sigma2, c.final_particles.params.sigma2)
-    assert np.array_equal(a.filtered_mean, c.filtered_mean)
     assert np.array_equal(a.filtered_quantiles, c.filtered_quantiles)
+    # the two kernels' CTA widths differ (512 / 256 threads), so the fp64
+    # moment sums are added in a different order: equal to rounding
+    assert _rel(a.filtered_mean, c.filtered_mean) <= REL
     for nm in ("sigma2", "tau2"):
-        assert np.array_equal(a.param_posterior[nm].mean, c.param_posterior[nm].mean)
+        assert _rel(a.param_posterior[nm].mean, c.param_posterior[nm].mean) <= REL
+        assert _rel(a.param_posterior[nm].sd, c.param_posterior[nm].sd) <= REL
         assert np.array_equal(a.param_posterior[nm].quantiles, c.param_posterior[nm].quantiles)
 
 
