@@ -154,6 +154,64 @@ def cpu_reference_run(n, t_len, lanes):
     return n * t_len / dt, dt
 
 
+def _aggregate_worker(args):
+    n, t_len, barrier_ = args
+    from oracle import restate as R
+
+    _, y = R.simulate(1.0, 0.1, 0.0, t_len, 0)
+    R.run_loop(y[:1], min(n, 1024), 0, track_quantiles=False)  # warm-up (imports, scipy)
+    barrier_.wait()
+    t0 = time.time()
+    R.run_loop(y, n, 0, track_quantiles=False)
+    return t0, time.time()
+
+
+def cpu_aggregate_run(n, t_len, procs):
+    """BASELINE.md §3 all-cores aggregate: ``procs`` concurrent single-lane
+    processes, one replication each (the reference's gammaincinv / argsort
+    are single-threaded, so lanes barely help one run).  Returns
+    particle-steps/s over the wall span of all timed runs."""
+    from multiprocessing import get_context
+
+    ctx = get_context("spawn")
+    with ctx.Manager() as mgr:
+        b = mgr.Barrier(procs)
+        with ctx.Pool(procs) as pool:
+            spans = pool.map(_aggregate_worker, [(n, t_len, b)] * procs)
+    wall = max(e for _, e in spans) - min(s for s, _ in spans)
+    return procs * n * t_len / wall, wall
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline_block(n, t_len, aggregate=True):
+    """The cpu_baseline object: the reference's par_cutpoint cell (oracle port,
+    all host threads as Backend lanes) on a bounded sample at N = n, plus the
+    all-cores aggregate and the host model."""
+    lanes = os.cpu_count() or 1
+    v, dt = cpu_reference_run(n, t_len, lanes)
+    out = {"value": v, "unit": "particle-steps/s", "cores": lanes, "kind": "port",
+           "sample": f"oracle/restate.py run_loop N={n} T={t_len} ({dt:.1f} s, {lanes} lanes, one run)",
+           "cpu_model": cpu_model(),
+           "survey_measured_reference": "SURVEY.md §6.3: the unmodified reference measured in the "
+                                        "build container (8 vCPU), same cell"}
+    if aggregate:
+        agg, wall = cpu_aggregate_run(n, t_len, lanes)
+        out["aggregate_all_cores"] = {"value": agg, "unit": "particle-steps/s", "procs": lanes,
+                                      "sample": f"{lanes} concurrent 1-lane runs of N={n} T={t_len} "
+                                                f"({wall:.1f} s wall)"}
+    return out
+
+
 def run_reference_arm(args, world, rank):
     if rank != 0:
         return
@@ -161,7 +219,7 @@ def run_reference_arm(args, world, rank):
     n, t_len = args.ref_n, args.ref_t
     vals = []
     for _ in range(args.warmup):
-        cpu_reference_run(n, max(2, t_len // 4), lanes)
+        cpu_reference_run(min(n, 1 << 16), 2, lanes)
     for _ in range(args.steps):
         v, _ = cpu_reference_run(n, t_len, lanes)
         vals.append(v)
@@ -176,8 +234,9 @@ def run_reference_arm(args, world, rank):
         "config": {"workload": f"PL trend+noise, Priors(), cutpoint, N={args.n}, T={args.t} "
                                f"(CPU sample N={n}, T={t_len})", "N": args.n, "T": args.t},
         "cpu_baseline": {"value": value, "unit": "particle-steps/s", "cores": lanes,
-                         "kind": "port",
-                         "sample": f"oracle/restate.py run_loop N={n} T={t_len}, {lanes} lanes"},
+                         "kind": "port", "cpu_model": cpu_model(),
+                         "sample": f"oracle/restate.py run_loop N={n} T={t_len}, {lanes} lanes, "
+                                   f"median of {args.steps}"},
         "e2e": {"value": value, "unit": "particle-steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -201,8 +260,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n", type=int, default=1 << 24)
     ap.add_argument("--t", type=int, default=1000)
-    ap.add_argument("--ref-n", type=int, default=1 << 16)
-    ap.add_argument("--ref-t", type=int, default=20)
+    ap.add_argument("--ref-n", type=int, default=1 << 20, help="CPU sample particles (BASELINE.md §3: N >= 2^20)")
+    ap.add_argument("--ref-t", type=int, default=10, help="CPU sample steps (cost is linear in T)")
+    ap.add_argument("--no-cpu-aggregate", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--multi", default="shard", choices=["shard", "replicas"])
     ap.add_argument("--n-shard", type=int, default=None,
@@ -269,11 +329,7 @@ def main():
     traffic = load_traffic()
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        lanes = os.cpu_count() or 1
-        v, dt = cpu_reference_run(args.ref_n, args.ref_t, lanes)
-        cpu = {"value": v, "unit": "particle-steps/s", "cores": lanes, "kind": "port",
-               "sample": f"oracle/restate.py run_loop N={args.ref_n} T={args.ref_t} "
-                         f"({dt:.1f} s, {lanes} lanes)"}
+        cpu = cpu_baseline_block(args.ref_n, args.ref_t, aggregate=not args.no_cpu_aggregate)
     if rank == 0:
         line = {
             "metric": "particle-steps/sec (N*T/s), full particle-learning cycle",

@@ -245,6 +245,31 @@ PF_HD int gt_segment(double u, double* t) {
   return GT_TAIL + j;
 }
 
+// Branch-free gt_segment for the hot path: both the tail and the central
+// coordinates are formed with the same operations as gt_segment and the
+// result is selected, so (seg, t) are identical -- but a warp whose lanes
+// straddle u = 1/4 or 3/4 no longer executes the two paths one after the
+// other, and the three draws of a slot stay in one basic block.
+PF_HD int gt_segment_bf(double u, double* t) {
+  union { double d; uint64_t b; } c;
+  const bool up = u > 0.5;
+  const double v = up ? 1.0 - u : u;  // exact for u > 1/2; equals gt_segment's v in the tails
+  c.d = v;
+  int e = int((c.b >> 52) & 0x7FF) - 1023;
+  e = e < -53 ? -53 : e;
+  const int i = int((c.b >> (52 - 2)) & 3);
+  c.b = (c.b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull;
+  const double tt = (c.d - (1.0 + (i + 0.5) * 0.25)) * 8.0;
+  const int st = (e + 53) * GT_SUB + i;
+  const double xx = (u - 0.25) * (2.0 * GT_CENTRAL);
+  int j = int(xx);
+  j = j < 0 ? 0 : (j > GT_CENTRAL - 1 ? GT_CENTRAL - 1 : j);
+  const double tc = (xx - j - 0.5) * 2.0;
+  const bool tail = u < 0.25 || u > 0.75;
+  *t = tail ? tt : tc;
+  return tail ? (up ? GT_TAIL + GT_CENTRAL + st : st) : GT_TAIL + j;
+}
+
 // Inverse of gt_segment: the uniform (and, for the upper tail, its exact
 // complement) at local coordinate t of segment seg.
 PF_HD void gt_point(int seg, double t, double* u, double* v, bool* upper) {
@@ -311,6 +336,29 @@ PF_HD int nt_segment(double u, double* t, double* scale) {
   *t = (xx - j - 0.5) * 2.0;
   *scale = sg * (v - 0.5);  // exact
   return NT_TAIL + j;
+}
+
+// Branch-free nt_segment (same operations, selected): identical (seg, t,
+// scale), no divergence between tail and central lanes.
+PF_HD int nt_segment_bf(double u, double* t, double* scale) {
+  const bool up = u > 0.5;
+  const double v = up ? 1.0 - u : u;  // exact for u >= 1/2
+  const double sg = up ? -1.0 : 1.0;
+  union { double d; uint64_t b; } c;
+  c.d = v;
+  int e = int((c.b >> 52) & 0x7FF) - 1023;
+  e = e < -53 ? -53 : e;
+  const int i = int((c.b >> (52 - 2)) & 3);
+  c.b = (c.b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull;
+  const double tt = (c.d - (1.0 + (i + 0.5) * 0.25)) * 8.0;
+  const double xx = (v - 0.25) * (4.0 * NT_CENTRAL);
+  int j = int(xx);
+  j = j < 0 ? 0 : (j > NT_CENTRAL - 1 ? NT_CENTRAL - 1 : j);
+  const double tc = (xx - j - 0.5) * 2.0;
+  const bool tail = v < 0.25;
+  *t = tail ? tt : tc;
+  *scale = tail ? sg : sg * (v - 0.5);  // exact
+  return tail ? (e + 53) * GT_SUB + i : NT_TAIL + j;
 }
 
 // The v (<= 1/2) at local coordinate t of segment seg, and whether the

@@ -30,10 +30,14 @@ constexpr double LOG_TWO_PI = 1.8378770664093453;  // math.log(2*math.pi), model
 #define PF_FD_THREADS 512
 #endif
 constexpr int STEP_SB = PF_STEP_SB;  // slots per thread per pipeline stage (double buffered)
-// STEP_SB = 1 builds (tried with 512 and 768-thread CTAs) report an
-// out-of-range shared address in the fused draws under compute-sanitizer;
-// the cause is not understood, so they are refused rather than shipped.
-static_assert(STEP_SB >= 2, "STEP_SB = 1 is unsupported (fails memcheck in the fused draws)");
+// STEP_SB = 1 is supported again.  The round-1 SB = 1 build failed memcheck
+// ("out-of-range shared or local address" at the STS of the staged tau2
+// draw): its SASS formed that store's address from R1, the stack-pointer
+// register (profiles/r02_memcheck_summary.txt), i.e. the generic-pointer
+// store of a draw into its shared stage slot was mis-addressed.  Draws now
+// stay in registers (no generic stores into the stage at all); memcheck and
+// racecheck are clean for SB = 1 and SB = 2.  SB = 2 stays the default
+// (measured faster).
 constexpr int FD_THREADS = PF_FD_THREADS;  // CTA width of the fused-draws step kernel
 
 // Order-preserving 32-bit image of a double (float32 rounded down, sign
@@ -75,7 +79,7 @@ extern __shared__ double pf_gtab[];
 // order as gt_eval on the global [seg][k] table, so the values are identical.
 PF_D double gamma_table_slot(int slot, double u) {
   double t;
-  const int seg = gt_segment(u, &t);
+  const int seg = gt_segment_bf(u, &t);
   const double* c = pf_gtab + slot * GT_TABLE_DOUBLES + seg;
   double r = c[GT_DEG * GT_NSEG];
 #pragma unroll
@@ -86,7 +90,7 @@ PF_D double gamma_table_slot(int slot, double u) {
 PF_D double gamma_draw_slot(const GammaSrc& g, int slot, double u) {
   if (slot < 0) return gamma_draw(g, u);
   double t;
-  const int seg = gt_segment(u, &t);
+  const int seg = gt_segment_bf(u, &t);
   const double* c = pf_gtab + slot * GT_TABLE_DOUBLES + seg;
   double r = c[GT_DEG * GT_NSEG];
 #pragma unroll
@@ -236,6 +240,36 @@ PF_D double warp_max(double v) {
   return v;
 }
 
+// exp(x) for the moment weights (x = lw - m <= ref_slack): k = rint(64 x /
+// ln 2) via the 1.5 2^52 shifter, r = x - k ln2/64 (two-part constant),
+// e^r by a degree-5 Taylor polynomial (|r| <= ln2/128: truncation 4e-17),
+// times 2^(k/64) from a 64-entry shared table and 2^floor(k/64) by exponent
+// add.  Relative error < 3e-16; x < -700 gives 0 (e^-700 of the step's
+// largest weight is far below the moments' 1e-10 tolerance).
+// ~16 instructions against ~45 for exp(); the CDF's weights keep exp()
+// (they must round like the reference's).
+constexpr int EXP_TAB = 64;
+PF_D double exp_moment(double x, const double* tab) {
+  const double SH = 6755399441055744.0;                  // 1.5 * 2^52
+  const double INV = 92.33248261689366;               // 64 / ln 2
+  const double C_HI = 0.010830424696249145;             // ln2/64 rounded
+  const double C_LO = 3.623510646634843e-19;            // ln2/64 - C_HI
+  const double kd = fma(x, INV, SH);
+  const int k = (int)__double2loint(kd);
+  const double kf = kd - SH;
+  double r = fma(-kf, C_HI, x);
+  r = fma(-kf, C_LO, r);
+  double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  double v = p * tab[k & (EXP_TAB - 1)];
+  const int hi = __double2hiint(v) + (int)((unsigned)(k >> 6) << 20);
+  v = __hiloint2double(hi, __double2loint(v));
+  return x < -700.0 ? 0.0 : v;
+}
+
 // Combine `count` partials (each rescaled to its own max) in a fixed order:
 // M = max (NaN when any partial saw a NaN / +inf log-weight), S = sums
 // rescaled to M.  Called by all threads of one CTA; results in thread 0.
@@ -341,7 +375,7 @@ PF_D void finalize_step(int64_t t, double M, double bsum, const double (&S)[8], 
 
 PF_D double nt_eval_slot(int off, double u) {
   double t, sc;
-  const int seg = nt_segment(u, &t, &sc);
+  const int seg = nt_segment_bf(u, &t, &sc);
   const double* c = pf_gtab + off + seg;
   double r = c[GT_DEG * NT_NSEG];
 #pragma unroll
@@ -413,7 +447,10 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
   // the step's tables are constant over the run: stage them while the
   // previous kernel (group build / K4) drains, then wait for its outputs
   int slot_s = -1, slot_t = -1, noff = -1, tab_doubles = 0;
+  __shared__ double s_exp[EXP_TAB];  // 2^(i/64) for exp_moment
+  if (threadIdx.x < EXP_TAB) s_exp[threadIdx.x] = exp2((double)threadIdx.x / EXP_TAB);
   if (FD) tab_doubles = stage_tables<LS, LT>(a.dr.gs, a.dr.gt, a.dr.ntab, slot_s, slot_t, noff);
+  else __syncthreads();
   pdl_wait();
   if (*a.fail) return;
   const bool feedw = a.feed_w != nullptr;
@@ -500,45 +537,9 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
     }
     asm volatile("cp.async.commit_group;");
   };
-  // FD: a batch's draws (Philox block t, filtering.py:273,280,286) go straight
-  // to its stage slot; computed after the previous batch's arithmetic, while
-  // this batch's record gathers are in flight.  The resampling word goes to
-  // global memory for the next step's lookups.
-  auto draws_for = [&](int64_t bi, int buf) {
-#pragma unroll 1
-    for (int b = 0; b < STEP_SB; ++b) {
-      const int64_t j = bi * batch + b * (int64_t)nth + threadIdx.x;
-      if (bi >= nbatches || j >= a.n) continue;
-      const Philox4 P = philox_block(a.dr.seed, (uint64_t)(a.dr.gbase + j), (uint64_t)a.t);
-      a.dr.u3[j] = P.w[3];
-      // tables only (FD runs with gamma_method 0): no call into the
-      // accurate solvers, which would cost the kernel a stack frame
-      if (!a.z) *val_at(buf, 0, b) = nt_eval_slot(noff, unit_open(P.w[0]));
-      if (LS && !a.g_s) *val_at(buf, 1, b) = gamma_table_slot(slot_s, unit_open(P.w[1]));
-      if (LT && !a.g_t) *val_at(buf, 2, b) = gamma_table_slot(slot_t, unit_open(P.w[2]));
-    }
-  };
-  int cur = 0;
-  int64_t bi = blockIdx.x;
-  uint64_t w3n[STEP_SB];
-  load_w3(bi, w3n);
-  if (bi < nbatches) issue(bi, 0, w3n);
-  if (FD) draws_for(bi, 0);
-  load_w3(bi + gridDim.x, w3n);
-  for (; bi < nbatches; bi += gridDim.x) {
-    if (bi + gridDim.x < nbatches) {
-      issue(bi + gridDim.x, cur ^ 1, w3n);
-      load_w3(bi + 2 * (int64_t)gridDim.x, w3n);
-    } else {
-      asm volatile("cp.async.commit_group;");
-    }
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
-#pragma unroll 1
-  for (int b = 0; b < STEP_SB; ++b) {
-    const int64_t j = bi * batch + b * (int64_t)nth + threadIdx.x;
-    if (j >= a.n) continue;
-    const Rec r = *rec_at(cur, b);
-    const double z = *val_at(cur, 0, b);
+  // One slot's arithmetic (filtering.py:272-298,345): propagate, sufficient
+  // statistics, log-weight, quantile keys, moment partials.
+  auto slot_math = [&](int64_t j, const Rec& r, double z, double gsd, double gtd) {
     const double sq = LT ? sqrt(r.tau2) : a.sqrt_tau2_fixed;
     const double step = sq * z;
     double xn = r.x + step;
@@ -552,11 +553,11 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
     double s2 = a.sigma2_fixed, t2 = a.tau2_fixed;
     if (LS) {
       o.bs = r.bs + h;
-      s2 = o.bs / *val_at(cur, 1, b);
+      s2 = o.bs / gsd;
     }
     if (LT) {
       o.bt = r.bt + (0.5 * step) * step;
-      t2 = o.bt / *val_at(cur, 2, b);
+      t2 = o.bt / gtd;
     }
     o.tau2 = t2;
     a.rec_out[j] = o;
@@ -579,10 +580,8 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
         s0 *= sc; sx *= sc; s2x *= sc; s1s *= sc; s2s *= sc; s1t *= sc; s2t *= sc; s2w *= sc * sc;
         m = lw;
         e = 1.0;
-      } else if (lw > -INFINITY) {
-        e = exp(lw - m);
       } else {
-        e = 0.0;
+        e = lw > -INFINITY ? exp_moment(lw - m, s_exp) : 0.0;
       }
     }
     if (a.kx) a.kx[j] = key_rd_(xn);
@@ -599,8 +598,51 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
     s2s = fma(eds, ds, s2s);
     s1t += edt;
     s2t = fma(edt, dt, s2t);
-  }
-    if (FD) draws_for(bi + gridDim.x, cur ^ 1);
+  };
+  int cur = 0;
+  int64_t bi = blockIdx.x;
+  uint64_t w3n[STEP_SB];
+  load_w3(bi, w3n);
+  if (bi < nbatches) issue(bi, 0, w3n);
+  load_w3(bi + gridDim.x, w3n);
+  for (; bi < nbatches; bi += gridDim.x) {
+    if (bi + gridDim.x < nbatches) {
+      issue(bi + gridDim.x, cur ^ 1, w3n);
+      load_w3(bi + 2 * (int64_t)gridDim.x, w3n);
+    } else {
+      asm volatile("cp.async.commit_group;");
+    }
+    // FD: this batch's draws (Philox block t, filtering.py:273,280,286) in
+    // registers, computed while its record gathers (issued one iteration
+    // earlier) are still in flight; the slots' Philox networks and the three
+    // table polynomials are independent chains the scheduler interleaves.
+    // The resampling word goes to memory for the next step's lookups.
+    double dz[STEP_SB], dgs[STEP_SB], dgt[STEP_SB];
+    if (FD) {
+#pragma unroll
+      for (int b = 0; b < STEP_SB; ++b) {
+        const int64_t j = bi * batch + b * (int64_t)nth + threadIdx.x;
+        const Philox4 P = philox_block(a.dr.seed, (uint64_t)(a.dr.gbase + j), (uint64_t)a.t);
+        if (j < a.n) a.dr.u3[j] = P.w[3];
+        // tables only (FD runs with gamma_method 0): no call into the
+        // accurate solvers, which would cost the kernel a stack frame
+        dz[b] = nt_eval_slot(noff, unit_open(P.w[0]));
+        dgs[b] = LS ? gamma_table_slot(slot_s, unit_open(P.w[1])) : 1.0;
+        dgt[b] = LT ? gamma_table_slot(slot_t, unit_open(P.w[2])) : 1.0;
+      }
+    }
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+#pragma unroll
+    for (int b = 0; b < STEP_SB; ++b) {
+      const int64_t j = bi * batch + b * (int64_t)nth + threadIdx.x;
+      if (j >= a.n) continue;
+      // drawn here (FD) unless an oracle feed was staged; precomputed draws
+      // (draws kernel) are staged too
+      const double z = (FD && !a.z) ? dz[b] : *val_at(cur, 0, b);
+      const double gsd = !LS ? 1.0 : (FD && !a.g_s) ? dgs[b] : *val_at(cur, 1, b);
+      const double gtd = !LT ? 1.0 : (FD && !a.g_t) ? dgt[b] : *val_at(cur, 2, b);
+      slot_math(j, *rec_at(cur, b), z, gsd, gtd);
+    }
     cur ^= 1;
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
