@@ -268,6 +268,9 @@ def main():
     ap.add_argument("--n-shard", type=int, default=None,
                     help="particles of the sharded filter (default: world x --n, weak scaling)")
     ap.add_argument("--shards", type=int, default=1)
+    ap.add_argument("--resampler", default="cutpoint", choices=["cutpoint", "spacings"],
+                    help="cutpoint: the reference's exact parallel resampler (parity path); spacings: "
+                         "the K7 ordered-uniform perf mode (exact multinomial, streaming gathers)")
     ap.add_argument("--process-group", action="store_true",
                     help="run the one-process-per-GPU sharded path even with one rank")
     args = ap.parse_args()
@@ -289,7 +292,8 @@ def main():
     backend = P.Backend("cuda", device=local)
     # first call: engine creation + gamma tables (excluded, like the
     # reference bench's numba warm-up, bench.py:153-161)
-    P.run_particle_learning(P.Priors(), y, n, seed=0, backend=backend, track_quantiles=False)
+    P.run_particle_learning(P.Priors(), y, n, seed=0, backend=backend, track_quantiles=False,
+                            resampler=args.resampler)
     eng = next(iter(backend._engines.values()))
     cfg = eng.cfg
     for _ in range(args.warmup):
@@ -314,7 +318,7 @@ def main():
     t0 = time.perf_counter()
     for _ in range(args.steps):
         out = P.run_particle_learning(P.Priors(), y, n, seed=0, backend=backend,
-                                      track_quantiles=False)
+                                      track_quantiles=False, resampler=args.resampler)
         _ = out.param_posterior["sigma2"].mean[-1]
     e2e_s = max_over_ranks(time.perf_counter() - t0, world)
     e2e = world * n * t_len * args.steps / e2e_s
@@ -336,7 +340,7 @@ def main():
             "value": value, "unit": "particle-steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"PL trend+noise, Priors(), cutpoint, N=2^{n.bit_length() - 1}, "
+            "config": {"workload": f"PL trend+noise, Priors(), {args.resampler}, N=2^{n.bit_length() - 1}, "
                                    f"T={t_len}, seed 0, track_quantiles=False",
                        "N": n, "T": t_len, "parallelism": f"replicas x{world}",
                        "l2": "working set >> L2 (no flush needed)"},
@@ -382,7 +386,8 @@ def run_sharded(args, world, rank, local):
         where = f"{G} shards on GPU {local} (one process)"
 
     def once():
-        return P.run_particle_learning(P.Priors(), y, n, seed=0, backend=backend, track_quantiles=False)
+        return P.run_particle_learning(P.Priors(), y, n, seed=0, backend=backend, track_quantiles=False,
+                                       resampler=args.resampler)
 
     once()
     eng = next(iter(backend._engines.values()))
@@ -415,7 +420,7 @@ def run_sharded(args, world, rank, local):
             "higher_is_better": True, "scaling": "strong" if (world > 1 and fixed_total) else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": f"PL trend+noise, Priors(), cutpoint, N=2^{n.bit_length() - 1} sharded "
+            "config": {"workload": f"PL trend+noise, Priors(), {args.resampler}, N=2^{n.bit_length() - 1} sharded "
                                    f"over {G} shards, T={t_len}, seed 0, track_quantiles=False",
                        "N": n, "T": t_len, "parallelism": where,
                        "l2": "working set >> L2 (no flush needed)"},

@@ -85,9 +85,16 @@ typedef struct pf_config {
 
 /* Resampling schemes (filtering.py:305-317, resampling.py:29-177).  The
  * baselines run on the reference's sequential CDF (a left-to-right cumsum,
- * prefix_sum.py:130-134) and accept any n >= 1; cutpoint needs a power of 2. */
+ * prefix_sum.py:130-134) and accept any n >= 1; cutpoint needs a power of 2.
+ * PF_RESAMPLE_SPACINGS (perf mode, not in the reference) is exact multinomial
+ * resampling like the reference's `sorted` (resampling.py:57-67), but its
+ * sorted uniforms are generated in order -- U_(k) = S_k / S_(N+1), S the
+ * prefix sums of standard exponentials drawn from each slot's Philox word 3
+ * -- and looked up in the cut-point tables, so ancestors are nondecreasing in
+ * the slot: record gathers stream, and a shard's ancestors stay in the shard
+ * except at its boundaries.  Power of 2 like cutpoint. */
 enum { PF_RESAMPLE_CUTPOINT = 0, PF_RESAMPLE_NAIVE = 1, PF_RESAMPLE_SORTED = 2,
-       PF_RESAMPLE_STRATIFIED = 3, PF_RESAMPLE_SYSTEMATIC = 4 };
+       PF_RESAMPLE_STRATIFIED = 3, PF_RESAMPLE_SYSTEMATIC = 4, PF_RESAMPLE_SPACINGS = 5 };
 
 /* Oracle mode: host arrays [T+1][n] (row 0 = initialisation) that replace the
  * ndtri / gammaincinv outputs (and optionally the normalised weights) with

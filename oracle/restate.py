@@ -336,6 +336,47 @@ def cutpoint_indices(q, cuts, u):
     return k
 
 
+# --------------------------------- K7 ordered uniforms (perf mode, B200) ---
+SPACINGS_STREAM = AUX_STREAM_BASE + 2
+
+
+def spacings_uniforms(words, seed, t):
+    """The ordered uniforms of the B200 `spacings` resampler (csrc/cdf.cuh K7;
+    not a reference algorithm -- a restatement of ours, checked statistically
+    against the reference's exact `sorted` scheme, resampling.py:57-67):
+    E_j = -log(unit_open(w3_j)), S = cumsum(E), E_aux from stream 2^62+2
+    block t word 0, U_k = S_k / (S_N + E_aux), snapped to the odd 53-bit grid
+    of unit_open (K = floor(U 2^53) | 1)."""
+    e = -np.log(unit_open(np.asarray(words, dtype=np.uint64)))
+    s = np.cumsum(e)
+    aux = -math.log(float(unit_open(block_words(seed, np.array([SPACINGS_STREAM], dtype=np.uint64), t)[0])[0]))
+    u = s * (1.0 / (s[-1] + aux))
+    k = np.floor(u * 2.0 ** 53).astype(np.uint64) | np.uint64(1)
+    k = np.minimum(k, np.uint64(2 ** 53 - 1))
+    return k.astype(np.float64) * 2.0 ** -53
+
+
+def spacings_uniforms_shard(words_local, totals, shard, seed, t):
+    """Sharded K7 (csrc/cdf.cuh spacings_words_kernel): shard `shard` scans its
+    own exponentials; `totals` are every shard's sums (exchanged), giving its
+    offset and the grand total S_(N+1) = sum(totals) + E_aux."""
+    e = -np.log(unit_open(np.asarray(words_local, dtype=np.uint64)))
+    s = np.cumsum(e)
+    off = float(sum(totals[:shard]))
+    tot = float(sum(totals))
+    aux = -math.log(float(unit_open(block_words(seed, np.array([SPACINGS_STREAM], dtype=np.uint64), t)[0])[0]))
+    u = (off + s) * (1.0 / (tot + aux))
+    k = np.floor(u * 2.0 ** 53).astype(np.uint64) | np.uint64(1)
+    k = np.minimum(k, np.uint64(2 ** 53 - 1))
+    return k.astype(np.float64) * 2.0 ** -53
+
+
+def spacings_indices(q, cuts, words, seed, t):
+    """1-based ancestors of the spacings resampler: the cut-point lookup of the
+    ordered uniforms (nondecreasing in the slot)."""
+    return cutpoint_indices(q, cuts, spacings_uniforms(words, seed, t))
+
+
 # ------------------------------------------- sequential baselines (CPU) ---
 def sequential_cdf(w):
     """prefix_sum.py:130-134: plain left-to-right cumsum (in the weights'
@@ -493,12 +534,14 @@ def run_loop(y, n, seed=0, *, x0_mean=0.0, x0_var=10.0,
         w_sum = float(wts.sum(dtype=np.float64))
         # cutpoint: the adder tree; the baselines: a sequential cumsum
         # (filtering.py:299-302)
-        q = tree_cdf(wts, lanes) if resampler == "cutpoint" else sequential_cdf(wts)
+        q = tree_cdf(wts, lanes) if resampler in ("cutpoint", "spacings") else sequential_cdf(wts)
         if q is None:
             raise Degenerate(t)
         # resample (filtering.py:305-317) with u = slot 3 of block t
         u = unit_open(wt[3])
-        if resampler == "cutpoint":  # resampling.py:161-177
+        if resampler == "spacings":  # B200 perf mode (K7)
+            idx = spacings_indices(q, cut_points(q), wt[3], seed, t)
+        elif resampler == "cutpoint":  # resampling.py:161-177
             cuts = cut_points(q)
             idx = np.empty(n, dtype=np.int64)
 

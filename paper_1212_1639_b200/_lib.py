@@ -34,7 +34,7 @@ PF_ERR_OUT_OF_MEMORY = 6
 PF_ERR_NOT_IMPLEMENTED = 7
 PF_DTYPE_F64 = 0
 PF_DTYPE_F32 = 1
-RESAMPLER_CODES = {"cutpoint": 0, "naive": 1, "sorted": 2, "stratified": 3, "systematic": 4}
+RESAMPLER_CODES = {"cutpoint": 0, "naive": 1, "sorted": 2, "stratified": 3, "systematic": 4, "spacings": 5}
 
 _dp = C.POINTER(C.c_double)
 _i64p = C.POINTER(C.c_int64)

@@ -721,6 +721,70 @@ __global__ void resample_uniforms_kernel(int scheme, const uint64_t* __restrict_
   }
 }
 
+// --------------------------------------- K7: ordered uniforms (spacings) ---
+// Perf-mode exact multinomial resampling (PF_RESAMPLE_SPACINGS).  The
+// reference's `sorted` scheme (resampling.py:57-67) sorts N uniforms and
+// merges them against the CDF (merge_indices, :29-36).  Here the sorted
+// uniforms are produced in order without a sort: with E_1..E_(N+1) i.i.d.
+// standard exponentials and S_k = E_1 + ... + E_k, (S_1, ..., S_N) / S_(N+1)
+// are distributed as the order statistics of N uniforms.  E_j comes from slot
+// j's resampling word (Philox word 3 of block t, the word cutpoint uses) and
+// E_(N+1) from the aux stream SPACINGS_STREAM; the scan is one pass over the
+// words (device prefix sum).  The ordered uniform of slot k is handed to the
+// next step as a resampling word (u = K 2^-53, K odd: the cut-point lookup's
+// input), so the lookup machinery is shared with cutpoint -- and because the
+// uniforms are nondecreasing in k, so are the ancestors: the step kernel's
+// record gathers stream instead of landing on random 128 B atoms, and in a
+// sharded run a shard's ancestors lie in the shard except at its ends.
+constexpr uint64_t SPACINGS_STREAM = (1ull << 62) + 2;  // aux stream (rng.py:34 numbering)
+
+struct ExpOfWord {  // E_j = -log(unit_open(w3_j)), a standard exponential
+  const uint64_t* w3;
+  __host__ __device__ double operator()(int64_t j) const { return -log(unit_open(w3[j])); }
+};
+
+PF_HD double spacings_aux_exp(uint64_t seed, int64_t t) {
+  const Philox4 P = philox_block(seed, SPACINGS_STREAM, (uint64_t)t);
+  return -log(unit_open(P.w[0]));
+}
+
+// Resampling word of the ordered uniform U = S / S_tot: K = floor(U 2^53) | 1
+// (odd, < 2^53), stored so that unit_open(word) = K 2^-53.
+PF_D uint64_t spacings_word(double S, double inv_tot) {
+  uint64_t K = (uint64_t)(S * inv_tot * 9007199254740992.0);
+  K |= 1ull;
+  if (K > 9007199254740991ull) K = 9007199254740991ull;
+  return (K >> 1) << 12;
+}
+
+// words[j] for a shard's slots: S_local (inclusive prefix sums over the
+// shard), the shard's offset (sum of the earlier shards' E totals) and the
+// grand total S_(N+1) (all shards' totals + the aux exponential).  One device
+// / one shard: offset 0, totals = {S_local[n-1]}.
+__global__ void spacings_words_kernel(const double* __restrict__ S, int64_t n, const double* __restrict__ totals,
+                                      int nshards, int shard, uint64_t seed, int64_t t, uint64_t* __restrict__ words,
+                                      const int64_t* __restrict__ fail) {
+  if (fail && *fail) return;
+  double off = 0.0, tot = 0.0;
+  for (int h = 0; h < nshards; ++h) {  // fixed order: identical on every shard
+    const double th = totals ? __ldcg(totals + h) : S[n - 1];
+    if (h < shard) off += th;
+    tot += th;
+  }
+  tot += spacings_aux_exp(seed, t);
+  const double inv = 1.0 / tot;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    words[j] = spacings_word(off + S[j], inv);
+}
+
+// Sharded K7: the shard's exponential total goes into its exchange record
+// (after its scan; the record itself was written by its step kernel).
+template <typename XRec>
+__global__ void spacings_shard_total_kernel(const double* __restrict__ S, int64_t ns, XRec* xrec, int shard) {
+  xrec[shard].se = S[ns - 1];
+  __threadfence_system();
+}
+
 // merge_indices (resampling.py:29-36): searchsorted(q, u, 'right'), 0-based.
 template <typename T>
 __global__ void merge_kernel(const T* __restrict__ q, int64_t n, const double* __restrict__ u, int64_t m,

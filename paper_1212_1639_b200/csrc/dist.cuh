@@ -279,6 +279,11 @@ struct ShardOps {
     }
     a.srk.B = 53 - ilog2(c.n);
     a.srk.on = s->rank_on && t > 1;
+    const bool spacings = c.resampler == PF_RESAMPLE_SPACINGS;  // K7: ordered uniforms
+    if (spacings && t > 1) {  // words of step t-1 from its scan and every rank's total
+      a.spS = e->spS.p;
+      a.sp_tot = e->sptot.p + (size_t)((t - 1) & 1) * PF_MAX_SHARDS;
+    }
     if (FDm) {
       a.dr.n = ns;
       a.dr.t = t;
@@ -299,6 +304,16 @@ struct ShardOps {
         int rc = draws(s, t + 1);
         if (rc != PF_OK) return rc;
       }
+    }
+    if (spacings) {
+      // K7: this rank's prefix sums of its step-t exponentials; the total
+      // rides in its exchange record (all-gathered after phase 1)
+      auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0),
+                                                ExpOfWord{e->du3.p + (size_t)par * ns});
+      size_t tb = e->sptmp_bytes;
+      CK(cub::DeviceScan::InclusiveSum(e->sptmp.p, tb, it, e->spS.p, (int)ns, e->st));
+      spacings_shard_total_kernel<<<1, 1, 0, e->st>>>(e->spS.p, ns, s->xrec, s->rank);
+      g_launches.fetch_add(2);
     }
     if (s->out && s->out->indices && t > 1)
       CK(cudaMemcpyAsync(s->out->indices + (size_t)(t - 2) * ns, e->idx.p, ns * sizeof(int64_t),
@@ -321,7 +336,9 @@ struct ShardOps {
     so.ess = e->o_ess.p;
     double* qmom = (s->rank == 0 && s->ntg) ? &(s->q_sh + par)->mean[0] : nullptr;
     combine_kernel<MODE><<<1, 256, 0, e->st>>>(s->xrec, s->world, t, 0, so, qmom, e->sc.p, e->mbuf.p + par,
-                                               e->fail.p);
+                                               e->fail.p,
+                                               s->cfg.resampler == PF_RESAMPLE_SPACINGS
+                                                   ? e->sptot.p + (size_t)(t & 1) * PF_MAX_SHARDS : nullptr);
     LAUNCHED();
     const CdfPlan plan = cdf_plan(ns);
     WSrc w;
@@ -505,6 +522,13 @@ struct ShardOps {
       m.t = T;
       m.seed = c.seed;
       m.u3 = e->du3.p + (size_t)(T & 1) * ns;
+      if (c.resampler == PF_RESAMPLE_SPACINGS) {
+        spacings_words_kernel<<<grid_for(ns, 256), 256, 0, e->st>>>(
+            e->spS.p, ns, e->sptot.p + (size_t)(T & 1) * PF_MAX_SHARDS, s->world, s->rank, c.seed, T, e->spw.p,
+            e->fail.p);
+        LAUNCHED();
+        m.u3 = e->spw.p;
+      }
       m.slk.G = s->world;
       m.slk.lg = s->lg;
       m.slk.n = c.n;

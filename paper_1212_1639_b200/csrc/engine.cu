@@ -9,6 +9,8 @@
 // and checks the device status word once, after the loop.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 #include <cuda_profiler_api.h>
 
 #include <algorithm>
@@ -80,6 +82,10 @@ struct DevBuf {
 // early-resident K4 / group / step CTAs cost the concurrent quantile work
 // more than the hidden launch latency saves.
 enum { PDL_STEP = 1, PDL_K2 = 2, PDL_K3 = 4, PDL_K4 = 8, PDL_GRP = 16 };
+// cutpoint and the K7 ordered-uniform resampler share the tree CDF and the
+// cut-point / rank tables
+inline bool uses_cut_tables(int r) { return r == PF_RESAMPLE_CUTPOINT || r == PF_RESAMPLE_SPACINGS; }
+
 int pdl_enabled() {
   static const int on = [] {
     const char* v = getenv("PF_PDL");
@@ -462,6 +468,15 @@ struct pf_engine {
   bool strata = false;
   DevBuf<int64_t> idx;
   // baseline resamplers: ancestors of the step, slot uniforms, sort buffers
+  // K7 ordered-uniform resampler (PF_RESAMPLE_SPACINGS): prefix sums of the
+  // slot exponentials, the next step's resampling words, scan scratch
+  DevBuf<double> spS;
+  DevBuf<uint64_t> spw;
+  DevBuf<double> sptot;  // sharded: every shard's exponential total, [2 parities][PF_MAX_SHARDS]
+  DevBuf<unsigned char> sptmp;
+  size_t sptmp_bytes = 0;
+  cudaStream_t spst = nullptr;                        // the scan runs here, beside K2-K4
+  cudaEvent_t ev_spk = nullptr, ev_sp = nullptr;      // step kernel done / scan done
   DevBuf<int32_t> ranc;
   DevBuf<double> ru;
   DevBuf<uint64_t> rsorted;
@@ -655,6 +670,16 @@ GammaSrc gamma_src(pf_engine* e, bool sigma, int64_t t) {
 
 double shape_at(const pf_engine* e, bool sigma, int64_t t) {
   return sigma ? sched_at(e->sched_s, e->cfg.sigma2_shape, t) : sched_at(e->sched_t, e->cfg.tau2_shape, t);
+}
+
+// K7: the resampling words of step t (after its scan) for the store / final
+// resample, on the main stream.
+int spacings_words(pf_engine* e, int64_t t) {
+  CK(cudaStreamWaitEvent(e->st, e->ev_sp, 0));
+  spacings_words_kernel<<<grid_for(e->n, 256), 256, 0, e->st>>>(e->spS.p, e->n, nullptr, 1, 0, e->cfg.seed, t,
+                                                                e->spw.p, e->fail.p);
+  LAUNCHED();
+  return PF_OK;
 }
 
 struct RunSpec {
@@ -857,7 +882,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   const bool fused = c.gamma_method == 0 && e->ntab &&
                      (fused_env >= 0 ? fused_env != 0 : n >= ((int64_t)1 << 22));
   e->last_path = (fused ? PF_PATH_FUSED_DRAWS : 0) | (e->strata ? PF_PATH_RANK_TABLES : 0) |
-                 (c.resampler == PF_RESAMPLE_CUTPOINT && fuse_top() ? PF_PATH_FUSED_TOP : 0);
+                 (uses_cut_tables(c.resampler) && fuse_top() ? PF_PATH_FUSED_TOP : 0);
   const int STEP_THREADS = fused ? FD_THREADS : 256;
   const size_t step_smem = (fused ? (size_t)(((draw_smem / 8) + 3) & ~size_t(3)) * 8 : 0) +
                            (size_t)2 * STEP_SB * STEP_THREADS * (sizeof(Rec) + 3 * sizeof(double));
@@ -921,7 +946,8 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   Lookup<TQ> lk;
   lk.q = qv;
   lk.cut = e->cut.p;
-  lk.anc = c.resampler != PF_RESAMPLE_CUTPOINT ? e->ranc.p : nullptr;
+  lk.anc = !uses_cut_tables(c.resampler) ? e->ranc.p : nullptr;
+  const bool spacings = c.resampler == PF_RESAMPLE_SPACINGS;
   lk.grp = nullptr;
   lk.fq = nullptr;
   lk.f32 = nullptr;
@@ -974,7 +1000,11 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     a.rec_out = e->rec[cur ^ 1].p;
     a.lw = lwp;
     a.Mout = e->mbuf.p + par;
+    // the resampling words of step t-1: the slots' own (cutpoint), or the
+    // ordered uniforms of the spacings pass (K7)
     a.u3 = e->du3.p + (size_t)((t - 1) % 3) * n;
+    a.spS = (spacings && t > 1) ? e->spS.p : nullptr;
+    if (spacings && t > 1) CK(cudaStreamWaitEvent(st, e->ev_sp, 0));  // scan of step t-1
     a.lk = lk;
     a.idx_out = (keep_idx && t > 1) ? e->idx.p : nullptr;
     a.feed_w = row(fw, t);
@@ -1039,6 +1069,21 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     LAUNCHED();
     ++step_launches;
     cur ^= 1;
+    static const bool sp_inline = getenv("PF_SP_INLINE") != nullptr;  // A/B: scan after the CDF chain
+    if (spacings && !sp_inline) {
+      // K7: ordered uniforms of this step's slot words (step kernel t), on
+      // their own stream beside the CDF chain; step t+1 forms its resampling
+      // words from the prefix sums (the scan of step t+1 waits for step
+      // kernel t+1, the last reader of these sums)
+      CK(cudaEventRecord(e->ev_spk, st));
+      CK(cudaStreamWaitEvent(e->spst, e->ev_spk, 0));
+      const uint64_t* w = e->du3.p + (size_t)(t % 3) * n;
+      auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0), ExpOfWord{w});
+      size_t tb = e->sptmp_bytes;
+      CK(cub::DeviceScan::InclusiveSum(e->sptmp.p, tb, it, e->spS.p, (int)n, e->spst));
+      g_launches.fetch_add(1);
+      CK(cudaEventRecord(e->ev_sp, e->spst));
+    }
     if (!fused) {
       CK(cudaEventRecord(e->ev_steps[t % 3], st));
       if (t < T) {
@@ -1064,7 +1109,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       CK(cudaEventRecord(e->ev_b, st));  // K1b(t): keys, log-weights, M, moments
       cudaStream_t ss = e->side;
       CK(cudaStreamWaitEvent(ss, e->ev_b, 0));
-      if (plan.small || c.resampler != PF_RESAMPLE_CUTPOINT) {  // any n (bounds-checked pass)
+      if (plan.small || !uses_cut_tables(c.resampler)) {  // any n (bounds-checked pass)
         q_window_kernel<TQ><<<grid_for(n, 256), 256, 0, ss>>>(wsrc, n, e->fail.p, qa);
         LAUNCHED();
       } else {
@@ -1074,8 +1119,16 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
           return rc;
       }
     }
-    if (c.resampler == PF_RESAMPLE_CUTPOINT) {
+    if (uses_cut_tables(c.resampler)) {
       if ((rc = launch_cdf<TQ>(e->cdf, wsrc, n, qv, e->cut.p, e->fail.p, t, st, so)) != PF_OK) return rc;
+      if (spacings && sp_inline) {
+        const uint64_t* w = e->du3.p + (size_t)(t % 3) * n;
+        auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0), ExpOfWord{w});
+        size_t tb = e->sptmp_bytes;
+        CK(cub::DeviceScan::InclusiveSum(e->sptmp.p, tb, it, e->spS.p, (int)n, st));
+        g_launches.fetch_add(1);
+        CK(cudaEventRecord(e->ev_sp, st));
+      }
     } else {
       // the reference's sequential baselines (filtering.py:299-316): a
       // sequential cumsum CDF, the scheme's uniforms, searchsorted 'right'
@@ -1181,6 +1234,8 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       m.resample = 1;
       m.rec = e->rec[cur].p;
       m.u3 = e->du3.p + (size_t)(t % 3) * n;
+      if (spacings && (rc = spacings_words(e, t)) != PF_OK) return rc;
+      if (spacings) m.u3 = e->spw.p;
       m.lk = lk;
       m.s2_direct = nullptr;
       m.gs = gamma_src(e, true, t);
@@ -1224,6 +1279,8 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     m.resample = 1;
     m.rec = e->rec[cur].p;
     m.u3 = e->du3.p + (size_t)(T % 3) * n;
+    if (spacings && (rc = spacings_words(e, T)) != PF_OK) return rc;
+    if (spacings) m.u3 = e->spw.p;
     m.lk = lk;
     m.s2_direct = nullptr;
     m.gs = gamma_src(e, true, T);
@@ -1477,9 +1534,9 @@ int pf_engine_create(const pf_config* cfg, pf_engine** out) {
   *out = nullptr;
   const int64_t n = cfg->n;
   if (n < 1) return set_err(PF_ERR_VALUE, "particle count must be >= 1");
-  if (cfg->resampler < PF_RESAMPLE_CUTPOINT || cfg->resampler > PF_RESAMPLE_SYSTEMATIC)
+  if (cfg->resampler < PF_RESAMPLE_CUTPOINT || cfg->resampler > PF_RESAMPLE_SPACINGS)
     return set_err(PF_ERR_VALUE, "unknown resampler code");
-  if (cfg->resampler == PF_RESAMPLE_CUTPOINT && !is_pow2(n))
+  if (uses_cut_tables(cfg->resampler) && !is_pow2(n))
     return set_err(PF_ERR_NOT_POWER_OF_TWO, "particle count must be a power of two, got " + std::to_string(n));
   if (n > (int64_t(1) << 28)) return set_err(PF_ERR_VALUE, "particle count above 2^28 per device");
   if (pf_device_count() < 1) return set_err(PF_ERR_CUDA, "no CUDA device visible");
@@ -1529,8 +1586,21 @@ int pf_engine_create(const pf_config* cfg, pf_engine** out) {
       (err = e->sc.ensure(1)) || (err = e->fail.ensure(1)) ||
       (err = e->cdf.ensure(n, e->single ? 4 : 8)) || (err = e->probs.ensure(8)))
     return bail(err);
-  e->strata = cfg->resampler == PF_RESAMPLE_CUTPOINT && ilog2(n) >= STRATA_MIN_LOG2N;
-  if (cfg->resampler != PF_RESAMPLE_CUTPOINT) {
+  e->strata = uses_cut_tables(cfg->resampler) && ilog2(n) >= STRATA_MIN_LOG2N;
+  if (cfg->resampler == PF_RESAMPLE_SPACINGS) {
+    if ((err = e->spS.ensure(n)) || (err = e->spw.ensure(n)) || (err = e->sptot.ensure(2 * PF_MAX_SHARDS)))
+      return bail(err);
+    size_t tb = 0;
+    auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0), ExpOfWord{e->du3.p});
+    cub::DeviceScan::InclusiveSum(nullptr, tb, it, e->spS.p, (int)n);
+    e->sptmp_bytes = tb;
+    if ((err = e->sptmp.ensure(tb))) return bail(err);
+    if ((err = cudaStreamCreateWithFlags(&e->spst, cudaStreamNonBlocking)) ||
+        (err = cudaEventCreateWithFlags(&e->ev_spk, cudaEventDisableTiming)) ||
+        (err = cudaEventCreateWithFlags(&e->ev_sp, cudaEventDisableTiming)))
+      return bail(err);
+  }
+  if (!uses_cut_tables(cfg->resampler)) {
     if ((err = e->ranc.ensure(n)) || (err = e->ru.ensure(n)) || (err = e->rsorted.ensure(n))) return bail(err);
     size_t tb = 0;
     cub::DeviceRadixSort::SortKeys(nullptr, tb, (const uint64_t*)e->ru.p, e->rsorted.p, (int)n);
@@ -1621,8 +1691,8 @@ int pf_group_create(const pf_config* cfg, int32_t nshards, const int32_t* device
   if (!is_pow2(n)) return set_err(PF_ERR_NOT_POWER_OF_TWO, "particle count must be a power of two, got " + std::to_string(n));
   if (G < 1 || G > PF_MAX_SHARDS || !is_pow2(G)) return set_err(PF_ERR_VALUE, "shard count must be 1, 2, 4 or 8");
   if (n / G < 4096) return set_err(PF_ERR_VALUE, "sharded runs need at least 4096 particles per shard");
-  if (cfg->resampler != PF_RESAMPLE_CUTPOINT)
-    return set_err(PF_ERR_NOT_IMPLEMENTED, "sharded runs use the cut-point resampler");
+  if (!uses_cut_tables(cfg->resampler))
+    return set_err(PF_ERR_NOT_IMPLEMENTED, "sharded runs use the cut-point or spacings resampler");
   if (n > ((int64_t)1 << 31)) return set_err(PF_ERR_VALUE, "particle count above 2^31");
   const int ndev = pf_device_count();
   if (ndev < 1) return set_err(PF_ERR_CUDA, "no CUDA device visible");
@@ -1796,8 +1866,8 @@ int pf_shard_create(const pf_config* cfg, int32_t rank, int32_t world, pf_shard*
   if (world < 1 || world > PF_MAX_SHARDS || !is_pow2(world)) return set_err(PF_ERR_VALUE, "world size must be 1, 2, 4 or 8");
   if (rank < 0 || rank >= world) return set_err(PF_ERR_VALUE, "rank out of range");
   if (n / world < 4096) return set_err(PF_ERR_VALUE, "sharded runs need at least 4096 particles per shard");
-  if (cfg->resampler != PF_RESAMPLE_CUTPOINT)
-    return set_err(PF_ERR_NOT_IMPLEMENTED, "sharded runs use the cut-point resampler");
+  if (!uses_cut_tables(cfg->resampler))
+    return set_err(PF_ERR_NOT_IMPLEMENTED, "sharded runs use the cut-point or spacings resampler");
   if (n > ((int64_t)1 << 31)) return set_err(PF_ERR_VALUE, "particle count above 2^31");
   if (pf_device_count() < 1) return set_err(PF_ERR_CUDA, "no CUDA device visible");
   pf_shard* s = new pf_shard();
@@ -2090,6 +2160,16 @@ int pf_engine_destroy(pf_engine* e) {
   e->rec[1].release();
   e->du3.release();
   e->ranc.release();
+  e->spS.release();
+  e->spw.release();
+  e->sptot.release();
+  e->sptmp.release();
+  if (e->spst) {
+    cudaStreamSynchronize(e->spst);
+    cudaStreamDestroy(e->spst);
+  }
+  if (e->ev_spk) cudaEventDestroy(e->ev_spk);
+  if (e->ev_sp) cudaEventDestroy(e->ev_sp);
   e->ru.release();
   e->rsorted.release();
   e->rtmp.release();

@@ -59,6 +59,7 @@ int run_group(pf_group* g, const double* y, int64_t T, pf_outputs* out) {
   const int64_t ns = g->ns, N = c.n;
   pf_engine* e0 = g->sh[0];
   int rc;
+  const bool spacings = c.resampler == PF_RESAMPLE_SPACINGS;  // K7: ordered uniforms
   const bool want_fq = out ? out->filtered_quantiles != nullptr : c.track_quantiles != 0;
   const bool keep_idx = out && out->indices;
   const bool keep_final = out && (out->final_states || out->final_sigma2);
@@ -294,8 +295,22 @@ int run_group(pf_group* g, const double* y, int64_t T, pf_outputs* out) {
       }
       a.srk.B = 53 - ilog2(N);
       a.srk.on = g->rank_on && t > 1;
+      if (spacings && t > 1) {  // words of step t-1 from its scan and every shard's total
+        a.spS = e->spS.p;
+        a.sp_tot = e->sptot.p + (size_t)((t - 1) & 1) * PF_MAX_SHARDS;
+      }
       step_kernel<MODE, TQ><<<step_grid, 256, step_smem, st>>>(a);
       LAUNCHED();
+      if (spacings) {
+        // K7: this shard's prefix sums of its step-t exponentials; its total
+        // joins the exchange record the combine kernels read
+        auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0),
+                                                  ExpOfWord{e->du3.p + (size_t)(t & 1) * ns});
+        size_t tb = e->sptmp_bytes;
+        CK(cub::DeviceScan::InclusiveSum(e->sptmp.p, tb, it, e->spS.p, (int)ns, st));
+        spacings_shard_total_kernel<<<1, 1, 0, st>>>(e->spS.p, ns, g->xrec, s);
+        g_launches.fetch_add(2);
+      }
       CK(cudaEventRecord(g->evA[s], st));
       if (t < T) {
         CK(cudaStreamWaitEvent(e->dstream, g->evA[s], 0));
@@ -321,7 +336,8 @@ int run_group(pf_group* g, const double* y, int64_t T, pf_outputs* out) {
       so.ess = e->o_ess.p;
       double* qmom = (s == 0 && ntg) ? &(e0->qsh.p + par)->mean[0] : nullptr;
       combine_kernel<MODE><<<1, 256, 0, e->st>>>(g->xrec, G, t, 0, so, qmom, e->sc.p, e->mbuf.p + par,
-                                                 e->fail.p);
+                                                 e->fail.p,
+                                                 spacings ? e->sptot.p + (size_t)(t & 1) * PF_MAX_SHARDS : nullptr);
       LAUNCHED();
       if (s == 0) CK(cudaEventRecord(g->evM, e->st));
       // ---- K2 (local) and this shard's subtree total
@@ -490,6 +506,12 @@ int run_group(pf_group* g, const double* y, int64_t T, pf_outputs* out) {
       m.t = T;
       m.seed = c.seed;
       m.u3 = e->du3.p + (size_t)(T & 1) * ns;
+      if (spacings) {
+        spacings_words_kernel<<<grid_for(ns, 256), 256, 0, st>>>(e->spS.p, ns, e->sptot.p + (size_t)(T & 1) * PF_MAX_SHARDS,
+                                                                 G, s, c.seed, T, e->spw.p, e->fail.p);
+        LAUNCHED();
+        m.u3 = e->spw.p;
+      }
       m.slk.G = G;
       m.slk.lg = g->lg;
       m.slk.n = N;

@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(256) init_kernel(InitArgs a) {
 // ---------------------------------------------------------------- step ---
 struct Partial {
   double m, s0, sx, s2x, s1s, s2s, s1t, s2t, s2w, bad;  // s2w: sum of squared weights (ESS)
+  double se;  // K7 (spacings): the shard's sum of slot exponentials (set after its scan)
 };
 
 struct Scalars {
@@ -224,6 +225,9 @@ struct StepArgs {
   DrawArgs dr;           // FD: this step's draws are computed here (tables, seed, u3 out)
   ShardLookup<TQ> slk;   // sharded run (slk.G > 0): cross-shard lookup
   ShardRank srk;         // sharded run: per-shard rank tables (srk.on)
+  const double* spS;     // K7 (spacings): prefix sums of step t-1's slot exponentials -- the
+                         // resampling words are formed from them here instead of read from u3
+  const double* sp_tot;  // sharded K7: every shard's exponential total of step t-1 (slk.G of them)
   int dbg_identity;      // diagnostics only (PF_DEBUG_IDENTITY_ANC): skip the lookup, ancestor = slot
   double ref_slack;      // moment-reference slack (64; 0 = rescale at every new max)
   const Rec* recs[PF_MAX_SHARDS];  // sharded run: every shard's records of step t-1
@@ -484,12 +488,29 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
     return reinterpret_cast<double*>(smem + buf * buf_bytes + (size_t)STEP_SB * nth * sizeof(Rec)) +
            (k * STEP_SB + b) * nth + threadIdx.x;
   };
+  // K7: the ordered uniform of slot j is S_j / S_(N+1) (spacings_words_kernel
+  // forms the same words for the store / final resample)
+  double sp_inv = 0.0, sp_off = 0.0;
+  if (a.spS && a.t > 1) {
+    double tot = 0.0;
+    if (a.sp_tot) {  // sharded: the shard's offset and the grand total, in shard order
+      for (int h = 0; h < a.slk.G; ++h) {
+        const double th = __ldcg(a.sp_tot + h);
+        if (h < a.shard) sp_off += th;
+        tot += th;
+      }
+    } else {
+      tot += __ldcg(a.spS + a.n - 1);
+    }
+    sp_inv = 1.0 / (tot + spacings_aux_exp(a.seed, a.t - 1));
+  }
   // resampling words are loaded one pipeline stage ahead of their lookups
   auto load_w3 = [&](int64_t bi, uint64_t (&w3)[STEP_SB]) {
 #pragma unroll
     for (int b = 0; b < STEP_SB; ++b) {
       const int64_t j = bi * batch + b * (int64_t)nth + threadIdx.x;
-      w3[b] = (a.t > 1 && bi < nbatches && j < a.n) ? __ldcs(a.u3 + j) : 0ull;
+      const bool live = a.t > 1 && bi < nbatches && j < a.n;
+      w3[b] = !live ? 0ull : a.spS ? spacings_word(sp_off + __ldcs(a.spS + j), sp_inv) : __ldcs(a.u3 + j);
     }
   };
   auto issue = [&](int64_t bi, int buf, const uint64_t (&w3)[STEP_SB]) {
@@ -704,6 +725,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
     p.s0 = S[0]; p.sx = S[1]; p.s2x = S[2]; p.s1s = S[3]; p.s2s = S[4]; p.s1t = S[5]; p.s2t = S[6];
     p.s2w = S[7];
     p.bad = bsum;
+    p.se = 0.0;
     a.xrec[a.shard] = p;
     __threadfence_system();
     a.sc->counter = 0;
@@ -717,9 +739,11 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
 template <int MODE>
 __global__ void __launch_bounds__(256) combine_kernel(const Partial* __restrict__ xrec, int G, int64_t t,
                                                       int feedw, StepOut out, double* qmom, Scalars* sc,
-                                                      double* Mout, int64_t* fail) {
+                                                      double* Mout, int64_t* fail, double* sp_tot = nullptr) {
   constexpr bool LS = MODE & M_LS, LT = MODE & M_LT;
   if (*fail) return;
+  // K7: keep every shard's exponential total of step t for step t+1's words
+  if (sp_tot && (int)threadIdx.x < G) sp_tot[threadIdx.x] = __ldcg(&xrec[threadIdx.x].se);
   __shared__ double red[8][10];
   const double cs = sc->cs, ct = sc->ct, cx = sc->cx;
   double M, bsum, S[8];

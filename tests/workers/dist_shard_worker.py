@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--kind", default="learning", choices=["learning", "filter", "single", "degenerate"])
     ap.add_argument("--same-gpu", action="store_true")
     ap.add_argument("--runs", type=int, default=1)
+    ap.add_argument("--resampler", default="cutpoint")
     a = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dev = 0 if a.same_gpu else local
@@ -54,7 +55,8 @@ def main():
             else:
                 prec = "single" if a.kind == "single" else "double"
                 o = P.run_particle_learning(P.Priors(), y, a.particles, seed=seed, backend=b, keep_indices=True,
-                                            keep_final=True, track_quantiles=True, precision=prec)
+                                            keep_final=True, track_quantiles=True, precision=prec,
+                                            resampler=a.resampler)
             res[f"indices{r}"] = o.resampled_indices
             res[f"states{r}"] = o.final_particles.states
             res[f"fmean{r}"] = o.filtered_mean
