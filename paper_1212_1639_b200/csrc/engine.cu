@@ -1175,33 +1175,12 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       vs.learn_s = LS;
       vs.learn_t = LT;
       double *ox = e->o_fq.p, *os = e->o_sq.p, *ot = e->o_tq.p;
-      const int hgrid = std::max(1, std::min(64, (int)((n / 64 + 255) / 256)));
       static DevOnce resolve_attr;
       if (resolve_attr.pending()) {
         CK(cudaFuncSetAttribute(q_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 Q_RESOLVE_SMEM));
+        CK(cudaFuncSetAttribute(q_round_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Q_RESOLVE_SMEM));
         resolve_attr.mark();
-      }
-      for (int round = 0; round < 2; ++round) {
-        q_hist_kernel<<<dim3(hgrid, ntg), 256, 0, ss>>>(qa, e->fail.p, round);
-        q_locate_kernel<<<ntg, 1024, 0, ss>>>(qa, e->fail.p, round);
-        q_filter_kernel<<<dim3(hgrid, ntg), 256, 0, ss>>>(qa, e->fail.p);
-        q_finish_kernel<<<ntg, 1024, Q_RESOLVE_SMEM, ss>>>(qa, vs, ox, os, ot, t, e->fail.p);
-        g_launches.fetch_add(2);
-        if (round == 0) {
-          // misses: bounded re-window (attempt 0), whole side (attempt 1)
-          for (int attempt = 0; attempt < 2; ++attempt) {
-            q_fallback_prep_kernel<<<1, 32, 0, ss>>>(qa, attempt, e->fail.p);
-            if ((rc = fb_hist_smem()) != PF_OK) return rc;
-            q_fallback_hist_kernel<<<fb_hist_grid(n), 256, QFB_SMEM_BYTES, ss>>>(qa, lwp, wsrc.mode, wsrc.M, n, SINGLE, attempt,
-                                                            e->fail.p);
-            q_fallback_select_kernel<<<ntg, 1024, 0, ss>>>(qa, attempt, e->fail.p);
-            g_launches.fetch_add(3);
-          }
-          q_fallback_fill_kernel<<<fb_grid, 256, 0, ss>>>(qa, lwp, wsrc.mode, wsrc.M, n, SINGLE, e->fail.p);
-          g_launches.fetch_add(1);
-        }
-        g_launches.fetch_add(2);
       }
       QAll all;
       memset(&all, 0, sizeof(all));
@@ -1212,9 +1191,53 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       all.M[0] = wsrc.M;
       all.wmode = wsrc.mode;
       all.single = SINGLE;
-      q_select_kernel<<<ntg, 1024, 0, ss>>>(qa, vs, e->qscratch.p, ox, os, ot, t, e->fail.p, e->qunres.p, all);
+      // Small n (<= 2^22 by default, PF_FUSED_RESOLVE_LOG2N): the resolve
+      // rounds as one CTA per target (q_round_kernel), 8 launches fewer per
+      // step -- the side chain's launch latency is what bounds small filters.
+      // Large n: the gridded histogram / filter passes (their candidate
+      // lists are long), measured faster there.
+      static const int fused_log2n = [] {
+        const char* v = getenv("PF_FUSED_RESOLVE_LOG2N");
+        return v ? atoi(v) : 22;
+      }();
+      const bool fused_resolve = ilog2(n) <= fused_log2n;
+      const int hgrid = std::max(1, std::min(64, (int)((n / 64 + 255) / 256)));
+      for (int round = 0; round < 2; ++round) {
+        if (fused_resolve) {
+          // histogram, locate, filter, exact finish; round 0 adds the fallback
+          // interval of a target whose window missed, round 1 the exact select
+          // of a target still unresolved
+          q_round_kernel<<<ntg, 1024, Q_RESOLVE_SMEM, ss>>>(qa, vs, e->qscratch.p, ox, os, ot, t, e->fail.p, round,
+                                                            e->qunres.p, all);
+          g_launches.fetch_add(1);
+        } else {
+          q_hist_kernel<<<dim3(hgrid, ntg), 256, 0, ss>>>(qa, e->fail.p, round);
+          q_locate_kernel<<<ntg, 1024, 0, ss>>>(qa, e->fail.p, round);
+          q_filter_kernel<<<dim3(hgrid, ntg), 256, 0, ss>>>(qa, e->fail.p);
+          q_finish_kernel<<<ntg, 1024, Q_RESOLVE_SMEM, ss>>>(qa, vs, ox, os, ot, t, e->fail.p);
+          g_launches.fetch_add(4);
+        }
+        if (round == 0) {
+          // misses only (the kernels exit at once otherwise): bounded re-window
+          // (attempt 0), whole side (attempt 1), candidate refill
+          for (int attempt = 0; attempt < 2; ++attempt) {
+            if (!fused_resolve) q_fallback_prep_kernel<<<1, 32, 0, ss>>>(qa, attempt, e->fail.p);
+            if ((rc = fb_hist_smem()) != PF_OK) return rc;
+            q_fallback_hist_kernel<<<fb_hist_grid(n), 256, QFB_SMEM_BYTES, ss>>>(qa, lwp, wsrc.mode, wsrc.M, n,
+                                                                                 SINGLE, attempt, e->fail.p);
+            q_fallback_select_kernel<<<ntg, 1024, 0, ss>>>(qa, attempt, e->fail.p, fused_resolve && attempt == 0);
+            g_launches.fetch_add(fused_resolve ? 2 : 3);
+          }
+          q_fallback_fill_kernel<<<fb_grid, 256, 0, ss>>>(qa, lwp, wsrc.mode, wsrc.M, n, SINGLE, e->fail.p);
+          g_launches.fetch_add(1);
+        }
+      }
+      if (!fused_resolve) {
+        q_select_kernel<<<ntg, 1024, 0, ss>>>(qa, vs, e->qscratch.p, ox, os, ot, t, e->fail.p, e->qunres.p, all);
+        g_launches.fetch_add(1);
+      }
       q_step_end_kernel<<<1, 1024, 0, ss>>>(qa, 1);
-      g_launches.fetch_add(2);
+      g_launches.fetch_add(1);
       CK(cudaEventRecord(e->ev_q[t & 1], ss));
     }
     mark(PH_CDF);

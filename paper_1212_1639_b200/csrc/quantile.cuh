@@ -718,20 +718,25 @@ PF_D unsigned long long block_exclusive_scan(unsigned long long* a, int n) {
   return total;
 }
 
-// R1: fixed-point sub-bin histogram of every target's candidates.
-__global__ void __launch_bounds__(256) q_hist_kernel(QArgs qa, const int64_t* fail, int fallback_round) {
-  if (*fail) return;
-  const int k = blockIdx.y;
-  if (k >= qa.ntarget) return;
+// R1: fixed-point sub-bin histogram of target k's candidates (threads i0,
+// i0 + stride, ... of the caller's launch).
+PF_D void q_hist_dev(const QArgs& qa, int k, int fallback_round, uint32_t i0, uint32_t stride) {
   QTarget& t = qa.tg[k];
   if (fallback_round && t.status != QS_REFILL) return;
   const uint32_t n = min(t.count, qa.cap);
   const uint32_t lo = t.klo, hi = t.khi;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+  for (uint32_t i = i0; i < n; i += stride) {
     const QCand c = qa.cand[(size_t)k * qa.cap + i];
     const uint32_t b = sub_bin(c.key, lo, hi, Q_SUB);
     atomicAdd(&qa.hist[(size_t)k * Q_SUB + b], (unsigned long long)llrint(c.w * qa.fx_scale));
   }
+}
+
+__global__ void __launch_bounds__(256) q_hist_kernel(QArgs qa, const int64_t* fail, int fallback_round) {
+  if (*fail) return;
+  const int k = blockIdx.y;
+  if (k >= qa.ntarget) return;
+  q_hist_dev(qa, k, fallback_round, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
 // Bitonic sort of (value, idx, w) triples in shared memory, ascending by
@@ -758,10 +763,7 @@ PF_D void bitonic_sort(double* v, uint32_t* id, double* w, int n2) {
 // R2a: one CTA per target.  Prefix the sub-bin histogram, classify the
 // window (hit / miss low / miss high / overflow), locate the crossing
 // sub-bin b* and the exact-enough weight below its left neighbour.
-__global__ void __launch_bounds__(1024)
-q_locate_kernel(QArgs qa, const int64_t* fail, int fallback_round) {
-  if (*fail) return;
-  const int k = blockIdx.x;
+PF_D void q_locate_dev(const QArgs& qa, int k, int fallback_round) {
   QTarget& tg = qa.tg[k];
   if (fallback_round && tg.status != QS_REFILL) return;
   __shared__ unsigned long long pre[Q_SUB + 1];
@@ -770,7 +772,7 @@ q_locate_kernel(QArgs qa, const int64_t* fail, int fallback_round) {
   const double T = tg.p * qa.sh->W;
   const double wb = tg.wbelow;
   const unsigned long long* H = qa.hist + (size_t)k * Q_SUB;
-  for (int b = threadIdx.x; b < Q_SUB; b += blockDim.x) pre[b] = H[b];
+  for (int b = threadIdx.x; b < Q_SUB; b += blockDim.x) pre[b] = __ldcg(H + b);
   __syncthreads();
   const unsigned long long tot = block_exclusive_scan(pre, Q_SUB);
   if (threadIdx.x == 0) {
@@ -802,18 +804,21 @@ q_locate_kernel(QArgs qa, const int64_t* fail, int fallback_round) {
   }
 }
 
+__global__ void __launch_bounds__(1024)
+q_locate_kernel(QArgs qa, const int64_t* fail, int fallback_round) {
+  if (*fail) return;
+  q_locate_dev(qa, blockIdx.x, fallback_round);
+}
+
 // R2b: grid pass over the candidate lists: keep the candidates of sub-bins
 // b*-1 .. b*+1 (a few hundred) for the exact resolve.
-__global__ void __launch_bounds__(256) q_filter_kernel(QArgs qa, const int64_t* fail) {
-  if (*fail) return;
-  const int k = blockIdx.y;
-  if (k >= qa.ntarget) return;
+PF_D void q_filter_dev(const QArgs& qa, int k, uint32_t i0, uint32_t stride) {
   QTarget& t = qa.tg[k];
   if (t.status != QS_LOCATED) return;
   const uint32_t n = min(t.count, qa.cap);
   const int b0 = max(t.bstar - 1, 0), b1 = min(t.bstar + 1, Q_SUB - 1);
   const uint32_t lo = t.klo, hi = t.khi;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+  for (uint32_t i = i0; i < n; i += stride) {
     const QCand c = qa.cand[(size_t)k * qa.cap + i];
     const int b = (int)sub_bin(c.key, lo, hi, Q_SUB);
     if (b >= b0 && b <= b1) {
@@ -826,22 +831,27 @@ __global__ void __launch_bounds__(256) q_filter_kernel(QArgs qa, const int64_t* 
   }
 }
 
+__global__ void __launch_bounds__(256) q_filter_kernel(QArgs qa, const int64_t* fail) {
+  if (*fail) return;
+  const int k = blockIdx.y;
+  if (k >= qa.ntarget) return;
+  q_filter_dev(qa, k, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+}
+
 // R2c: one CTA per target: exact values of the kept candidates, stable
 // (value, index) order, cumulative weight from cum0 -> the quantile; then
 // the window predictor update.
-__global__ void __launch_bounds__(1024)
-q_finish_kernel(QArgs qa, QValueSrc vs, double* out_x, double* out_s, double* out_t, int64_t t_step,
-                const int64_t* fail) {
-  if (*fail) return;
-  const int k = blockIdx.x;
+extern __shared__ unsigned long long qsm[];  // q_finish / q_round dynamic shared memory
+
+PF_D void q_finish_dev(const QArgs& qa, const QValueSrc& vs, double* out_x, double* out_s, double* out_t,
+                       int64_t t_step, int k) {
   QTarget& tg = qa.tg[k];
   if (tg.status != QS_LOCATED) return;
   // dynamic smem: sv[Q_LIST] f64 | sw[Q_LIST] f64 | sid[Q_LIST] u32
-  extern __shared__ unsigned long long qsm[];
   double* sv = reinterpret_cast<double*>(qsm);
   double* sw = sv + Q_LIST;
   uint32_t* sid = reinterpret_cast<uint32_t*>(sw + Q_LIST);
-  const int m = (int)tg.nlist;
+  const int m = (int)__ldcg(&tg.nlist);
   if (m > Q_LIST) {
     if (threadIdx.x == 0) {
       tg.status = QS_CROWD;
@@ -893,15 +903,19 @@ q_finish_kernel(QArgs qa, QValueSrc vs, double* out_x, double* out_s, double* ou
   }
 }
 
+__global__ void __launch_bounds__(1024)
+q_finish_kernel(QArgs qa, QValueSrc vs, double* out_x, double* out_s, double* out_t, int64_t t_step,
+                const int64_t* fail) {
+  if (*fail) return;
+  q_finish_dev(qa, vs, out_x, out_s, out_t, t_step, blockIdx.x);
+}
+
 
 // F0: interval for each target that missed.  Attempt 0 uses a secant
 // estimate from the missing mass, bounded so the histogram pass touches few
 // particles; attempt 1 (only if attempt 0's interval did not hold the
 // crossing either) takes everything on the missing side.
-__global__ void q_fallback_prep_kernel(QArgs qa, int attempt, const int64_t* fail) {
-  if (*fail || !qa.sh->any_miss) return;
-  const int k = threadIdx.x;
-  if (k >= qa.ntarget) return;
+PF_D void q_prep_target(const QArgs& qa, int attempt, int k) {
   QTarget& t = qa.tg[k];
   const uint32_t st = t.status;
   const double W = qa.sh->W, T = t.p * W;
@@ -944,6 +958,13 @@ __global__ void q_fallback_prep_kernel(QArgs qa, int attempt, const int64_t* fai
   t.status = QS_FB;
   t.missed = 1;
   qa.sh->fb_active[attempt] = 1;
+}
+
+__global__ void q_fallback_prep_kernel(QArgs qa, int attempt, const int64_t* fail) {
+  if (*fail || !qa.sh->any_miss) return;
+  const int k = threadIdx.x;
+  if (k >= qa.ntarget) return;
+  q_prep_target(qa, attempt, k);
 }
 
 // F1: full pass over the particles for targets in fallback: fixed-point
@@ -1071,7 +1092,8 @@ q_fallback_hist_kernel(QArgs qa, const double* __restrict__ lw, int wmode, const
 // F2: pick the fallback bin holding the crossing; it becomes the new window
 // (one CTA per target).  If the interval does not hold it (attempt 0's
 // bounded guess fell short) the target is marked for attempt 1.
-__global__ void __launch_bounds__(1024) q_fallback_select_kernel(QArgs qa, int attempt, const int64_t* fail) {
+__global__ void __launch_bounds__(1024) q_fallback_select_kernel(QArgs qa, int attempt, const int64_t* fail,
+                                                                  int fuse_prep = 0) {
   if (*fail || !qa.sh->fb_active[attempt]) return;
   const int k = blockIdx.x;
   QTarget& t = qa.tg[k];
@@ -1102,6 +1124,7 @@ __global__ void __launch_bounds__(1024) q_fallback_select_kernel(QArgs qa, int a
   if ((below || above) && attempt == 0 && !(t.ilo == 0 && below) && !(t.ihi == 0xFFFFFFFFu && above)) {
     t.side = below ? -1 : 1;
     t.status = QS_RETRY;
+    if (fuse_prep) q_prep_target(qa, 1, k);  // attempt 1's interval (F0), without its own launch
     return;
   }
   const int b = bsel < Q_FB ? bsel : (below ? 0 : Q_FB - 1);
@@ -1184,11 +1207,9 @@ struct QAll {
 // identical states) is selected exactly over every particle whose key lies
 // in the window, read from `all`; the weights are formed as the candidate
 // passes form them, so the answer is the one the full list would give.
-__global__ void __launch_bounds__(1024)
-q_select_kernel(QArgs qa, QValueSrc vs, double* __restrict__ scratch, double* out_x, double* out_s,
-                double* out_t, int64_t t_step, const int64_t* fail, unsigned int* unresolved, QAll all) {
-  if (*fail || !qa.sh->any_miss) return;
-  const int k = blockIdx.x;
+PF_D void q_select_dev(const QArgs& qa, const QValueSrc& vs, double* __restrict__ scratch, double* out_x,
+                       double* out_s, double* out_t, int64_t t_step, unsigned int* unresolved, const QAll& all,
+                       int k) {
   QTarget& tg = qa.tg[k];
   if (tg.status == QS_OK) return;
   __shared__ unsigned long long hist[256];
@@ -1259,6 +1280,43 @@ q_select_kernel(QArgs qa, QValueSrc vs, double* __restrict__ scratch, double* ou
     o[(t_step - 1) * ncol + tg.col] = v;
     if (over && !exact_all) atomicAdd(unresolved, 1u);  // the host raises on this
     tg.status = QS_OK;
+  }
+}
+
+__global__ void __launch_bounds__(1024)
+q_select_kernel(QArgs qa, QValueSrc vs, double* __restrict__ scratch, double* out_x, double* out_s,
+                double* out_t, int64_t t_step, const int64_t* fail, unsigned int* unresolved, QAll all) {
+  if (*fail || !qa.sh->any_miss) return;
+  q_select_dev(qa, vs, scratch, out_x, out_s, out_t, t_step, unresolved, all, blockIdx.x);
+}
+
+// One step's exact resolve for the single-device engine in two launches
+// instead of eight: one CTA per target runs, in order, the candidate
+// histogram (R1), the crossing location (R2a), the filter (R2b) and the
+// exact stable-order finish (R2c) -- the same device code as the separate
+// kernels, which the sharded runs still launch.  Round 0 then prepares the
+// target's fallback interval if its window missed (F0, attempt 0); round 1
+// (re-windowed targets only) ends with the weighted radix select (S) for a
+// target that is still unresolved.  A target is owned by one CTA from start
+// to end, so the CTA barrier is the only ordering needed.
+__global__ void __launch_bounds__(1024)
+q_round_kernel(QArgs qa, QValueSrc vs, double* __restrict__ scratch, double* out_x, double* out_s, double* out_t,
+               int64_t t_step, const int64_t* fail, int round, unsigned int* unresolved, QAll all) {
+  if (*fail) return;
+  const int k = blockIdx.x;
+  if (round && qa.tg[k].status == QS_OK) return;  // resolved in round 0 (uniform over the CTA)
+  q_hist_dev(qa, k, round, threadIdx.x, blockDim.x);
+  __syncthreads();
+  q_locate_dev(qa, k, round);
+  __syncthreads();
+  q_filter_dev(qa, k, threadIdx.x, blockDim.x);
+  __syncthreads();
+  q_finish_dev(qa, vs, out_x, out_s, out_t, t_step, k);
+  __syncthreads();
+  if (round == 0) {
+    if (threadIdx.x == 0 && qa.tg[k].status != QS_OK) q_prep_target(qa, 0, k);
+  } else {
+    q_select_dev(qa, vs, scratch, out_x, out_s, out_t, t_step, unresolved, all, k);
   }
 }
 
