@@ -1024,39 +1024,6 @@ PF_D void ancestors_of(const Lookup<TQ>& L, const uint64_t (&w3)[SB], const bool
     if (ok[b]) anc[b] = cutpoint_lookup<TQ>(L.q, L.cut, L.n, unit_open(w3[b]));
 }
 
-// The same lookups with each slot's group record already in shared memory
-// (the step kernel prefetches it one pipeline stage earlier with cp.async):
-// one L2 round trip (the fq window) instead of two dependent ones.
-template <typename TQ, int SB>
-PF_D void ancestors_of_staged(const Lookup<TQ>& L, const uint64_t (&w3)[SB], const bool (&ok)[SB],
-                              int64_t (&anc)[SB], const Grp* const (&staged)[SB]) {
-  const uint64_t pol = l2_policy_last();
-  uint32_t r[SB];
-  uint64_t s0[SB];
-  int64_t first[SB];
-  int cnt[SB];
-#pragma unroll
-  for (int b = 0; b < SB; ++b) {
-    const uint64_t K = ((w3[b] >> 12) << 1) | 1ull;
-    s0[b] = ok[b] ? (K >> L.B) : 0;
-    r[b] = (uint32_t)(K & ((1ull << L.B) - 1ull));
-    const Grp G = ok[b] ? *staged[b] : Grp{0u, 0u, 0ull};
-    stratum_run(L, G, s0[b], first[b], cnt[b]);
-  }
-  uint64_t w0[SB], w1[SB];
-#pragma unroll
-  for (int b = 0; b < SB; ++b) {
-    const uint8_t* p = L.fq + (first[b] & ~7ll);
-    w0[b] = ld_fq8(p, pol);
-    w1[b] = ld_fq8(p + 8, pol);
-  }
-#pragma unroll
-  for (int b = 0; b < SB; ++b) {
-    const int64_t k = run_count_win(L, first[b], cnt[b], r[b], w0[b], w1[b], pol);
-    if (ok[b]) anc[b] = k;
-  }
-}
-
 // ------------------------------------------- sharded rank-table lookup ---
 // The rank tables of a sharded run, per shard g: grp over the GLOBAL stratum
 // groups (entries valid only for groups whose 8 strata and closing cut lie

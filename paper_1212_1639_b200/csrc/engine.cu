@@ -82,10 +82,6 @@ struct DevBuf {
 // early-resident K4 / group / step CTAs cost the concurrent quantile work
 // more than the hidden launch latency saves.
 enum { PDL_STEP = 1, PDL_K2 = 2, PDL_K3 = 4, PDL_K4 = 8, PDL_GRP = 16 };
-// Dynamic shared memory the step kernel may take: the 227 KB per-block
-// opt-in limit less its static shared memory (reduction scratch, exp table).
-constexpr int STEP_SMEM_LIMIT = 232448 - 8 * 1024;
-
 // cutpoint and the K7 ordered-uniform resampler share the tree CDF and the
 // cut-point / rank tables
 inline bool uses_cut_tables(int r) { return r == PF_RESAMPLE_CUTPOINT || r == PF_RESAMPLE_SPACINGS; }
@@ -888,17 +884,8 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   e->last_path = (fused ? PF_PATH_FUSED_DRAWS : 0) | (e->strata ? PF_PATH_RANK_TABLES : 0) |
                  (uses_cut_tables(c.resampler) && fuse_top() ? PF_PATH_FUSED_TOP : 0);
   const int STEP_THREADS = fused ? FD_THREADS : 256;
-  const size_t step_smem0 = (fused ? (size_t)(((draw_smem / 8) + 3) & ~size_t(3)) * 8 : 0) +
-                            (size_t)2 * STEP_SB * STEP_THREADS * (sizeof(Rec) + 3 * sizeof(double));
-  // group-record stage of the rank-table lookups (single run, N >= 2^21),
-  // when it fits beside the tables (one shared gamma table: Priors())
-  static const bool grp_env = [] {
-    const char* v = getenv("PF_GRP_PREFETCH");
-    return v ? atoi(v) != 0 : true;
-  }();
-  const size_t grp_stage = (size_t)2 * STEP_SB * STEP_THREADS * sizeof(Grp);
-  const bool grp_pref = grp_env && e->strata && step_smem0 + grp_stage <= (size_t)STEP_SMEM_LIMIT;
-  const size_t step_smem = step_smem0 + (grp_pref ? grp_stage : 0);
+  const size_t step_smem = (fused ? (size_t)(((draw_smem / 8) + 3) & ~size_t(3)) * 8 : 0) +
+                           (size_t)2 * STEP_SB * STEP_THREADS * (sizeof(Rec) + 3 * sizeof(double));
   if (!fused) {
     CK(e->dz.ensure(3 * (size_t)n));
     CK(e->dgs.ensure(3 * (size_t)n));
@@ -910,9 +897,10 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       CK(cudaFuncSetAttribute(draws_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)((2 * GT_TABLE_DOUBLES + NT_TABLE_DOUBLES) * sizeof(double))));
       CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              STEP_SMEM_LIMIT));
+                              (int)((2 * GT_TABLE_DOUBLES + NT_TABLE_DOUBLES + 4) * sizeof(double) +
+                                    2 * STEP_SB * FD_THREADS * (sizeof(Rec) + 3 * sizeof(double)))));
       CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              STEP_SMEM_LIMIT));
+                              (int)(2 * STEP_SB * 256 * (sizeof(Rec) + 3 * sizeof(double)))));
       attr.mark();
     }
   }
@@ -1039,7 +1027,6 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     a.shard = 0;
     static const int dbg_identity = getenv("PF_DEBUG_IDENTITY_ANC") ? 1 : 0;  // timing diagnostics only
     a.dbg_identity = dbg_identity;
-    a.grp_pref = grp_pref ? 1 : 0;
     static const double ref_slack = [] {
       const char* v = getenv("PF_MOMENT_SLACK");
       return v ? atof(v) : 64.0;

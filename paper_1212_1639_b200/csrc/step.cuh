@@ -228,7 +228,6 @@ struct StepArgs {
   const double* spS;     // K7 (spacings): prefix sums of step t-1's slot exponentials -- the
                          // resampling words are formed from them here instead of read from u3
   const double* sp_tot;  // sharded K7: every shard's exponential total of step t-1 (slk.G of them)
-  int grp_pref;          // the launch carries the group-record stage (single run, rank tables)
   int dbg_identity;      // diagnostics only (PF_DEBUG_IDENTITY_ANC): skip the lookup, ancestor = slot
   double ref_slack;      // moment-reference slack (64; 0 = rescale at every new max)
   const Rec* recs[PF_MAX_SHARDS];  // sharded run: every shard's records of step t-1
@@ -514,25 +513,6 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
       w3[b] = !live ? 0ull : a.spS ? spacings_word(sp_off + __ldcs(a.spS + j), sp_inv) : __ldcs(a.u3 + j);
     }
   };
-  // Group records of the rank tables, prefetched one pipeline stage ahead of
-  // their lookups into a double-buffered shared stage (after the record /
-  // draw stages): the lookup then waits for one L2 round trip, not two.
-  const bool pre_grp = a.grp_pref && a.lk.grp && !a.lk.anc && a.slk.G == 0 && !a.dbg_identity && a.t > 1;
-  Grp* gstage = reinterpret_cast<Grp*>(smem + 2 * buf_bytes);
-  auto grp_at = [&](int buf, int b) { return gstage + (buf * STEP_SB + b) * nth + threadIdx.x; };
-  auto prefetch_grp = [&](int64_t bk, int buf, const uint64_t (&w3)[STEP_SB]) {
-    if (pre_grp) {
-#pragma unroll
-      for (int b = 0; b < STEP_SB; ++b) {
-        const int64_t j = bk * batch + b * (int64_t)nth + threadIdx.x;
-        if (bk < nbatches && j < a.n) {
-          const uint64_t K = ((w3[b] >> 12) << 1) | 1ull;
-          cp_async16((uint32_t)__cvta_generic_to_shared(grp_at(buf, b)), a.lk.grp + ((K >> a.lk.B) / GRP_STRATA));
-        }
-      }
-    }
-    asm volatile("cp.async.commit_group;");
-  };
   auto issue = [&](int64_t bi, int buf, const uint64_t (&w3)[STEP_SB]) {
     int64_t jj[STEP_SB], anc[STEP_SB];
     bool ok[STEP_SB];
@@ -551,11 +531,6 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
 #pragma unroll
         for (int b = 0; b < STEP_SB; ++b)
           if (ok[b]) anc[b] = a.lk.anc[jj[b]];
-      } else if (pre_grp) {
-        const Grp* st[STEP_SB];
-#pragma unroll
-        for (int b = 0; b < STEP_SB; ++b) st[b] = grp_at(buf, b);
-        ancestors_of_staged<TQ, STEP_SB>(a.lk, w3, ok, anc, st);
       } else {
         ancestors_of<TQ, STEP_SB>(a.lk, w3, ok, anc);
       }
@@ -645,36 +620,19 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
     s1t += edt;
     s2t = fma(edt, dt, s2t);
   };
-  // cp.async groups per iteration j: P_j (group records of batch j+2), then
-  // C_j (records / staged values of batch j+1).  wait_group 2 before the
-  // lookups of j+1 completes P_(j-1); wait_group 2 before the arithmetic of
-  // j completes C_(j-1).
   int cur = 0;
   int64_t bi = blockIdx.x;
-  const int64_t G = gridDim.x;
-  uint64_t wA[STEP_SB], wB[STEP_SB];  // words of batches bi+G (next lookups) and bi+2G (next prefetch)
-  {
-    uint64_t w0[STEP_SB];
-    load_w3(bi, w0);
-    load_w3(bi + G, wA);
-    prefetch_grp(bi, 0, w0);
-    prefetch_grp(bi + G, 1, wA);
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
-    if (bi < nbatches) issue(bi, 0, w0);
-    else asm volatile("cp.async.commit_group;");
-  }
-  load_w3(bi + 2 * G, wB);
-  for (; bi < nbatches; bi += G) {
-    prefetch_grp(bi + 2 * G, cur, wB);
-    asm volatile("cp.async.wait_group 2;" ::: "memory");
-    if (bi + G < nbatches) {
-      issue(bi + G, cur ^ 1, wA);
+  uint64_t w3n[STEP_SB];
+  load_w3(bi, w3n);
+  if (bi < nbatches) issue(bi, 0, w3n);
+  load_w3(bi + gridDim.x, w3n);
+  for (; bi < nbatches; bi += gridDim.x) {
+    if (bi + gridDim.x < nbatches) {
+      issue(bi + gridDim.x, cur ^ 1, w3n);
+      load_w3(bi + 2 * (int64_t)gridDim.x, w3n);
     } else {
       asm volatile("cp.async.commit_group;");
     }
-#pragma unroll
-    for (int b = 0; b < STEP_SB; ++b) wA[b] = wB[b];
-    load_w3(bi + 3 * G, wB);
     // FD: this batch's draws (Philox block t, filtering.py:273,280,286) in
     // registers, computed while its record gathers (issued one iteration
     // earlier) are still in flight; the slots' Philox networks and the three
@@ -694,7 +652,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
         dgt[b] = LT ? gamma_table_slot(slot_t, unit_open(P.w[2])) : 1.0;
       }
     }
-    asm volatile("cp.async.wait_group 2;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
 #pragma unroll
     for (int b = 0; b < STEP_SB; ++b) {
       const int64_t j = bi * batch + b * (int64_t)nth + threadIdx.x;
