@@ -35,6 +35,7 @@ struct pf_shard {
   // rank tables (N >= 2^21): grp over the global stratum groups, fq / f32
   // over this rank's particles
   bool rank_on = false;
+  bool resolve_pending = false;  // rank 0: a resolve on the side stream not yet joined
   Grp* sgrp = nullptr;
   uint8_t* sfq = nullptr;
   uint32_t* sf32 = nullptr;
@@ -88,6 +89,7 @@ struct ShardOps {
     int rc;
     s->y_host.assign(y, y + T);
     s->T = T;
+    s->resolve_pending = false;
     s->cur = 0;
     s->out = out;
     const size_t TT = (size_t)(T > 0 ? T : 1);
@@ -199,6 +201,15 @@ struct ShardOps {
   }
 
   // Phase 1: ancestors (step t-1's resample) + step kernel -> xrec[rank].
+  // Rank 0: the main stream waits for the last resolve (before the partial
+  // all-gather that follows phase 1, or the outputs).
+  static int join_resolve(pf_shard* s, int64_t t_resolved) {
+    if (!s->resolve_pending) return PF_OK;
+    CK(cudaStreamWaitEvent(s->e->st, s->e->ev_q[t_resolved & 1], 0));
+    s->resolve_pending = false;
+    return PF_OK;
+  }
+
   static int phase1(pf_shard* s, int64_t t) {
     pf_engine* e = s->e;
     const pf_config& c = s->cfg;
@@ -319,7 +330,7 @@ struct ShardOps {
       CK(cudaMemcpyAsync(s->out->indices + (size_t)(t - 2) * ns, e->idx.p, ns * sizeof(int64_t),
                          cudaMemcpyDeviceToHost, e->st));
     s->cur ^= 1;
-    return PF_OK;
+    return join_resolve(s, t - 1);
   }
 
   // Phase 2: combine the G partials (every rank identically) + K2 -> xtot[rank].
@@ -379,6 +390,10 @@ struct ShardOps {
     pf_engine* e = s->e;
     const int64_t ns = s->ns, N = s->cfg.n;
     const int par = (int)(t & 1);
+    if (s->ntg) {  // the side stream's classification starts from here (M and keys of step t)
+      CK(cudaEventRecord(e->ev_b, e->st));
+      CK(cudaStreamWaitEvent(e->side, e->ev_b, 0));
+    }
     const CdfPlan plan = cdf_plan(ns);
     const size_t top_smem = 4 * (size_t)plan.chunks * sizeof(TQ);
     CK(cudaFuncSetAttribute(cdf_top_shard_kernel<TQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -407,6 +422,9 @@ struct ShardOps {
     }
     LAUNCHED();
     if (s->ntg) {
+      // the window classification on the side stream, beside K3 / K4: it
+      // needs only this step's M and keys (phase 2); the barrier after this
+      // phase orders it before rank 0's resolve
       QArgs q2 = qargs(s, par);
       uint32_t* kb = e->keys.p + (size_t)par * 3 * ns;
       q2.keys[0] = s->want_fq ? kb : nullptr;
@@ -415,8 +433,10 @@ struct ShardOps {
       q2.pbase = s->rank * s->cls_grid;
       q2.ptotal = s->world * s->cls_grid;
       q2.gbase = (uint32_t)((int64_t)s->rank * ns);
-      int rc = launch_classify<TQ>(s->qm, s->cls_grid, w, (int)plan.tiles, e->fail.p, q2, e->st);
+      int rc = launch_classify<TQ>(s->qm, s->cls_grid, w, (int)plan.tiles, e->fail.p, q2, e->side);
       if (rc != PF_OK) return rc;
+      CK(cudaEventRecord(e->ev_e, e->side));
+      CK(cudaStreamWaitEvent(e->st, e->ev_e, 0));
     }
     return PF_OK;
   }
@@ -429,7 +449,12 @@ struct ShardOps {
     const int64_t ns = s->ns, N = c.n;
     const int par = (int)(t & 1);
     const int ntg = s->ntg;
-    cudaStream_t ss = e->st;
+    // rank 0's resolve of step t runs on its side stream, overlapping step
+    // t+1's step kernel; phase 1 of step t+1 holds rank 0's main stream (and
+    // with it every rank, through the partial all-gather) until it is done
+    cudaStream_t ss = e->side;
+    CK(cudaEventRecord(e->ev_b, e->st));
+    CK(cudaStreamWaitEvent(ss, e->ev_b, 0));
     QArgs qa = qargs(s, par);
     qa.lidx = e->qlidx.p;
     qa.lw = e->qlw.p;
@@ -503,6 +528,8 @@ struct ShardOps {
     q_select_kernel<<<ntg, 1024, 0, ss>>>(qa, vs, e->qscratch.p, ox, os, ot, t, e->fail.p, s->q_unres, all);
     q_step_end_kernel<<<1, 1024, 0, ss>>>(qa, 1);
     g_launches.fetch_add(2);
+    CK(cudaEventRecord(e->ev_q[t & 1], ss));
+    s->resolve_pending = true;
     return PF_OK;
   }
 
@@ -511,6 +538,7 @@ struct ShardOps {
     pf_engine* e = s->e;
     const pf_config& c = s->cfg;
     const int64_t ns = s->ns, T = s->T;
+    if (int rc = join_resolve(s, T)) return rc;
     pf_outputs* out = s->out;
     const bool keep_idx = out && out->indices;
     const bool keep_final = out && (out->final_states || out->final_sigma2);
