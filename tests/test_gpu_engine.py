@@ -286,3 +286,21 @@ def test_replications_match_individual_runs(gpu):
         assert np.array_equal(o.resampled_indices, ref.resampled_indices)
         assert np.array_equal(o.param_posterior["tau2"].quantiles, ref.param_posterior["tau2"].quantiles)
     assert rank_seeds(range(10), 1, 4) == [1, 5, 9]
+
+
+def test_resident_graph_replay_leaves_results_unchanged(gpu):
+    """Resident runs capture the T-loop as one CUDA graph and replay it
+    (csrc/engine.cu run_impl); API runs before and after the replays return
+    identical outputs, and the replays time their step kernels."""
+    _, y = _data(12, 31)
+    with P.Backend() as b:
+        first = P.run_particle_learning(P.Priors(), y, 1 << 14, seed=6, keep_indices=True, backend=b)
+        eng = next(iter(b._engines.values()))
+        eng.run_resident(12)   # capture + launch
+        eng.run_resident(12)   # replay
+        t = eng.last_timing()
+        again = P.run_particle_learning(P.Priors(), y, 1 << 14, seed=6, keep_indices=True, backend=b)
+    assert t["step_kernel_ms"] > 0 and t["step_kernel_launches"] == 12
+    assert np.array_equal(first.resampled_indices, again.resampled_indices)
+    assert np.array_equal(first.filtered_mean, again.filtered_mean)
+    assert np.array_equal(first.param_posterior["sigma2"].quantiles, again.param_posterior["sigma2"].quantiles)
