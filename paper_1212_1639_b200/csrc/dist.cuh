@@ -217,16 +217,17 @@ struct ShardOps {
     const int par = (int)(t & 1);
     const bool FDm = s->fused;
     const int threads = FDm ? FD_THREADS : 256;
+    const int sbx = FDm ? FD_SB : STEP_SB;
     const bool share_tab = LS && LT && e->tab_s == e->tab_t && c.gamma_method == 0;
     const int ngt = c.gamma_method == 0 ? (LS ? 1 : 0) + (LT && !share_tab ? 1 : 0) : 0;
     const size_t draw_smem = ((size_t)ngt * GT_TABLE_DOUBLES + (e->ntab ? NT_TABLE_DOUBLES : 0)) * sizeof(double);
     const size_t step_smem = (FDm ? (size_t)(((draw_smem / 8) + 3) & ~size_t(3)) * 8 : 0) +
-                             (size_t)2 * STEP_SB * threads * (sizeof(Rec) + 3 * sizeof(double));
+                             (size_t)2 * sbx * threads * (sizeof(Rec) + 3 * sizeof(double));
     static DevOnce attr;
     if (attr.pending()) {
       CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)((2 * GT_TABLE_DOUBLES + NT_TABLE_DOUBLES + 4) * sizeof(double) +
-                                    2 * STEP_SB * FD_THREADS * (sizeof(Rec) + 3 * sizeof(double)))));
+                                    2 * FD_SB * FD_THREADS * (sizeof(Rec) + 3 * sizeof(double)))));
       CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(2 * STEP_SB * 256 * (sizeof(Rec) + 3 * sizeof(double)))));
       attr.mark();
@@ -236,7 +237,7 @@ struct ShardOps {
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, step_kernel<MODE, TQ, true>, threads, step_smem));
     else
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, step_kernel<MODE, TQ, false>, threads, step_smem));
-    const int64_t nb = (ns + STEP_SB * threads - 1) / (STEP_SB * threads);
+    const int64_t nb = (ns + sbx * threads - 1) / (sbx * threads);
     const int grid = (int)std::min<int64_t>(nb, (int64_t)sm_count() * std::max(occ, 1));
     StepArgs<TQ> a;
     memset(&a, 0, sizeof(a));

@@ -916,8 +916,9 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   e->last_path = (fused ? PF_PATH_FUSED_DRAWS : 0) | (e->strata ? PF_PATH_RANK_TABLES : 0) |
                  (uses_cut_tables(c.resampler) && fuse_top() ? PF_PATH_FUSED_TOP : 0);
   const int STEP_THREADS = fused ? FD_THREADS : 256;
+  const int STEP_SBX = fused ? FD_SB : STEP_SB;  // slots per thread per stage of the kernel launched
   const size_t step_smem = (fused ? (size_t)(((draw_smem / 8) + 3) & ~size_t(3)) * 8 : 0) +
-                           (size_t)2 * STEP_SB * STEP_THREADS * (sizeof(Rec) + 3 * sizeof(double));
+                           (size_t)2 * STEP_SBX * STEP_THREADS * (sizeof(Rec) + 3 * sizeof(double));
   if (!fused) {
     CK(e->dz.ensure(3 * (size_t)n));
     CK(e->dgs.ensure(3 * (size_t)n));
@@ -930,7 +931,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
                               (int)((2 * GT_TABLE_DOUBLES + NT_TABLE_DOUBLES) * sizeof(double))));
       CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)((2 * GT_TABLE_DOUBLES + NT_TABLE_DOUBLES + 4) * sizeof(double) +
-                                    2 * STEP_SB * FD_THREADS * (sizeof(Rec) + 3 * sizeof(double)))));
+                                    2 * FD_SB * FD_THREADS * (sizeof(Rec) + 3 * sizeof(double)))));
       CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(2 * STEP_SB * 256 * (sizeof(Rec) + 3 * sizeof(double)))));
       attr.mark();
@@ -945,7 +946,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   if (occ < 1) occ = 1;
   if (docc < 1) docc = 1;
   // persistent grids: one wave of resident CTAs
-  const int64_t nbatches = (n + STEP_SB * STEP_THREADS - 1) / (STEP_SB * STEP_THREADS);
+  const int64_t nbatches = (n + STEP_SBX * STEP_THREADS - 1) / (STEP_SBX * STEP_THREADS);
   const int step_grid = (int)std::min<int64_t>(nbatches, (int64_t)sms * occ);
   const int draw_grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sms * docc);
   auto launch_draws = [&](int64_t t, cudaStream_t s_) {

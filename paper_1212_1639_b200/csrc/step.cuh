@@ -27,7 +27,10 @@ constexpr double LOG_TWO_PI = 1.8378770664093453;  // math.log(2*math.pi), model
 #define PF_STEP_SB 2
 #endif
 #ifndef PF_FD_THREADS
-#define PF_FD_THREADS 512
+#define PF_FD_THREADS 768
+#endif
+#ifndef PF_FD_SB
+#define PF_FD_SB 1
 #endif
 constexpr int STEP_SB = PF_STEP_SB;  // slots per thread per pipeline stage (double buffered)
 // STEP_SB = 1 is supported again.  The round-1 SB = 1 build failed memcheck
@@ -39,6 +42,13 @@ constexpr int STEP_SB = PF_STEP_SB;  // slots per thread per pipeline stage (dou
 // racecheck are clean for SB = 1 and SB = 2.  SB = 2 stays the default
 // (measured faster).
 constexpr int FD_THREADS = PF_FD_THREADS;  // CTA width of the fused-draws step kernel
+// The fused-draws kernel runs 768 threads with one slot per thread per stage
+// (80 registers, 24 warps per SM) -- measured faster than 512 x 2 (122
+// registers, 16 warps), 640 x 1, 896 x 1 and 1024 x 1 (the last two spill);
+// the 256-thread kernel (draws kernel beside it) keeps two slots.
+constexpr int FD_SB = PF_FD_SB;
+template <bool FD>
+constexpr int step_sb() { return FD ? FD_SB : STEP_SB; }
 
 // Order-preserving 32-bit image of a double (float32 rounded down, sign
 // folded): the quantile keys of quantile.cuh.
@@ -448,6 +458,7 @@ PF_D void cp_async8(uint32_t dst, const void* src) {
 template <int MODE, typename TQ, bool FD = false>
 __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs<TQ> a) {
   constexpr bool LS = MODE & M_LS, LT = MODE & M_LT, SINGLE = MODE & M_SINGLE;
+  constexpr int SB = step_sb<FD>();  // slots per thread per pipeline stage
   // the step's tables are constant over the run: stage them while the
   // previous kernel (group build / K4) drains, then wait for its outputs
   int slot_s = -1, slot_t = -1, noff = -1, tab_doubles = 0;
@@ -468,7 +479,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
   double s0 = 0, sx = 0, s2x = 0, s1s = 0, s2s = 0, s1t = 0, s2t = 0, s2w = 0;
   bool bad = false;
 
-  // Software pipeline over batches of STEP_SB x blockDim slots (batches are
+  // Software pipeline over batches of SB x blockDim slots (batches are
   // dealt to CTAs round robin).  Iteration i: resolve the ancestors of batch
   // i+1 (cut-point lookups against L2-resident tables) and start, with
   // cp.async into the other half of a double buffer, their 32-byte record
@@ -477,16 +488,16 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
   // run its arithmetic while batch i+1's reads are in flight.  Each thread
   // reads back only what it staged itself.
   const int nth = blockDim.x;
-  const int64_t batch = (int64_t)STEP_SB * nth;
+  const int64_t batch = (int64_t)SB * nth;
   const int64_t nbatches = (a.n + batch - 1) / batch;
   char* smem = reinterpret_cast<char*>(pf_gtab + ((tab_doubles + 3) & ~3));
-  const size_t buf_bytes = (size_t)STEP_SB * nth * (sizeof(Rec) + 3 * sizeof(double));
+  const size_t buf_bytes = (size_t)SB * nth * (sizeof(Rec) + 3 * sizeof(double));
   auto rec_at = [&](int buf, int b) {
     return reinterpret_cast<Rec*>(smem + buf * buf_bytes) + b * nth + threadIdx.x;
   };
   auto val_at = [&](int buf, int k, int b) {
-    return reinterpret_cast<double*>(smem + buf * buf_bytes + (size_t)STEP_SB * nth * sizeof(Rec)) +
-           (k * STEP_SB + b) * nth + threadIdx.x;
+    return reinterpret_cast<double*>(smem + buf * buf_bytes + (size_t)SB * nth * sizeof(Rec)) +
+           (k * SB + b) * nth + threadIdx.x;
   };
   // K7: the ordered uniform of slot j is S_j / S_(N+1) (spacings_words_kernel
   // forms the same words for the store / final resample)
@@ -505,19 +516,19 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
     sp_inv = 1.0 / (tot + spacings_aux_exp(a.seed, a.t - 1));
   }
   // resampling words are loaded one pipeline stage ahead of their lookups
-  auto load_w3 = [&](int64_t bi, uint64_t (&w3)[STEP_SB]) {
+  auto load_w3 = [&](int64_t bi, uint64_t (&w3)[SB]) {
 #pragma unroll
-    for (int b = 0; b < STEP_SB; ++b) {
+    for (int b = 0; b < SB; ++b) {
       const int64_t j = bi * batch + b * (int64_t)nth + threadIdx.x;
       const bool live = a.t > 1 && bi < nbatches && j < a.n;
       w3[b] = !live ? 0ull : a.spS ? spacings_word(sp_off + __ldcs(a.spS + j), sp_inv) : __ldcs(a.u3 + j);
     }
   };
-  auto issue = [&](int64_t bi, int buf, const uint64_t (&w3)[STEP_SB]) {
-    int64_t jj[STEP_SB], anc[STEP_SB];
-    bool ok[STEP_SB];
+  auto issue = [&](int64_t bi, int buf, const uint64_t (&w3)[SB]) {
+    int64_t jj[SB], anc[SB];
+    bool ok[SB];
 #pragma unroll
-    for (int b = 0; b < STEP_SB; ++b) {
+    for (int b = 0; b < SB; ++b) {
       jj[b] = bi * batch + b * (int64_t)nth + threadIdx.x;
       ok[b] = jj[b] < a.n;
       anc[b] = jj[b];
@@ -525,23 +536,23 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
     if (a.t > 1 && !a.dbg_identity) {
       if (a.slk.G > 0) {
 #pragma unroll
-        for (int b = 0; b < STEP_SB; ++b)
+        for (int b = 0; b < SB; ++b)
           if (ok[b]) anc[b] = a.srk.on ? sharded_lookup_rank<TQ>(a.slk, a.srk, w3[b]) : sharded_lookup<TQ>(a.slk, w3[b]);
       } else if (a.lk.anc) {  // baseline resamplers: ancestors precomputed
 #pragma unroll
-        for (int b = 0; b < STEP_SB; ++b)
+        for (int b = 0; b < SB; ++b)
           if (ok[b]) anc[b] = a.lk.anc[jj[b]];
       } else {
-        ancestors_of<TQ, STEP_SB>(a.lk, w3, ok, anc);
+        ancestors_of<TQ, SB>(a.lk, w3, ok, anc);
       }
       if (a.idx_out) {
 #pragma unroll
-        for (int b = 0; b < STEP_SB; ++b)
+        for (int b = 0; b < SB; ++b)
           if (ok[b]) a.idx_out[jj[b]] = anc[b] + 1;
       }
     }
 #pragma unroll
-    for (int b = 0; b < STEP_SB; ++b) {
+    for (int b = 0; b < SB; ++b) {
       if (!ok[b]) continue;
       const uint32_t dst = (uint32_t)__cvta_generic_to_shared(rec_at(buf, b));
       // ancestors are global indices in a sharded run (identity, local, at t = 1)
@@ -622,7 +633,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
   };
   int cur = 0;
   int64_t bi = blockIdx.x;
-  uint64_t w3n[STEP_SB];
+  uint64_t w3n[SB];
   load_w3(bi, w3n);
   if (bi < nbatches) issue(bi, 0, w3n);
   load_w3(bi + gridDim.x, w3n);
@@ -638,10 +649,10 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
     // earlier) are still in flight; the slots' Philox networks and the three
     // table polynomials are independent chains the scheduler interleaves.
     // The resampling word goes to memory for the next step's lookups.
-    double dz[STEP_SB], dgs[STEP_SB], dgt[STEP_SB];
+    double dz[SB], dgs[SB], dgt[SB];
     if (FD) {
 #pragma unroll
-      for (int b = 0; b < STEP_SB; ++b) {
+      for (int b = 0; b < SB; ++b) {
         const int64_t j = bi * batch + b * (int64_t)nth + threadIdx.x;
         const Philox4 P = philox_block(a.dr.seed, (uint64_t)(a.dr.gbase + j), (uint64_t)a.t);
         if (j < a.n) a.dr.u3[j] = P.w[3];
@@ -654,7 +665,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
     }
     asm volatile("cp.async.wait_group 1;" ::: "memory");
 #pragma unroll
-    for (int b = 0; b < STEP_SB; ++b) {
+    for (int b = 0; b < SB; ++b) {
       const int64_t j = bi * batch + b * (int64_t)nth + threadIdx.x;
       if (j >= a.n) continue;
       // drawn here (FD) unless an oracle feed was staged; precomputed draws
