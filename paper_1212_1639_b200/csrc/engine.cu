@@ -520,11 +520,19 @@ struct pf_engine {
   // CUDA graph of the resident T-loop (every launch of T steps, both streams),
   // captured on the first resident run and replayed by later ones; dropped
   // when a non-resident run or a reconfigure changes what was captured
-  cudaGraphExec_t gexec = nullptr;
-  uint64_t gkey = 0;
-  int64_t g_launches_per_run = 0;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_step_evs;  // the graph's step-kernel events
-  std::vector<double> g_y;  // the series the graph was captured for
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    uint64_t key = 0;
+    int64_t launches = 0;                                       // kernels per replay
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> step_evs;  // resident: the step kernels' events
+    std::vector<std::pair<int, int>> loop_marks;                // API: phase marks inside the loop
+    int nev_end = 0;
+  };
+  std::vector<GraphEntry> graphs;  // a few captured T-loops (resident / API, per T)
+  // the run's seed and series in device memory, so one captured loop serves
+  // every seed and series of its shape (replications)
+  DevBuf<uint64_t> seed_dev;
+  DevBuf<double> y_dev;
   int64_t qstats[4] = {0, 0, 0, 0};  // quantile: unresolved, fallbacks, max candidates, resolves
   int64_t last_step_launches = 0, last_kernels = 0;
   int32_t last_path = 0;  // PF_PATH_* of the last run
@@ -533,15 +541,34 @@ struct pf_engine {
 
 namespace {
 
-void drop_graph(pf_engine* e) {
-  if (e->gexec) cudaGraphExecDestroy(e->gexec);
-  e->gexec = nullptr;
-  e->gkey = 0;
-  for (auto& pr : e->g_step_evs) {
+void drop_graph_entry(pf_engine::GraphEntry& g) {
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  g.exec = nullptr;
+  for (auto& pr : g.step_evs) {
     cudaEventDestroy(pr.first);
     cudaEventDestroy(pr.second);
   }
-  e->g_step_evs.clear();
+  g.step_evs.clear();
+}
+
+void drop_graph(pf_engine* e) {
+  for (auto& g : e->graphs) drop_graph_entry(g);
+  e->graphs.clear();
+}
+
+// Every device buffer a captured loop's kernels point at: a captured graph is
+// only valid while none of them has moved.
+uint64_t graph_buffers_sig(const pf_engine* e) {
+  const void* ps[] = {e->rec[0].p, e->rec[1].p, e->lw.p, e->du3.p, e->dz.p, e->dgs.p, e->dgt.p, e->q.p, e->cut.p,
+                      e->rank.p, e->f32.p, e->keys.p, e->qtg.p, e->qsh.p, e->qcand.p, e->qpart.p, e->qscratch.p,
+                      e->mbuf.p, e->qhist.p, e->qfhist.p, e->qunres.p, e->qlidx.p, e->qlw.p, e->partials.p, e->sc.p,
+                      e->fail.p, e->o_fm.p, e->o_sm.p, e->o_ssd.p, e->o_tm.p, e->o_tsd.p, e->o_fq.p, e->o_sq.p,
+                      e->o_tq.p, e->o_ess.p, e->spS.p, e->spw.p, e->sptmp.p, e->sptot.p, e->seed_dev.p, e->y_dev.p,
+                      e->tab_s, e->tab_t, e->ntab, e->cdf.tile_tot.p, e->cdf.chunk_tot.p, e->cdf.node.p,
+                      e->cdf.carry.p, e->cdf.total.p, e->cdf.top_scratch.p, e->cdf.top_ctr.p};
+  uint64_t h = 1469598103934665603ull;
+  for (const void* p : ps) h = (h ^ (uint64_t)(uintptr_t)p) * 1099511628211ull;
+  return h;
 }
 
 // Ends a stream capture left open by an early error return.
@@ -831,6 +858,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
 
   // events
   int nev = 0;
+  bool capturing = false;  // inside a graph capture: event records become external nodes
   auto ev_record = [&]() -> int {
     if (!timing) return 0;
     if ((int)e->evs.size() <= nev) {
@@ -838,7 +866,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       cudaEventCreate(&ev);
       e->evs.push_back(ev);
     }
-    cudaEventRecord(e->evs[nev], st);
+    cudaEventRecordWithFlags(e->evs[nev], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
     return nev++;
   };
   std::vector<std::pair<int, int>> phase_marks;  // (event index, phase id)
@@ -868,6 +896,15 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   CK(cudaMemcpyAsync(e->sc.p, &s0h, sizeof(Scalars), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(e->fail.p, 0, sizeof(int64_t), st));
 
+  // the run's seed and series in device memory (read by the loop's kernels)
+  CK(e->seed_dev.ensure(1));
+  CK(e->y_dev.ensure(TT));
+  {
+    const uint64_t sd = c.seed;
+    CK(cudaMemcpyAsync(e->seed_dev.p, &sd, sizeof(sd), cudaMemcpyHostToDevice, st));
+    const double* yh = rs.y ? rs.y : e->y_host.data();
+    if (T > 0) CK(cudaMemcpyAsync(e->y_dev.p, yh, (size_t)T * sizeof(double), cudaMemcpyHostToDevice, st));
+  }
   // ---- K0 init
   {
     InitArgs a;
@@ -951,6 +988,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   const int draw_grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sms * docc);
   auto launch_draws = [&](int64_t t, cudaStream_t s_) {
     DrawArgs d;
+    memset(&d, 0, sizeof(d));
     d.gbase = 0;
     d.n = n;
     d.t = t;
@@ -964,6 +1002,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     d.g_t = e->dgt.p + off;
     d.u3 = e->du3.p + off;
     d.fail = e->fail.p;
+    d.seedp = e->seed_dev.p;
     draws_kernel<MODE><<<draw_grid, 256, draw_smem, s_>>>(d);
     LAUNCHED();
   };
@@ -1007,28 +1046,40 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     return v ? (int64_t)atoll(v) : (int64_t)0;
   }();
   bool profiling = false;
-  // Resident runs (the bench's device-timed repeats) capture the T-loop as
-  // one CUDA graph and replay it: the same kernels with the same arguments,
-  // without T x ~22 host launches.  PF_GRAPH=0 disables.
+  // The T-loop is captured as one CUDA graph (both streams, every kernel of
+  // the T steps) and replayed by later runs of the same shape -- resident
+  // repeats and API runs alike; the seed and the series are read from device
+  // memory, so replications share one graph.  PF_GRAPH=0 disables.
   static const bool graphs_on = [] {
     const char* v = getenv("PF_GRAPH");
     return v ? atoi(v) != 0 : true;
   }();
-  const bool use_graph = rs.resident && graphs_on && !chain_dbg && prof_from == 0 && T > 0;
-  // an API run keeps the resident graph only if it leaves the series as captured
-  if (!rs.resident && e->gexec &&
-      (T != (int64_t)e->g_y.size() || memcmp(rs.y, e->g_y.data(), (size_t)T * sizeof(double)) != 0))
-    drop_graph(e);
-  const uint64_t gkey = ((uint64_t)T << 16) ^ ((uint64_t)MODE << 8) ^ (fused ? 1u : 0u) ^ (ntg ? 2u : 0u) ^
-                        ((uint64_t)c.resampler << 4) ^ ((uint64_t)c.seed * 0x9E3779B97F4A7C15ull);
-  const bool replay = use_graph && e->gexec && e->gkey == gkey;
+  // API runs with per-step host copies (keep_indices, store), oracle feeds or
+  // the sequential baselines are launched step by step
+  const bool graphable = graphs_on && !chain_dbg && prof_from == 0 && T > 0 && !keep_idx && !store &&
+                         !(fz || fgs || fgt || fw) && uses_cut_tables(c.resampler);
+  const bool use_graph = graphable;
+  uint64_t gkey = graph_buffers_sig(e);
+  for (uint64_t v : {(uint64_t)T, (uint64_t)MODE, (uint64_t)fused, (uint64_t)ntg, (uint64_t)want_fq,
+                     (uint64_t)c.resampler, (uint64_t)timing, (uint64_t)rs.resident, (uint64_t)(out && out->ess)})
+    gkey = (gkey ^ v) * 1099511628211ull;
+  pf_engine::GraphEntry* gent = nullptr;
+  for (auto& g : e->graphs)
+    if (use_graph && g.exec && g.key == gkey) gent = &g;
+  const bool replay = gent != nullptr;
   CaptureGuard capture{st};
+  capturing = false;
   if (use_graph && !replay) {
-    drop_graph(e);
+    if (e->graphs.size() >= 4) {  // keep the cache small: drop the oldest
+      drop_graph_entry(e->graphs.front());
+      e->graphs.erase(e->graphs.begin());
+    }
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     capture.active = true;
+    capturing = true;
   }
   const int64_t k_before_loop = g_launches.load();
+  const size_t marks_before_loop = phase_marks.size();
   // events recorded inside a capture cannot be waited on outside it: after a
   // graph launch, re-record the ones later code waits on (on st, which the
   // graph has joined every stream into)
@@ -1040,9 +1091,11 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     return PF_OK;
   };
   if (replay) {
-    CK(cudaGraphLaunch(e->gexec, st));
+    CK(cudaGraphLaunch(gent->exec, st));
     if ((rc = rerecord_after_graph()) != PF_OK) return rc;
-    g_launches.fetch_add(e->g_launches_per_run);
+    g_launches.fetch_add(gent->launches);
+    phase_marks.insert(phase_marks.end(), gent->loop_marks.begin(), gent->loop_marks.end());
+    nev = gent->nev_end;
     step_launches = T;
     cur = (int)(T & 1);
   }
@@ -1064,6 +1117,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     a.t = t;
     a.seed = c.seed;
     a.y = rs.y ? rs.y[t - 1] : e->y_host[(size_t)(t - 1)];
+    a.yp = e->y_dev.p;  // read on the device (a captured loop serves any series)
     a.sigma2_fixed = c.sigma2_fixed;
     a.tau2_fixed = c.tau2_fixed;
     a.sqrt_tau2_fixed = c.sqrt_tau2_fixed;
@@ -1115,6 +1169,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     a.dr.ntab = e->ntab;
     a.dr.u3 = e->du3.p + (size_t)(t % 3) * n;
     a.dr.fail = e->fail.p;
+    a.dr.seedp = e->seed_dev.p;  // read on the device (a captured loop serves any seed)
     a.z = fz ? row(fz, t) : nullptr;
     a.g_s = fgs ? row(fgs, t) : nullptr;
     a.g_t = fgt ? row(fgt, t) : nullptr;
@@ -1243,6 +1298,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       memset(&vs, 0, sizeof(vs));
       vs.rec = e->rec[cur].p;
       vs.seed = c.seed;
+      vs.seedp = e->seed_dev.p;
       vs.t = t;
       vs.gs = gamma_src(e, true, t);
       vs.feed_gs = row(fgs, t);
@@ -1382,15 +1438,20 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     cudaGraph_t g = nullptr;
     CK(cudaStreamEndCapture(st, &g));
     capture.active = false;
-    cudaError_t ierr = cudaGraphInstantiate(&e->gexec, g, 0);
+    capturing = false;
+    pf_engine::GraphEntry ent;
+    cudaError_t ierr = cudaGraphInstantiate(&ent.exec, g, 0);
     cudaGraphDestroy(g);
     CK(ierr);
-    e->gkey = gkey;
-    e->g_y.assign(e->y_host.begin(), e->y_host.begin() + T);
-    e->g_launches_per_run = g_launches.load() - k_before_loop;
-    e->g_step_evs = step_evs;  // recorded by the graph on every launch
+    ent.key = gkey;
+    ent.launches = g_launches.load() - k_before_loop;
+    ent.step_evs = step_evs;  // recorded by the graph on every launch
     step_evs.clear();
-    CK(cudaGraphLaunch(e->gexec, st));
+    ent.loop_marks.assign(phase_marks.begin() + (std::ptrdiff_t)marks_before_loop, phase_marks.end());
+    ent.nev_end = nev;
+    e->graphs.push_back(std::move(ent));
+    gent = &e->graphs.back();
+    CK(cudaGraphLaunch(gent->exec, st));
     if ((rc = rerecord_after_graph()) != PF_OK) return rc;
   }
   if (profiling) {
@@ -1524,7 +1585,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   e->last_total_ms = ms;
   e->last_step_launches = step_launches;
   if (rs.resident) {
-    const auto& sevs = use_graph ? e->g_step_evs : step_evs;
+    const auto& sevs = gent ? gent->step_evs : step_evs;
     double acc = 0;
     for (auto& pr : sevs) {
       float k = 0;
@@ -1778,7 +1839,15 @@ int pf_engine_create(const pf_config* cfg, pf_engine** out) {
 
 int pf_engine_reconfigure(pf_engine* e, const pf_config* cfg) {
   if (!e || !cfg) return set_err(PF_ERR_VALUE, "null argument");
-  if (memcmp(cfg, &e->cfg, sizeof(pf_config)) != 0) drop_graph(e);  // same config: the graph stays valid
+  {
+    // captured loops read the seed from device memory and leave the output
+    // flags to the host: only the rest of the configuration is baked in
+    pf_config a = *cfg, b = e->cfg;
+    a.seed = b.seed = 0;
+    a.keep_indices = b.keep_indices = a.keep_final = b.keep_final = 0;
+    a.store_particles = b.store_particles = 0;
+    if (memcmp(&a, &b, sizeof(pf_config)) != 0) drop_graph(e);
+  }
   if (cfg->n != e->n || (cfg->precision == PF_DTYPE_F32) != e->single || cfg->device != e->cfg.device ||
       cfg->resampler != e->cfg.resampler)
     return set_err(PF_ERR_VALUE, "reconfigure cannot change n, precision, device or resampler");

@@ -184,6 +184,7 @@ int run_group(pf_group* g, const double* y, int64_t T, pf_outputs* out) {
   auto launch_draws = [&](int s, int64_t t, cudaStream_t strm) {
     pf_engine* e = g->sh[s];
     DrawArgs d;
+    memset(&d, 0, sizeof(d));
     d.n = ns;
     d.t = t;
     d.seed = c.seed;

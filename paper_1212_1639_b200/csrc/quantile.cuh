@@ -146,6 +146,7 @@ struct QValueSrc {
   const Rec* recs[PF_MAX_SHARDS];  // sharded run: per-shard records, nsh > 0
   int nsh, lg;
   uint64_t seed;
+  const uint64_t* seedp; // non-null: read the seed from device memory (graph replays)
   int64_t t;
   GammaSrc gs;           // step t's sigma2 table
   const double* feed_gs; // oracle feed row t
@@ -162,7 +163,7 @@ PF_D double quantity_value(const QValueSrc& s, int q, uint32_t idx) {
   if (s.feed_gs) {
     g = s.feed_gs[idx];
   } else {
-    const Philox4 P = philox_block(s.seed, (uint64_t)idx, (uint64_t)s.t);
+    const Philox4 P = philox_block(s.seedp ? *s.seedp : s.seed, (uint64_t)idx, (uint64_t)s.t);
     g = gamma_draw(s.gs, unit_open(P.w[1]));
   }
   return r.bs / g;

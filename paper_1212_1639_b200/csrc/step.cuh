@@ -202,7 +202,10 @@ struct DrawArgs {
   uint64_t* u3;
   const int64_t* fail;
   int64_t gbase;         // global index of this shard's first slot (stream id offset)
+  const uint64_t* seedp; // non-null: the seed is read from device memory (graph replays)
 };
+
+PF_D uint64_t seed_of(uint64_t seed, const uint64_t* seedp) { return seedp ? *seedp : seed; }
 
 template <typename TQ>
 struct StepArgs {
@@ -238,6 +241,7 @@ struct StepArgs {
   const double* spS;     // K7 (spacings): prefix sums of step t-1's slot exponentials -- the
                          // resampling words are formed from them here instead of read from u3
   const double* sp_tot;  // sharded K7: every shard's exponential total of step t-1 (slk.G of them)
+  const double* yp;      // non-null: the observation is yp[t-1] (device memory; graph replays)
   int dbg_identity;      // diagnostics only (PF_DEBUG_IDENTITY_ANC): skip the lookup, ancestor = slot
   double ref_slack;      // moment-reference slack (64; 0 = rescale at every new max)
   const Rec* recs[PF_MAX_SHARDS];  // sharded run: every shard's records of step t-1
@@ -431,9 +435,10 @@ __global__ void __launch_bounds__(256) draws_kernel(DrawArgs a) {
   if (*a.fail) return;
   int slot_s, slot_t, noff = -1;
   stage_tables<LS, LT>(a.gs, a.gt, a.ntab, slot_s, slot_t, noff);
+  const uint64_t seed = seed_of(a.seed, a.seedp);
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n;
        j += (int64_t)gridDim.x * blockDim.x) {
-    const Philox4 P = philox_block(a.seed, (uint64_t)(a.gbase + j), (uint64_t)a.t);
+    const Philox4 P = philox_block(seed, (uint64_t)(a.gbase + j), (uint64_t)a.t);
     a.u3[j] = P.w[3];
     const double u0 = unit_open(P.w[0]);
     a.z[j] = noff >= 0 ? nt_eval_slot(noff, u0) : ndtri(u0);
@@ -470,6 +475,8 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
   if (*a.fail) return;
   const bool feedw = a.feed_w != nullptr;
   const double cs = a.sc->cs, ct = a.sc->ct, cx = a.sc->cx;
+  const double yobs = a.yp ? a.yp[a.t - 1] : a.y;
+  const uint64_t dseed = seed_of(a.dr.seed, a.dr.seedp);
   // m: reference of this thread's moment sums (moved, with a rescale, only
   // when a log-weight exceeds it by more than ref_slack = 64 -- e <= e^64
   // keeps the fp64 sums far from overflow); mx: the true running max, the
@@ -513,7 +520,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
     } else {
       tot += __ldcg(a.spS + a.n - 1);
     }
-    sp_inv = 1.0 / (tot + spacings_aux_exp(a.seed, a.t - 1));
+    sp_inv = 1.0 / (tot + spacings_aux_exp(seed_of(a.seed, a.dr.seedp), a.t - 1));
   }
   // resampling words are loaded one pipeline stage ahead of their lookups
   auto load_w3 = [&](int64_t bi, uint64_t (&w3)[SB]) {
@@ -576,7 +583,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
     const double step = sq * z;
     double xn = r.x + step;
     if (SINGLE) xn = (double)(float)xn;
-    const double resid = a.y - xn;
+    const double resid = yobs - xn;
     const double h = (0.5 * resid) * resid;
     Rec o;
     o.x = xn;
@@ -654,7 +661,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
 #pragma unroll
       for (int b = 0; b < SB; ++b) {
         const int64_t j = bi * batch + b * (int64_t)nth + threadIdx.x;
-        const Philox4 P = philox_block(a.dr.seed, (uint64_t)(a.dr.gbase + j), (uint64_t)a.t);
+        const Philox4 P = philox_block(dseed, (uint64_t)(a.dr.gbase + j), (uint64_t)a.t);
         if (j < a.n) a.dr.u3[j] = P.w[3];
         // tables only (FD runs with gamma_method 0): no call into the
         // accurate solvers, which would cost the kernel a stack frame
