@@ -141,3 +141,37 @@ def test_backend_shard_arguments():
         P.Backend("cuda", shards=3)
     with pytest.raises(ValueError):
         P.Backend("cuda", shards=2, devices=[0])
+
+
+def test_backend_run_covers_ranges_and_reraises():
+    """Backend.run (reference backend.py:52-70): fn(lo, hi) over disjoint lane
+    ranges covering [0, n), a barrier in both modes, lane exceptions re-raised."""
+    for mode, lanes in (("sequential", 1), ("parallel", 4), ("cuda", 1)):
+        b = P.Backend(mode, lanes=lanes, min_chunk=16)
+        out = np.zeros(1000, dtype=np.int64)
+
+        def fn(lo, hi):
+            out[lo:hi] += np.arange(lo, hi)
+
+        b.run(1000, fn)
+        assert np.array_equal(out, np.arange(1000))
+        b.run(0, fn)  # no-op
+        if mode == "parallel":
+            assert len(b.split(1000)) == 4
+
+        def bad(lo, hi):
+            if hi == 1000:  # the last lane fails
+                raise ValueError("lane failed")
+
+        with pytest.raises(ValueError):
+            b.run(1000, bad)
+        b.close()
+
+
+def test_spacings_resampler_is_accepted_and_needs_power_of_two():
+    with pytest.raises(P.NotPowerOfTwoError):
+        P.run_particle_filter(P.TrendNoiseModel(), [1.0], 100, resampler="spacings")
+    from paper_1212_1639_b200 import _lib
+    from paper_1212_1639_b200.filtering import PERF_RESAMPLERS
+
+    assert "spacings" in PERF_RESAMPLERS and _lib.RESAMPLER_CODES["spacings"] == 5
