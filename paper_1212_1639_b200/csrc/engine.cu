@@ -949,7 +949,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     return v ? atoi(v) : -1;
   }();
   const bool fused = c.gamma_method == 0 && e->ntab &&
-                     (fused_env >= 0 ? fused_env != 0 : n >= ((int64_t)1 << 22));
+                     (fused_env >= 0 ? fused_env != 0 : n >= ((int64_t)1 << 21));
   e->last_path = (fused ? PF_PATH_FUSED_DRAWS : 0) | (e->strata ? PF_PATH_RANK_TABLES : 0) |
                  (uses_cut_tables(c.resampler) && fuse_top() ? PF_PATH_FUSED_TOP : 0);
   const int STEP_THREADS = fused ? FD_THREADS : 256;

@@ -1,6 +1,6 @@
 """Oracle parity on the benchmarked kernel path.
 
-At N >= 2^22 the engine runs the fused-draws step kernel (draws computed in
+At N >= 2^21 the engine runs the fused-draws step kernel (draws computed in
 the step kernel, csrc/step.cuh step_kernel<..., true>), strata rank-table
 lookups (N >= 2^21) and the top tree in K2's last CTA -- the path bench.py
 measures at configs[2].  These tests feed the reference's own noise draws
