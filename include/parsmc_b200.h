@@ -230,9 +230,10 @@ int pf_shard_close_peers(pf_shard* s);
 int pf_shard_destroy(pf_shard* s);
 
 /* ------------------------------------------------- kernel level (L2) --- */
-/* All kernel-level entries take HOST pointers and run synchronously on the
- * current device; they exist for parity tests and for the reference's
- * kernel-level API surface. */
+/* These kernel-level entries take HOST pointers and run synchronously on
+ * the current device; they exist for parity tests and for the reference's
+ * kernel-level API surface.  The *_d forms below take device pointers and
+ * a stream. */
 
 /* philox_block_lanes (rng.py:103-110): words_out is [4][n]. */
 int pf_philox_block(uint64_t seed, const uint64_t* stream_ids, int64_t n,
@@ -276,6 +277,38 @@ int pf_resample_cutpoint(const void* q, int64_t n, int32_t dtype, uint64_t seed,
 /* weighted_quantiles (filtering.py:135-140); weights dtype PF_DTYPE_F64/F32. */
 int pf_weighted_quantiles(const double* values, const void* weights, int32_t wdtype,
                           int64_t n, const double* probs, int32_t nprobs, double* out);
+
+/* ------------------- kernel level, device pointers + stream (L2d) --- */
+/* The same operations on DEVICE-resident buffers (every pointer argument is
+ * device memory on the current device), enqueued on `stream` (a
+ * cudaStream_t; NULL = the legacy default stream) and returning without a
+ * host synchronisation.  Scratch comes from the stream's memory pool
+ * (cudaMallocAsync) and is returned stream-ordered.  Size and dtype checks
+ * return an error code as above; data-dependent conditions cannot (nothing
+ * is read back), so each entry documents where they show up instead.
+ * Results are bit-identical to the host-pointer forms on the same inputs. */
+
+/* uniforms_at (rng.py:122-140). */
+int pf_uniforms_at_d(uint64_t seed, const uint64_t* stream_ids, const uint64_t* counters,
+                     int64_t n, double* u_out, void* stream);
+/* parallel_cdf (prefix_sum.py:109-127).  total_out (device f64, optional)
+ * receives the adder-tree root: the caller's all-zero / non-finite check
+ * (prefix_sum.py:94-106 raises there) is `!(total > 0) || !isfinite(total)`. */
+int pf_tree_cdf_d(const void* w, int64_t n, int32_t dtype, void* q_out, double* total_out,
+                  void* stream);
+/* cut_points_parallel (resampling.py:110-134): 1-based cut table. */
+int pf_cut_table_d(const void* q, int64_t n, int32_t dtype, int64_t* cuts_out, void* stream);
+/* cutpoint_indices (resampling.py:146-158) over m device uniforms. */
+int pf_cutpoint_lookup_d(const void* q, const int64_t* cuts, int64_t n, int32_t dtype,
+                         const double* u, int64_t m, int64_t* idx_out, void* stream);
+/* resample_cutpoint (resampling.py:161-177), as pf_resample_cutpoint. */
+int pf_resample_cutpoint_d(const void* q, int64_t n, int32_t dtype, uint64_t seed,
+                           uint64_t counter, int64_t* idx_out, void* stream);
+/* weighted_quantiles (filtering.py:135-140); probs and out are device
+ * arrays of nprobs doubles. */
+int pf_weighted_quantiles_d(const double* values, const void* weights, int32_t wdtype,
+                            int64_t n, const double* probs, int32_t nprobs, double* out,
+                            void* stream);
 
 #ifdef __cplusplus
 }

@@ -39,6 +39,7 @@ RESAMPLER_CODES = {"cutpoint": 0, "naive": 1, "sorted": 2, "stratified": 3, "sys
 _dp = C.POINTER(C.c_double)
 _i64p = C.POINTER(C.c_int64)
 _u64p = C.POINTER(C.c_uint64)
+_vp = C.c_void_p
 
 
 class PfConfig(C.Structure):
@@ -128,6 +129,13 @@ SIGNATURES = {
     "pf_merge_indices": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, _dp, C.c_int64, C.c_int32, _i64p]),
     "pf_resample_cutpoint": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_uint64, C.c_uint64, _i64p]),
     "pf_weighted_quantiles": (C.c_int, [_dp, C.c_void_p, C.c_int32, C.c_int64, _dp, C.c_int32, _dp]),
+    # device-pointer forms: every pointer is device memory, last arg the stream
+    "pf_uniforms_at_d": (C.c_int, [C.c_uint64, _vp, _vp, C.c_int64, _vp, _vp]),
+    "pf_tree_cdf_d": (C.c_int, [_vp, C.c_int64, C.c_int32, _vp, _vp, _vp]),
+    "pf_cut_table_d": (C.c_int, [_vp, C.c_int64, C.c_int32, _vp, _vp]),
+    "pf_cutpoint_lookup_d": (C.c_int, [_vp, _vp, C.c_int64, C.c_int32, _vp, C.c_int64, _vp, _vp]),
+    "pf_resample_cutpoint_d": (C.c_int, [_vp, C.c_int64, C.c_int32, C.c_uint64, C.c_uint64, _vp, _vp]),
+    "pf_weighted_quantiles_d": (C.c_int, [_vp, _vp, C.c_int32, C.c_int64, _vp, C.c_int32, _vp, _vp]),
 }
 
 _lib = None
@@ -206,3 +214,31 @@ def dtype_code(dt):
     if dt == np.float32:
         return PF_DTYPE_F32
     raise TypeError(f"unsupported dtype {dt}")
+
+
+def is_cuda_tensor(x):
+    """True for a torch tensor on a CUDA device (checked without importing
+    torch when the caller never did)."""
+    return type(x).__module__.startswith("torch") and bool(getattr(x, "is_cuda", False))
+
+
+def dptr(t):
+    """Device pointer of a contiguous torch CUDA tensor (or None)."""
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def current_stream(t):
+    """The torch current stream of t's device, as the void* the *_d entries take."""
+    import torch
+
+    return C.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def device_dtype_code(t):
+    import torch
+
+    if t.dtype == torch.float64:
+        return PF_DTYPE_F64
+    if t.dtype == torch.float32:
+        return PF_DTYPE_F32
+    raise TypeError(f"expected a float32 or float64 tensor, got {t.dtype}")

@@ -57,17 +57,29 @@ template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t cap = 0;
+  // Stream-ordered mode (the kernel-level *_d entries): allocate and free
+  // with cudaMallocAsync / cudaFreeAsync on `ord`, so the caller's stream
+  // never waits on a device-wide cudaFree.
+  bool ordered = false;
+  cudaStream_t ord = nullptr;
+  void order_on(cudaStream_t s) {
+    ordered = true;
+    ord = s;
+  }
   cudaError_t ensure(size_t count) {
     if (count <= cap && p) return cudaSuccess;
-    if (p) cudaFree(p);
-    p = nullptr;
-    cap = 0;
-    cudaError_t e = cudaMalloc((void**)&p, (count ? count : 1) * sizeof(T));
+    release();
+    const size_t bytes = (count ? count : 1) * sizeof(T);
+    cudaError_t e = ordered ? cudaMallocAsync((void**)&p, bytes, ord) : cudaMalloc((void**)&p, bytes);
     if (e == cudaSuccess) cap = count;
+    else p = nullptr;
     return e;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (ordered) cudaFreeAsync(p, ord);
+      else cudaFree(p);
+    }
     p = nullptr;
     cap = 0;
   }
@@ -205,6 +217,12 @@ struct QuantileScratch {
     tmp_bytes = b1 > b2 ? b1 : b2;
     return tmp.ensure(tmp_bytes);
   }
+  void order_on(cudaStream_t s) {
+    kin.order_on(s); kout.order_on(s); iin.order_on(s); iout.order_on(s); ws.order_on(s); tmp.order_on(s);
+  }
+  void release() {
+    kin.release(); kout.release(); iin.release(); iout.release(); ws.release(); tmp.release();
+  }
 };
 
 template <typename TQ>
@@ -316,7 +334,16 @@ struct CdfBufs {
         (e = node.ensure(plan.chunks * esz)) || (e = carry.ensure(plan.chunks * esz)) ||
         (e = total.ensure(2 * esz)) || (e = top_scratch.ensure(4 * plan.chunks * esz)) || (e = top_ctr.ensure(1)))
       return e;
-    return cudaMemset(top_ctr.p, 0, sizeof(unsigned int));
+    return top_ctr.ordered ? cudaMemsetAsync(top_ctr.p, 0, sizeof(unsigned int), top_ctr.ord)
+                           : cudaMemset(top_ctr.p, 0, sizeof(unsigned int));
+  }
+  void order_on(cudaStream_t s) {
+    tile_tot.order_on(s); chunk_tot.order_on(s); node.order_on(s); carry.order_on(s); total.order_on(s);
+    top_scratch.order_on(s); top_ctr.order_on(s);
+  }
+  void release() {
+    tile_tot.release(); chunk_tot.release(); node.release(); carry.release(); total.release();
+    top_scratch.release(); top_ctr.release();
   }
 };
 
@@ -2391,11 +2418,7 @@ int pf_engine_destroy(pf_engine* e) {
   e->partials.release();
   e->sc.release();
   e->fail.release();
-  e->cdf.tile_tot.release();
-  e->cdf.chunk_tot.release();
-  e->cdf.node.release();
-  e->cdf.carry.release();
-  e->cdf.total.release();
+  e->cdf.release();
   e->keys.release();
   e->qtg.release();
   e->qsh.release();
@@ -2527,6 +2550,41 @@ struct Scratch {
   }
 };
 
+// Stream-ordered RAII scratch for the device-pointer (*_d) entries: memory
+// comes from the stream's pool (cudaMallocAsync) and goes back with
+// cudaFreeAsync after the entry's last launch, so nothing blocks the host.
+struct StreamScratch {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit StreamScratch(cudaStream_t s) : st(s) {}
+  ~StreamScratch() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+  template <typename T>
+  cudaError_t alloc(T** p, size_t count) {
+    cudaError_t e = cudaMallocAsync((void**)p, (count ? count : 1) * sizeof(T), st);
+    if (e == cudaSuccess) ptrs.push_back(*p);
+    return e;
+  }
+};
+
+__global__ void widen_kernel(const float* in, int64_t n, double* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (double)in[i];
+}
+
+template <typename T>
+__global__ void total_out_kernel(const T* total, double* out) {
+  out[0] = (double)total[0];
+}
+
+cudaStream_t as_stream(void* s) { return (cudaStream_t)s; }
+int check_dtype(int32_t dtype) {
+  if (dtype != PF_DTYPE_F64 && dtype != PF_DTYPE_F32)
+    return set_err(PF_ERR_VALUE, "dtype must be PF_DTYPE_F64 or PF_DTYPE_F32");
+  return PF_OK;
+}
+
 int need_device() {
   if (pf_device_count() < 1) return set_err(PF_ERR_CUDA, "no CUDA device visible");
   return PF_OK;
@@ -2584,7 +2642,7 @@ int tree_cdf_impl(const std::vector<double>& w, int64_t n, T* q_host, double* to
     if (q_host) cudaMemcpy(q_host, dq, n * sizeof(T), cudaMemcpyDeviceToHost);
     if (cut_dev_out) cudaMemcpy(cut_dev_out, dcut, n * sizeof(int32_t), cudaMemcpyDeviceToDevice);
   }
-  b.tile_tot.release(); b.chunk_tot.release(); b.node.release(); b.carry.release(); b.total.release();
+  b.release();
   if (rc != PF_OK) return rc;
   if (total_host) *total_host = (double)tot;
   if (!std::isfinite((double)tot)) return set_err(PF_ERR_ALL_WEIGHTS_ZERO, "weight total is not finite");
@@ -2938,8 +2996,182 @@ int pf_weighted_quantiles(const double* values, const void* weights, int32_t wdt
     cudaError_t e = cudaMemcpy(out, dout, nprobs * 8, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) rc = set_err(PF_ERR_CUDA, cudaGetErrorString(e));
   }
-  qs.kin.release(); qs.kout.release(); qs.iin.release(); qs.iout.release(); qs.ws.release(); qs.tmp.release();
+  qs.release();
   return rc;
+}
+
+/* ---------------- kernel level, device pointers + caller's stream ---- */
+// The same kernels as the host-pointer entries above, on device-resident
+// data, enqueued on the caller's stream without a host synchronisation.
+// Argument checks that need only sizes run on the host (and return an error
+// code); data-dependent failures cannot, because nothing is read back --
+// see the header for how each entry reports them.
+
+int pf_uniforms_at_d(uint64_t seed, const uint64_t* ids, const uint64_t* ctr, int64_t n, double* u_out,
+                     void* stream) {
+  int rc;
+  if ((rc = need_device())) return rc;
+  if (n <= 0) return PF_OK;
+  uniforms_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(seed, ids, ctr, n, u_out);
+  LAUNCHED();
+  CK(cudaGetLastError());
+  return PF_OK;
+}
+
+int pf_tree_cdf_d(const void* w, int64_t n, int32_t dtype, void* q_out, double* total_out, void* stream) {
+  int rc;
+  if ((rc = check_dtype(dtype))) return rc;
+  if (n < 1) return set_err(PF_ERR_VALUE, "empty weights");
+  if (!is_pow2(n)) return set_err(PF_ERR_NOT_POWER_OF_TWO, "parallel CDF needs a power-of-two particle count, got " + std::to_string(n));
+  if ((rc = need_device())) return rc;
+  cudaStream_t st = as_stream(stream);
+  StreamScratch s(st);
+  const double* dw = (const double*)w;
+  if (dtype == PF_DTYPE_F32) {
+    double* wide;
+    CK(s.alloc(&wide, n));
+    widen_kernel<<<grid_for(n, 256), 256, 0, st>>>((const float*)w, n, wide);
+    LAUNCHED();
+    dw = wide;
+  }
+  int32_t* dcut;
+  int64_t* dfail;
+  CK(s.alloc(&dcut, n));
+  CK(s.alloc(&dfail, 1));
+  CK(cudaMemsetAsync(dfail, 0, sizeof(int64_t), st));
+  CdfBufs b;
+  b.order_on(st);
+  const size_t es = dtype == PF_DTYPE_F32 ? 4 : 8;
+  if (cudaError_t e = b.ensure(n, es)) {
+    b.release();
+    return set_err(e == cudaErrorMemoryAllocation ? PF_ERR_OUT_OF_MEMORY : PF_ERR_CUDA, cudaGetErrorString(e));
+  }
+  WSrc src;
+  src.src = dw;
+  src.M = nullptr;
+  src.mode = 1;
+  if (dtype == PF_DTYPE_F32) {
+    rc = launch_cdf<float>(b, src, n, (float*)q_out, dcut, dfail, 0, st);
+    if (rc == PF_OK && total_out) { total_out_kernel<float><<<1, 1, 0, st>>>((const float*)b.total.p, total_out); LAUNCHED(); }
+  } else {
+    rc = launch_cdf<double>(b, src, n, (double*)q_out, dcut, dfail, 0, st);
+    if (rc == PF_OK && total_out) { total_out_kernel<double><<<1, 1, 0, st>>>((const double*)b.total.p, total_out); LAUNCHED(); }
+  }
+  b.release();
+  if (rc != PF_OK) return rc;
+  CK(cudaGetLastError());
+  return PF_OK;
+}
+
+int pf_cut_table_d(const void* q, int64_t n, int32_t dtype, int64_t* cuts_out, void* stream) {
+  int rc;
+  if ((rc = check_dtype(dtype))) return rc;
+  if (n < 1) return set_err(PF_ERR_VALUE, "empty CDF");
+  if ((rc = need_device())) return rc;
+  cudaStream_t st = as_stream(stream);
+  StreamScratch s(st);
+  int32_t* dc;
+  CK(s.alloc(&dc, n));
+  CK(cudaMemsetAsync(dc, 0, n * 4, st));
+  if (dtype == PF_DTYPE_F64)
+    cut_table_kernel<double><<<grid_for(n, 256), 256, 0, st>>>((const double*)q, n, dc);
+  else
+    cut_table_kernel<float><<<grid_for(n, 256), 256, 0, st>>>((const float*)q, n, dc);
+  LAUNCHED();
+  cuts_to_i64_kernel<<<grid_for(n, 256), 256, 0, st>>>(dc, n, cuts_out);
+  LAUNCHED();
+  CK(cudaGetLastError());
+  return PF_OK;
+}
+
+int pf_cutpoint_lookup_d(const void* q, const int64_t* cuts, int64_t n, int32_t dtype, const double* u,
+                         int64_t m, int64_t* idx_out, void* stream) {
+  int rc;
+  if ((rc = check_dtype(dtype))) return rc;
+  if (n < 1) return set_err(PF_ERR_VALUE, "empty CDF");
+  if ((rc = need_device())) return rc;
+  if (m <= 0) return PF_OK;
+  cudaStream_t st = as_stream(stream);
+  StreamScratch s(st);
+  int32_t* dc;
+  CK(s.alloc(&dc, n));
+  cuts_to_i32_kernel<<<grid_for(n, 256), 256, 0, st>>>(cuts, n, dc);
+  LAUNCHED();
+  if (dtype == PF_DTYPE_F64)
+    lookup_kernel<double><<<grid_for(m, 256), 256, 0, st>>>((const double*)q, dc, n, u, m, idx_out);
+  else
+    lookup_kernel<float><<<grid_for(m, 256), 256, 0, st>>>((const float*)q, dc, n, u, m, idx_out);
+  LAUNCHED();
+  CK(cudaGetLastError());
+  return PF_OK;
+}
+
+int pf_resample_cutpoint_d(const void* q, int64_t n, int32_t dtype, uint64_t seed, uint64_t counter,
+                           int64_t* idx_out, void* stream) {
+  int rc;
+  if ((rc = check_dtype(dtype))) return rc;
+  if (n < 1) return set_err(PF_ERR_VALUE, "empty CDF");
+  if ((rc = need_device())) return rc;
+  cudaStream_t st = as_stream(stream);
+  StreamScratch s(st);
+  int32_t* dc;
+  double* du;
+  CK(s.alloc(&dc, n));
+  CK(s.alloc(&du, n));
+  CK(cudaMemsetAsync(dc, 0, n * 4, st));
+  stream_uniforms_kernel<<<grid_for(n, 256), 256, 0, st>>>(seed, counter, n, du);
+  LAUNCHED();
+  if (dtype == PF_DTYPE_F64) {
+    cut_table_kernel<double><<<grid_for(n, 256), 256, 0, st>>>((const double*)q, n, dc);
+    lookup_kernel<double><<<grid_for(n, 256), 256, 0, st>>>((const double*)q, dc, n, du, n, idx_out);
+  } else {
+    cut_table_kernel<float><<<grid_for(n, 256), 256, 0, st>>>((const float*)q, n, dc);
+    lookup_kernel<float><<<grid_for(n, 256), 256, 0, st>>>((const float*)q, dc, n, du, n, idx_out);
+  }
+  LAUNCHED();
+  LAUNCHED();
+  CK(cudaGetLastError());
+  return PF_OK;
+}
+
+int pf_weighted_quantiles_d(const double* values, const void* weights, int32_t wdtype, int64_t n,
+                            const double* probs, int32_t nprobs, double* out, void* stream) {
+  int rc;
+  if ((rc = check_dtype(wdtype))) return rc;
+  if (n < 1) return set_err(PF_ERR_VALUE, "empty values");
+  if (nprobs < 1 || nprobs > 32) return set_err(PF_ERR_VALUE, "1..32 probabilities supported");
+  if ((rc = need_device())) return rc;
+  cudaStream_t st = as_stream(stream);
+  StreamScratch s(st);
+  const double* dw = (const double*)weights;
+  if (wdtype == PF_DTYPE_F32) {
+    double* wide;
+    CK(s.alloc(&wide, n));
+    widen_kernel<<<grid_for(n, 256), 256, 0, st>>>((const float*)weights, n, wide);
+    LAUNCHED();
+    dw = wide;
+  }
+  int64_t* dfail;
+  CK(s.alloc(&dfail, 1));
+  CK(cudaMemsetAsync(dfail, 0, 8, st));
+  QuantileScratch qs;
+  qs.order_on(st);
+  if (cudaError_t e = qs.ensure(n)) {
+    qs.release();
+    return set_err(e == cudaErrorMemoryAllocation ? PF_ERR_OUT_OF_MEMORY : PF_ERR_CUDA, cudaGetErrorString(e));
+  }
+  WSrc src;
+  src.src = dw;
+  src.M = nullptr;
+  src.mode = 1;
+  if (wdtype == PF_DTYPE_F32)
+    rc = weighted_quantiles_dev<float>(qs, values, src, n, probs, nprobs, out, st, dfail);
+  else
+    rc = weighted_quantiles_dev<double>(qs, values, src, n, probs, nprobs, out, st, dfail);
+  qs.release();
+  if (rc != PF_OK) return rc;
+  CK(cudaGetLastError());
+  return PF_OK;
 }
 
 }  // extern "C"

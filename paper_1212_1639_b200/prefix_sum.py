@@ -97,7 +97,12 @@ def _finalize_check(total):
 
 def parallel_cdf(weights, backend=None, pad=False):
     """q(i) = s(i)/s(N) from the two adder passes (prefix_sum.py:109-127).
-    ``pad=True`` zero-extends a non-power-of-two input."""
+    ``pad=True`` zero-extends a non-power-of-two input.  A CUDA tensor stays
+    on the device (device_ops.parallel_cdf) and a device tensor comes back."""
+    if _lib.is_cuda_tensor(weights):
+        from . import device_ops
+
+        return device_ops.parallel_cdf(weights, pad=pad)
     w = check_weights(weights)
     w = _float_array(w)
     n = w.shape[0]

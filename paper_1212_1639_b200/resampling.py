@@ -43,6 +43,10 @@ def cut_points_bruteforce(cdf):
 
 def cut_points_parallel(cdf, backend=None):
     """1-based cut-point table (resampling.py:110-134)."""
+    if _lib.is_cuda_tensor(cdf):
+        from . import device_ops
+
+        return device_ops.cut_points_parallel(cdf)
     q = _cdf_array(cdf)
     out = np.empty(len(q), dtype=np.int64)
     lib = _lib.require_device()
@@ -53,6 +57,10 @@ def cut_points_parallel(cdf, backend=None):
 
 def cutpoint_indices(cdf, cuts, u):
     """Cut-point lookup for an array of uniforms (resampling.py:146-158)."""
+    if _lib.is_cuda_tensor(cdf):
+        from . import device_ops
+
+        return device_ops.cutpoint_indices(cdf, _on_device(cuts, cdf), _on_device(u, cdf))
     q = _cdf_array(cdf)
     cuts = np.ascontiguousarray(np.asarray(cuts, dtype=np.int64))
     u = np.ascontiguousarray(np.asarray(u, dtype=np.float64))
@@ -73,7 +81,10 @@ def cut_point_draw(cdf, cuts, u):
 
 def resample_cutpoint(cdf, streams, backend=None):
     """Exact multinomial resampling (resampling.py:161-177): one uniform per
-    stream, cut table, lookup; 1-based indices."""
+    stream, cut table, lookup; 1-based indices.  A CUDA-tensor CDF stays on
+    the device and device indices come back."""
+    if _lib.is_cuda_tensor(cdf):
+        return _resample_cutpoint_device(cdf, streams)
     q = _cdf_array(cdf)
     n = len(q)
     c = streams.lockstep_counter() if hasattr(streams, "lockstep_counter") else None
@@ -88,6 +99,26 @@ def resample_cutpoint(cdf, streams, backend=None):
         return out
     u = streams.uniforms()
     return cutpoint_indices(q, cut_points_parallel(q), u)
+
+
+def _on_device(x, like):
+    import torch
+
+    return torch.as_tensor(x, device=like.device)
+
+
+def _resample_cutpoint_device(cdf, streams):
+    from . import device_ops
+
+    n = cdf.shape[0]
+    c = streams.lockstep_counter() if hasattr(streams, "lockstep_counter") else None
+    if c is not None and len(streams) == n and np.array_equal(
+            streams.stream_ids, np.arange(n, dtype=np.uint64)):
+        out = device_ops.resample_cutpoint(cdf, streams.seed, c)
+        streams.skip(1)
+        return out
+    u = _on_device(streams.uniforms(), cdf)
+    return device_ops.cutpoint_indices(cdf, device_ops.cut_points_parallel(cdf), u)
 
 
 def merge_indices(cdf, u, sort_first=False):

@@ -50,7 +50,12 @@ def philox_block_lanes(block, seed, stream_ids):
 
 
 def uniforms_at(seed, stream_ids, counters):
-    """Uniform(0,1) draw for each (stream_id, counter) pair (rng.py:122-140)."""
+    """Uniform(0,1) draw for each (stream_id, counter) pair (rng.py:122-140).
+    CUDA-tensor stream ids run on the device stream (device_ops)."""
+    if _lib.is_cuda_tensor(stream_ids):
+        from . import device_ops
+
+        return device_ops.uniforms_at(seed, stream_ids, counters)
     ids, ctr = np.broadcast_arrays(np.asarray(stream_ids, dtype=np.uint64),
                                    np.asarray(counters, dtype=np.uint64))
     shape = ids.shape
