@@ -154,6 +154,18 @@ int pf_engine_run(pf_engine* e, const double* y, int64_t t_len,
 /* Device-resident repeat of the last run's workload: y is already on the
  * device; no host outputs are copied.  Used by bench.py for the kernel-only
  * throughput (value); pf_engine_run is the end-to-end path (e2e). */
+/* Batched replications (BASELINE configs[4]; the paper's timing experiment,
+ * replication r = an independent run with seed seeds[r]): `reps` filters of
+ * the engine's n particles on the same series, every kernel launch covering
+ * all of them.  Outputs are the per-step summaries only, each [reps][t_len]
+ * row-major (quantiles [reps][t_len][k]); indices, store and final states
+ * must be NULL.  Each replication follows pf_engine_run with that seed:
+ * the same particles and ancestors; means / sds to rounding and quantiles
+ * except at exact near-ties (the weight sums are split over fewer CTAs per
+ * replication).  reps > 1 needs
+ * cut-point resampling, gamma_method 0 and 2^11 <= n < 2^21. */
+int pf_engine_run_batch(pf_engine* e, const uint64_t* seeds, int32_t reps, const double* y,
+                        int64_t t_len, pf_outputs* out);
 int pf_engine_run_resident(pf_engine* e, int64_t t_len);
 /* Device time (ms, CUDA events) of the last run / resident run, and the
  * average duration and launch count of the step kernel inside it. */

@@ -92,6 +92,7 @@ SIGNATURES = {
     "pf_engine_reconfigure": (C.c_int, [C.c_void_p, C.POINTER(PfConfig)]),
     "pf_engine_run": (C.c_int, [C.c_void_p, _dp, C.c_int64, C.POINTER(PfFeed), C.POINTER(PfOutputs)]),
     "pf_engine_run_resident": (C.c_int, [C.c_void_p, C.c_int64]),
+    "pf_engine_run_batch": (C.c_int, [C.c_void_p, _u64p, C.c_int32, _dp, C.c_int64, C.POINTER(PfOutputs)]),
     "pf_engine_last_timing": (C.c_int, [C.c_void_p, _dp, _dp, _i64p, _i64p]),
     "pf_engine_quantile_stats": (C.c_int, [C.c_void_p, _i64p]),
     "pf_engine_last_path": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),

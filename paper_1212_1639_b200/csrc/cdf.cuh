@@ -43,6 +43,16 @@ struct WSrc {
   int mode;
 };
 
+// Batched replications (gridDim.z = R, step.cuh RepStride): the weight
+// source of replication blockIdx.z -- its n_r log-weights and its max, held
+// per replication by step parity ([R][2]).
+PF_D WSrc wsrc_rep(WSrc s, int64_t n_r) {
+  const int64_t r = blockIdx.z;
+  s.src += r * n_r;
+  if (s.M) s.M += 2 * r;
+  return s;
+}
+
 template <typename T>
 PF_D T weight_of(double v, double M, int mode) {
   return mode == 0 ? (T)exp(v - M) : (T)v;
@@ -203,6 +213,21 @@ template <typename T>
 __global__ void __launch_bounds__(CDF_THREADS)
 cdf_reduce_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ chunk_tot,
                   const int64_t* __restrict__ fail, TopFuse<T> top = TopFuse<T>()) {
+  if (gridDim.z > 1) {  // batched replications: replication blockIdx.z's tree
+    const int64_t r = blockIdx.z, G = gridDim.x;
+    src = wsrc_rep(src, G * R * CDF_TILE);
+    tile_tot += r * G * R;
+    chunk_tot += r * G;
+    if (fail) fail += r;
+    if (top.ctr) {
+      top.ctr += r;
+      top.scratch += r * 4 * G;
+      top.node += r * G;
+      top.carry += r * G;
+      top.total += 2 * r;
+      top.fail += r;
+    }
+  }
   pdl_wait();
   pdl_launch_dependents();
   if (fail && *fail) return;
@@ -351,6 +376,17 @@ cdf_expand_kernel(WSrc src, int64_t n, int R, const T* __restrict__ tile_tot,
                   const T* __restrict__ total_p, T* __restrict__ q_out,
                   int32_t* __restrict__ cut_out, const int64_t* __restrict__ fail,
                   RankOut ro = RankOut(), int64_t gbase = 0) {
+  if (gridDim.z > 1) {  // batched replications (non-strata tables only)
+    const int64_t r = blockIdx.z, G = gridDim.x;
+    src = wsrc_rep(src, n);
+    tile_tot += r * G * R;
+    node += r * G;
+    carry += r * G;
+    total_p += 2 * r;
+    q_out += r * n;
+    cut_out += r * n;
+    if (fail) fail += r;
+  }
   pdl_wait();
   pdl_launch_dependents();
   if (fail && *fail) return;

@@ -254,7 +254,7 @@ int weighted_quantiles_dev(QuantileScratch& s, const double* vals, WSrc w, int64
 constexpr int CLS_THR = 256;
 template <typename TQ, int QM>
 int launch_reduce_qr_m(int grid, WSrc src, int R, TQ* tt, TQ* ct, int64_t* fail, const QArgs& qa,
-                       cudaStream_t st) {
+                       cudaStream_t st, int reps) {
   constexpr int NQ = (QM & 1) + ((QM >> 1) & 1) + ((QM >> 2) & 1);
   const size_t smem = (size_t)NQ * (2 * Q_PER + 1) * CLS_THR * sizeof(double);
   auto kern = cdf_reduce_qr_kernel<TQ, QM, false, CLS_THR>;
@@ -274,8 +274,8 @@ int launch_reduce_qr_m(int grid, WSrc src, int R, TQ* tt, TQ* ct, int64_t* fail,
   }();
   const int64_t tiles = R * (int64_t)(CDF_THREADS / CLS_THR);  // R: K2 tiles
   const int64_t want = env_grid > 0 ? std::min<int64_t>(env_grid, CDF_MAX_CHUNKS) : (int64_t)sm_count() * occ;
-  const int g = (int)std::min<int64_t>(tiles, want);
-  kern<<<g, CLS_THR, smem, st>>>(src, (int)tiles, tt, ct, fail, qa);
+  const int g = (int)std::min<int64_t>(tiles, std::max<int64_t>(1, want / reps));
+  kern<<<dim3(g, 1, reps), CLS_THR, smem, st>>>(src, (int)tiles, tt, ct, fail, qa);
   LAUNCHED();
   return PF_OK;
 }
@@ -309,15 +309,15 @@ int launch_classify(int qm, int grid, WSrc src, int tiles, int64_t* fail, const 
 
 template <typename TQ>
 int launch_reduce_qr(int qm, int grid, WSrc src, int R, TQ* tt, TQ* ct, int64_t* fail, const QArgs& qa,
-                     cudaStream_t st) {
+                     cudaStream_t st, int reps = 1) {
   switch (qm) {
-    case 1: return launch_reduce_qr_m<TQ, 1>(grid, src, R, tt, ct, fail, qa, st);
-    case 2: return launch_reduce_qr_m<TQ, 2>(grid, src, R, tt, ct, fail, qa, st);
-    case 3: return launch_reduce_qr_m<TQ, 3>(grid, src, R, tt, ct, fail, qa, st);
-    case 4: return launch_reduce_qr_m<TQ, 4>(grid, src, R, tt, ct, fail, qa, st);
-    case 5: return launch_reduce_qr_m<TQ, 5>(grid, src, R, tt, ct, fail, qa, st);
-    case 6: return launch_reduce_qr_m<TQ, 6>(grid, src, R, tt, ct, fail, qa, st);
-    case 7: return launch_reduce_qr_m<TQ, 7>(grid, src, R, tt, ct, fail, qa, st);
+    case 1: return launch_reduce_qr_m<TQ, 1>(grid, src, R, tt, ct, fail, qa, st, reps);
+    case 2: return launch_reduce_qr_m<TQ, 2>(grid, src, R, tt, ct, fail, qa, st, reps);
+    case 3: return launch_reduce_qr_m<TQ, 3>(grid, src, R, tt, ct, fail, qa, st, reps);
+    case 4: return launch_reduce_qr_m<TQ, 4>(grid, src, R, tt, ct, fail, qa, st, reps);
+    case 5: return launch_reduce_qr_m<TQ, 5>(grid, src, R, tt, ct, fail, qa, st, reps);
+    case 6: return launch_reduce_qr_m<TQ, 6>(grid, src, R, tt, ct, fail, qa, st, reps);
+    case 7: return launch_reduce_qr_m<TQ, 7>(grid, src, R, tt, ct, fail, qa, st, reps);
   }
   return set_err(PF_ERR_VALUE, "quantile mask");
 }
@@ -336,6 +336,18 @@ struct CdfBufs {
       return e;
     return top_ctr.ordered ? cudaMemsetAsync(top_ctr.p, 0, sizeof(unsigned int), top_ctr.ord)
                            : cudaMemset(top_ctr.p, 0, sizeof(unsigned int));
+  }
+  // R independent trees of n leaves each (batched replications): the plan of
+  // one tree, every per-tree array R times (see cdf.cuh wsrc_rep / K2 / K4)
+  cudaError_t ensure_batch(int64_t n, int64_t R, size_t esz) {
+    plan = cdf_plan(n);
+    cudaError_t e;
+    if ((e = tile_tot.ensure(R * plan.tiles * esz)) || (e = chunk_tot.ensure(R * plan.chunks * esz)) ||
+        (e = node.ensure(R * plan.chunks * esz)) || (e = carry.ensure(R * plan.chunks * esz)) ||
+        (e = total.ensure(2 * R * esz)) || (e = top_scratch.ensure(4 * R * plan.chunks * esz)) ||
+        (e = top_ctr.ensure(R)))
+      return e;
+    return cudaMemset(top_ctr.p, 0, R * sizeof(unsigned int));
   }
   void order_on(cudaStream_t s) {
     tile_tot.order_on(s); chunk_tot.order_on(s); node.order_on(s); carry.order_on(s); total.order_on(s);
@@ -376,14 +388,14 @@ int fb_hist_smem() {
 
 // One full wave of the fallback histogram kernel (a partial second wave
 // would cost a whole pass's latency for a third of the work).
-int fb_hist_grid(int64_t n) {
+int fb_hist_grid(int64_t n, int reps = 1) {
   static int occ = 0;
   if (!occ) {
     if (fb_hist_smem() != PF_OK) return 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, q_fallback_hist_kernel, 256, QFB_SMEM_BYTES);
     if (occ < 1) occ = 1;
   }
-  return grid_for(n, 256, sm_count() * occ);
+  return grid_for(n, 256, std::max(1, sm_count() * occ / reps));
 }
 
 // PF_CHAIN_DEBUG: events after each CDF-chain launch (resident diagnostics)
@@ -398,13 +410,17 @@ void chain_mark(cudaStream_t st) {
 
 template <typename T>
 int launch_cdf_tail(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t* fail, int64_t step,
-                    cudaStream_t st, StrataOut so = StrataOut(), bool top_done = false);
+                    cudaStream_t st, StrataOut so = StrataOut(), bool top_done = false, int reps = 1);
 
+// reps > 1: that many independent trees of n leaves in one launch each
+// (batched replications; K3 fused into K2, no strata tables)
 template <typename T>
 int launch_cdf(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t* fail, int64_t step,
-               cudaStream_t st, StrataOut so = StrataOut()) {
+               cudaStream_t st, StrataOut so = StrataOut(), int reps = 1) {
   const CdfPlan& p = b.plan;
   T* total = (T*)b.total.p;
+  if (reps > 1 && (p.small || so.on || !fuse_top()))
+    return set_err(PF_ERR_NOT_IMPLEMENTED, "batched CDF needs n >= one tile, fused top tree, no strata tables");
   if (p.small) {
     cdf_small_kernel<T><<<1, 256, 0, st>>>(src, n, q, cut, total, fail, step);
     LAUNCHED();
@@ -421,17 +437,17 @@ int launch_cdf(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t* fai
     top.fail = fail;
     top.step = step;
   }
-  CK(launch_pdl(PDL_K2, cdf_reduce_kernel<T>, dim3((int)p.chunks), dim3(CDF_THREADS), 0, st, src, p.R, (T*)b.tile_tot.p,
-                (T*)b.chunk_tot.p, (const int64_t*)fail, top));
+  CK(launch_pdl(PDL_K2, cdf_reduce_kernel<T>, dim3((int)p.chunks, 1, reps), dim3(CDF_THREADS), 0, st, src, p.R,
+                (T*)b.tile_tot.p, (T*)b.chunk_tot.p, (const int64_t*)fail, top));
   LAUNCHED();
   chain_mark(st);
-  return launch_cdf_tail<T>(b, src, n, q, cut, fail, step, st, so, fused);
+  return launch_cdf_tail<T>(b, src, n, q, cut, fail, step, st, so, fused, reps);
 }
 
 // K3 + K4 (after K2, or after the quantile-fused K2).
 template <typename T>
 int launch_cdf_tail(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t* fail, int64_t step,
-                    cudaStream_t st, StrataOut so, bool top_done) {
+                    cudaStream_t st, StrataOut so, bool top_done, int reps) {
   const CdfPlan& p = b.plan;
   T* total = (T*)b.total.p;
   T* tt = (T*)b.tile_tot.p;
@@ -461,8 +477,8 @@ int launch_cdf_tail(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t
     CK(launch_pdl(PDL_GRP, group_build_kernel, dim3(grid_for(ng, 256, 148 * 8)), dim3(256), 0, st,
                   (const int32_t*)so.ro.cut, ng, so.grp, (const int64_t*)fail));
   } else
-    cdf_expand_kernel<T, false><<<(int)p.chunks, CDF_THREADS, 0, st>>>(src, n, p.R, tt, nd, cr, total, q, cut,
-                                                                     fail);
+    cdf_expand_kernel<T, false><<<dim3((int)p.chunks, 1, reps), CDF_THREADS, 0, st>>>(src, n, p.R, tt, nd, cr, total,
+                                                                                    q, cut, fail);
   LAUNCHED();
   return PF_OK;
 }
@@ -774,6 +790,8 @@ struct RunSpec {
   const pf_feed* feed;
   pf_outputs* out;  // null for resident runs
   bool resident;
+  int64_t reps = 1;              // batched replications (pf_engine_run_batch): R filters per launch
+  const uint64_t* seeds = nullptr;  // their seeds [R]
 };
 
 template <int MODE, typename TQ>
@@ -782,6 +800,11 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   constexpr int SINGLE = (MODE & M_SINGLE) ? 1 : 0;
   const pf_config& c = e->cfg;
   const int64_t n = e->n, T = rs.T;
+  // batched replications: R independent filters of n slots each, every
+  // launch covering all of them (gridDim.z = R); NT slots in all.  Per-slot
+  // buffers hold replication r at [r n, (r+1) n) of each parity block.
+  const int64_t R = rs.reps > 1 ? rs.reps : 1;
+  const int64_t NT = n * R;
   cudaStream_t st = e->st;
   pf_outputs* out = rs.out;
   // PF_SKIP_QUANTILES=1: diagnostic only (measures the weighted-quantile
@@ -797,13 +820,27 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   int rc;
   if ((rc = build_tables(e, T)) != PF_OK) return rc;
 
-  const size_t TT = (size_t)(T > 0 ? T : 1);
+  const size_t TT = (size_t)(T > 0 ? T : 1) * R;  // [R][T] rows
   CK(e->o_fm.ensure(TT));
   const bool want_ess = out && out->ess;
   if (want_ess) CK(e->o_ess.ensure(TT));
   if (LS) { CK(e->o_sm.ensure(TT)); CK(e->o_ssd.ensure(TT)); CK(e->o_sq.ensure(TT * 5)); }
   if (LT) { CK(e->o_tm.ensure(TT)); CK(e->o_tsd.ensure(TT)); CK(e->o_tq.ensure(TT * 5)); }
   if (want_fq) CK(e->o_fq.ensure(TT * 3));
+  if (R > 1) {
+    // every per-slot / per-replication buffer of the batched path, R times
+    const size_t esz = e->single ? 4 : 8;
+    CK(e->rec[0].ensure(NT));
+    CK(e->rec[1].ensure(NT));
+    CK(e->lw.ensure(2 * NT));
+    CK(e->du3.ensure(3 * NT));
+    CK(e->q.ensure(NT * esz));
+    CK(e->cut.ensure(NT + 1));
+    CK(e->sc.ensure(R));
+    CK(e->fail.ensure(R));
+    CK(e->mbuf.ensure(2 * R));
+    CK(e->cdf.ensure_batch(n, R, esz));
+  }
   if (keep_idx) CK(e->idx.ensure(n));
 
   // ---- weighted-quantile targets (filtering.py:346-355): state probs when
@@ -834,23 +871,28 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   memset(&qa, 0, sizeof(qa));
   qa.ntarget = ntg;
   if (ntg) {
-    CK(e->keys.ensure((size_t)6 * n));
-    CK(e->qtg.ensure(Q_MAXT));
-    CK(e->qsh.ensure(2));
-    CK(e->qcand.ensure((size_t)ntg * qcap));
-    CK(e->qscratch.ensure((size_t)ntg * qcap));
-    CK(e->qpart.ensure((size_t)std::max<int64_t>(CDF_MAX_CHUNKS, sm_count() * 8) * (Q_SLOTS + 1)));
-    CK(e->qhist.ensure((size_t)Q_MAXT * Q_SUB));
-    CK(e->qfhist.ensure((size_t)Q_MAXT * Q_FB));
+    const size_t part_stride = (size_t)std::max<int64_t>(CDF_MAX_CHUNKS, sm_count() * 8) * (Q_SLOTS + 1);
+    CK(e->keys.ensure((size_t)6 * NT));
+    CK(e->qtg.ensure(Q_MAXT * R));
+    CK(e->qsh.ensure(2 * R));
+    CK(e->qcand.ensure((size_t)ntg * qcap * R));
+    CK(e->qscratch.ensure((size_t)ntg * qcap * R));
+    CK(e->qpart.ensure(part_stride * R));
+    CK(e->qhist.ensure((size_t)Q_MAXT * Q_SUB * R));
+    CK(e->qfhist.ensure((size_t)Q_MAXT * Q_FB * R));
     CK(e->qunres.ensure(4));
-    CK(e->qlidx.ensure((size_t)Q_MAXT * Q_LIST));
-    CK(e->qlw.ensure((size_t)Q_MAXT * Q_LIST));
+    CK(e->qlidx.ensure((size_t)Q_MAXT * Q_LIST * R));
+    CK(e->qlw.ensure((size_t)Q_MAXT * Q_LIST * R));
     qa.lidx = e->qlidx.p;
     qa.lw = e->qlw.p;
-    CK(cudaMemcpyAsync(e->qtg.p, tgs.data(), ntg * sizeof(QTarget), cudaMemcpyHostToDevice, st));
-    CK(cudaMemsetAsync(e->qsh.p, 0, 2 * sizeof(QShared), st));
-    CK(cudaMemsetAsync(e->qhist.p, 0, (size_t)Q_MAXT * Q_SUB * 8, st));
-    CK(cudaMemsetAsync(e->qfhist.p, 0, (size_t)Q_MAXT * Q_FB * 8, st));
+    qa.rslots = n;
+    qa.rpart = (int64_t)part_stride;
+    qa.rT = T;
+    for (int64_t r = 0; r < R; ++r)
+      CK(cudaMemcpyAsync(e->qtg.p + r * Q_MAXT, tgs.data(), ntg * sizeof(QTarget), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(e->qsh.p, 0, 2 * R * sizeof(QShared), st));
+    CK(cudaMemsetAsync(e->qhist.p, 0, (size_t)Q_MAXT * Q_SUB * 8 * R, st));
+    CK(cudaMemsetAsync(e->qfhist.p, 0, (size_t)Q_MAXT * Q_FB * 8 * R, st));
     CK(cudaMemsetAsync(e->qunres.p, 0, 4 * sizeof(unsigned int), st));
     qa.stats = e->qunres.p;
     qa.tg = e->qtg.p;
@@ -920,15 +962,19 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   s0h.ct = (LT && c.tau2_shape > 1.0) ? c.tau2_scale / (c.tau2_shape - 1.0) : 0.0;
   s0h.counter = 0;
   s0h.pad = 0;
-  CK(cudaMemcpyAsync(e->sc.p, &s0h, sizeof(Scalars), cudaMemcpyHostToDevice, st));
-  CK(cudaMemsetAsync(e->fail.p, 0, sizeof(int64_t), st));
+  for (int64_t r = 0; r < R; ++r)
+    CK(cudaMemcpyAsync(e->sc.p + r, &s0h, sizeof(Scalars), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(e->fail.p, 0, R * sizeof(int64_t), st));
 
-  // the run's seed and series in device memory (read by the loop's kernels)
-  CK(e->seed_dev.ensure(1));
+  // the run's seed(s) and series in device memory (read by the loop's kernels)
+  CK(e->seed_dev.ensure(R));
   CK(e->y_dev.ensure(TT));
+  if (R > 1) {
+    CK(cudaMemcpyAsync(e->seed_dev.p, rs.seeds, R * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+  }
   {
     const uint64_t sd = c.seed;
-    CK(cudaMemcpyAsync(e->seed_dev.p, &sd, sizeof(sd), cudaMemcpyHostToDevice, st));
+    if (R == 1) CK(cudaMemcpyAsync(e->seed_dev.p, &sd, sizeof(sd), cudaMemcpyHostToDevice, st));
     const double* yh = rs.y ? rs.y : e->y_host.data();
     if (T > 0) CK(cudaMemcpyAsync(e->y_dev.p, yh, (size_t)T * sizeof(double), cudaMemcpyHostToDevice, st));
   }
@@ -951,11 +997,12 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     a.feed_gt = row(fgt, 0);
     a.rec = e->rec[0].p;
     a.s2_init = nullptr;
+    a.seedp = R > 1 ? e->seed_dev.p : nullptr;
     if (T == 0 && keep_final && LS) {
       CK(e->s2init.ensure(n));
       a.s2_init = e->s2init.p;
     }
-    init_kernel<MODE><<<grid_for(n, 256), 256, 0, st>>>(a);
+    init_kernel<MODE><<<dim3(grid_for(n, 256), 1, R), 256, 0, st>>>(a);
     LAUNCHED();
   }
   mark(PH_INIT);
@@ -976,7 +1023,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     return v ? atoi(v) : -1;
   }();
   const bool fused = c.gamma_method == 0 && e->ntab &&
-                     (fused_env >= 0 ? fused_env != 0 : n >= ((int64_t)1 << 21));
+                     (fused_env >= 0 ? fused_env != 0 : NT >= ((int64_t)1 << 21));
   e->last_path = (fused ? PF_PATH_FUSED_DRAWS : 0) | (e->strata ? PF_PATH_RANK_TABLES : 0) |
                  (uses_cut_tables(c.resampler) && fuse_top() ? PF_PATH_FUSED_TOP : 0);
   const int STEP_THREADS = fused ? FD_THREADS : 256;
@@ -984,9 +1031,9 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   const size_t step_smem = (fused ? (size_t)(((draw_smem / 8) + 3) & ~size_t(3)) * 8 : 0) +
                            (size_t)2 * STEP_SBX * STEP_THREADS * (sizeof(Rec) + 3 * sizeof(double));
   if (!fused) {
-    CK(e->dz.ensure(3 * (size_t)n));
-    CK(e->dgs.ensure(3 * (size_t)n));
-    CK(e->dgt.ensure(3 * (size_t)n));
+    CK(e->dz.ensure(3 * (size_t)NT));
+    CK(e->dgs.ensure(3 * (size_t)NT));
+    CK(e->dgt.ensure(3 * (size_t)NT));
   }
   {
     static DevOnce attr;  // per MODE / TQ instantiation
@@ -1011,8 +1058,9 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   if (docc < 1) docc = 1;
   // persistent grids: one wave of resident CTAs
   const int64_t nbatches = (n + STEP_SBX * STEP_THREADS - 1) / (STEP_SBX * STEP_THREADS);
-  const int step_grid = (int)std::min<int64_t>(nbatches, (int64_t)sms * occ);
-  const int draw_grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sms * docc);
+  // (batched: one wave shared by the R replications)
+  const int step_grid = (int)std::min<int64_t>(nbatches, std::max<int64_t>(1, (int64_t)sms * occ / R));
+  const int draw_grid = (int)std::min<int64_t>((n + 255) / 256, std::max<int64_t>(1, (int64_t)sms * docc / R));
   auto launch_draws = [&](int64_t t, cudaStream_t s_) {
     DrawArgs d;
     memset(&d, 0, sizeof(d));
@@ -1023,14 +1071,14 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     d.gs = gamma_src(e, true, t);
     d.gt = gamma_src(e, false, t);
     d.ntab = e->ntab;
-    const size_t off = (size_t)(t % 3) * n;  // draws are triple-buffered
+    const size_t off = (size_t)(t % 3) * NT;  // draws are triple-buffered
     d.z = e->dz.p + off;
     d.g_s = e->dgs.p + off;
     d.g_t = e->dgt.p + off;
     d.u3 = e->du3.p + off;
     d.fail = e->fail.p;
     d.seedp = e->seed_dev.p;
-    draws_kernel<MODE><<<draw_grid, 256, draw_smem, s_>>>(d);
+    draws_kernel<MODE><<<dim3(draw_grid, 1, R), 256, draw_smem, s_>>>(d);
     LAUNCHED();
   };
   if (!fused && T >= 1) launch_draws(1, st);
@@ -1087,7 +1135,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
                          !(fz || fgs || fgt || fw) && uses_cut_tables(c.resampler);
   const bool use_graph = graphable;
   uint64_t gkey = graph_buffers_sig(e);
-  for (uint64_t v : {(uint64_t)T, (uint64_t)MODE, (uint64_t)fused, (uint64_t)ntg, (uint64_t)want_fq,
+  for (uint64_t v : {(uint64_t)T, (uint64_t)R, (uint64_t)MODE, (uint64_t)fused, (uint64_t)ntg, (uint64_t)want_fq,
                      (uint64_t)c.resampler, (uint64_t)timing, (uint64_t)rs.resident, (uint64_t)(out && out->ess)})
     gkey = (gkey ^ v) * 1099511628211ull;
   pf_engine::GraphEntry* gent = nullptr;
@@ -1132,10 +1180,10 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       profiling = true;
     }
     const int par = (int)(t & 1);
-    double* lwp = e->lw.p + (size_t)par * n;
+    double* lwp = e->lw.p + (size_t)par * NT;
     wsrc.src = lwp;
     wsrc.M = e->mbuf.p + par;
-    uint32_t* kbase = ntg ? e->keys.p + (size_t)par * 3 * n : nullptr;
+    uint32_t* kbase = ntg ? e->keys.p + (size_t)par * 3 * NT : nullptr;
     QShared* qshp = ntg ? e->qsh.p + par : nullptr;
     // ---- K1
     StepArgs<TQ> a;
@@ -1155,7 +1203,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     a.Mout = e->mbuf.p + par;
     // the resampling words of step t-1: the slots' own (cutpoint), or the
     // ordered uniforms of the spacings pass (K7)
-    a.u3 = e->du3.p + (size_t)((t - 1) % 3) * n;
+    a.u3 = e->du3.p + (size_t)((t - 1) % 3) * NT;
     a.spS = (spacings && t > 1) ? e->spS.p : nullptr;
     if (spacings && t > 1) CK(cudaStreamWaitEvent(st, e->ev_sp, 0));  // scan of step t-1
     a.lk = lk;
@@ -1164,8 +1212,10 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     // the side stream's step t-2 work reads the buffers this step overwrites
     if (ntg && t > 2) CK(cudaStreamWaitEvent(st, e->ev_q[t & 1], 0));
     a.kx = want_fq ? kbase : nullptr;
-    a.ks = want_sq ? kbase + n : nullptr;
-    a.kt = want_tq ? kbase + 2 * (size_t)n : nullptr;
+    a.ks = want_sq ? kbase + NT : nullptr;
+    a.kt = want_tq ? kbase + 2 * (size_t)NT : nullptr;
+    a.rp.out = T;
+    a.rp.qsh_bytes = 2 * (int64_t)sizeof(QShared);
     a.qmom = ntg ? &qshp->mean[0] : nullptr;
     a.partials = e->partials.p;
     a.sc = e->sc.p;
@@ -1194,14 +1244,14 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     a.dr.gs = gamma_src(e, true, t);
     a.dr.gt = gamma_src(e, false, t);
     a.dr.ntab = e->ntab;
-    a.dr.u3 = e->du3.p + (size_t)(t % 3) * n;
+    a.dr.u3 = e->du3.p + (size_t)(t % 3) * NT;
     a.dr.fail = e->fail.p;
     a.dr.seedp = e->seed_dev.p;  // read on the device (a captured loop serves any seed)
     a.z = fz ? row(fz, t) : nullptr;
     a.g_s = fgs ? row(fgs, t) : nullptr;
     a.g_t = fgt ? row(fgt, t) : nullptr;
     if (!fused) {  // draws_kernel output of step t
-      const size_t off = (size_t)(t % 3) * n;
+      const size_t off = (size_t)(t % 3) * NT;
       if (!a.z) a.z = e->dz.p + off;
       if (!a.g_s) a.g_s = e->dgs.p + off;
       if (!a.g_t) a.g_t = e->dgt.p + off;
@@ -1215,13 +1265,13 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       // timed after every launch of the graph
       const unsigned rf = capture.active ? cudaEventRecordExternal : cudaEventRecordDefault;
       CK(cudaEventRecordWithFlags(b0, st, rf));
-      if (fused) CK(launch_pdl(PDL_STEP, step_kernel<MODE, TQ, true>, dim3(step_grid), dim3(STEP_THREADS), step_smem, st, a));
-      else CK(launch_pdl(PDL_STEP, step_kernel<MODE, TQ, false>, dim3(step_grid), dim3(STEP_THREADS), step_smem, st, a));
+      if (fused) CK(launch_pdl(PDL_STEP, step_kernel<MODE, TQ, true>, dim3(step_grid, 1, R), dim3(STEP_THREADS), step_smem, st, a));
+      else CK(launch_pdl(PDL_STEP, step_kernel<MODE, TQ, false>, dim3(step_grid, 1, R), dim3(STEP_THREADS), step_smem, st, a));
       CK(cudaEventRecordWithFlags(b1, st, rf));
       step_evs.push_back({b0, b1});
     } else {
-      if (fused) CK(launch_pdl(PDL_STEP, step_kernel<MODE, TQ, true>, dim3(step_grid), dim3(STEP_THREADS), step_smem, st, a));
-      else CK(launch_pdl(PDL_STEP, step_kernel<MODE, TQ, false>, dim3(step_grid), dim3(STEP_THREADS), step_smem, st, a));
+      if (fused) CK(launch_pdl(PDL_STEP, step_kernel<MODE, TQ, true>, dim3(step_grid, 1, R), dim3(STEP_THREADS), step_smem, st, a));
+      else CK(launch_pdl(PDL_STEP, step_kernel<MODE, TQ, false>, dim3(step_grid, 1, R), dim3(STEP_THREADS), step_smem, st, a));
     }
     LAUNCHED();
     ++step_launches;
@@ -1262,8 +1312,8 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     if (ntg) {
       qa.sh = qshp;
       qa.keys[0] = want_fq ? kbase : nullptr;
-      qa.keys[1] = want_sq ? kbase + n : nullptr;
-      qa.keys[2] = want_tq ? kbase + 2 * (size_t)n : nullptr;
+      qa.keys[1] = want_sq ? kbase + NT : nullptr;
+      qa.keys[2] = want_tq ? kbase + 2 * (size_t)NT : nullptr;
       CK(cudaEventRecord(e->ev_b, st));  // K1b(t): keys, log-weights, M, moments
       cudaStream_t ss = e->side;
       CK(cudaStreamWaitEvent(ss, e->ev_b, 0));
@@ -1273,12 +1323,12 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       } else {
         const int qm = (want_fq ? 1 : 0) | (want_sq ? 2 : 0) | (want_tq ? 4 : 0);
         if ((rc = launch_reduce_qr<TQ>(qm, 0, wsrc, (int)plan.tiles, nullptr, nullptr, e->fail.p, qa,
-                                       ss)) != PF_OK)
+                                       ss, (int)R)) != PF_OK)
           return rc;
       }
     }
     if (uses_cut_tables(c.resampler)) {
-      if ((rc = launch_cdf<TQ>(e->cdf, wsrc, n, qv, e->cut.p, e->fail.p, t, st, so)) != PF_OK) return rc;
+      if ((rc = launch_cdf<TQ>(e->cdf, wsrc, n, qv, e->cut.p, e->fail.p, t, st, so, (int)R)) != PF_OK) return rc;
       if (spacings && sp_inline) {
         const uint64_t* w = e->du3.p + (size_t)(t % 3) * n;
         auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0), ExpOfWord{w});
@@ -1359,14 +1409,14 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
         const char* v = getenv("PF_FUSED_RESOLVE_LOG2N");
         return v ? atoi(v) : 22;
       }();
-      const bool fused_resolve = ilog2(n) <= fused_log2n;
+      const bool fused_resolve = R > 1 || ilog2(n) <= fused_log2n;  // (batched: rounds only)
       const int hgrid = std::max(1, std::min(64, (int)((n / 64 + 255) / 256)));
       for (int round = 0; round < 2; ++round) {
         if (fused_resolve) {
           // histogram, locate, filter, exact finish; round 0 adds the fallback
           // interval of a target whose window missed, round 1 the exact select
           // of a target still unresolved
-          q_round_kernel<<<ntg, 1024, Q_RESOLVE_SMEM, ss>>>(qa, vs, e->qscratch.p, ox, os, ot, t, e->fail.p, round,
+          q_round_kernel<<<dim3(ntg, 1, R), 1024, Q_RESOLVE_SMEM, ss>>>(qa, vs, e->qscratch.p, ox, os, ot, t, e->fail.p, round,
                                                             e->qunres.p, all);
           g_launches.fetch_add(1);
         } else {
@@ -1382,12 +1432,12 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
           for (int attempt = 0; attempt < 2; ++attempt) {
             if (!fused_resolve) q_fallback_prep_kernel<<<1, 32, 0, ss>>>(qa, attempt, e->fail.p);
             if ((rc = fb_hist_smem()) != PF_OK) return rc;
-            q_fallback_hist_kernel<<<fb_hist_grid(n), 256, QFB_SMEM_BYTES, ss>>>(qa, lwp, wsrc.mode, wsrc.M, n,
+            q_fallback_hist_kernel<<<dim3(fb_hist_grid(n, (int)R), 1, R), 256, QFB_SMEM_BYTES, ss>>>(qa, lwp, wsrc.mode, wsrc.M, n,
                                                                                  SINGLE, attempt, e->fail.p);
-            q_fallback_select_kernel<<<ntg, 1024, 0, ss>>>(qa, attempt, e->fail.p, fused_resolve && attempt == 0);
+            q_fallback_select_kernel<<<dim3(ntg, 1, R), 1024, 0, ss>>>(qa, attempt, e->fail.p, fused_resolve && attempt == 0);
             g_launches.fetch_add(fused_resolve ? 2 : 3);
           }
-          q_fallback_fill_kernel<<<fb_grid, 256, 0, ss>>>(qa, lwp, wsrc.mode, wsrc.M, n, SINGLE, e->fail.p);
+          q_fallback_fill_kernel<<<dim3(std::max(1, fb_grid / (int)R), 1, R), 256, 0, ss>>>(qa, lwp, wsrc.mode, wsrc.M, n, SINGLE, e->fail.p);
           g_launches.fetch_add(1);
         }
       }
@@ -1395,7 +1445,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
         q_select_kernel<<<ntg, 1024, 0, ss>>>(qa, vs, e->qscratch.p, ox, os, ot, t, e->fail.p, e->qunres.p, all);
         g_launches.fetch_add(1);
       }
-      q_step_end_kernel<<<1, 1024, 0, ss>>>(qa, 1);
+      q_step_end_kernel<<<dim3(1, 1, R), 1024, 0, ss>>>(qa, 1);
       g_launches.fetch_add(1);
       CK(cudaEventRecord(e->ev_q[t & 1], ss));
     }
@@ -1574,26 +1624,31 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       if (h) CK(cudaMemcpyAsync(h, d.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
       return PF_OK;
     };
-    if ((rc = cp(out->filtered_mean, e->o_fm, T)) != PF_OK) return rc;
-    if (want_ess && (rc = cp(out->ess, e->o_ess, T)) != PF_OK) return rc;
-    if (want_fq && (rc = cp(out->filtered_quantiles, e->o_fq, T * 3)) != PF_OK) return rc;
+    const size_t TR = (size_t)T * R;  // [R][T] rows
+    if ((rc = cp(out->filtered_mean, e->o_fm, TR)) != PF_OK) return rc;
+    if (want_ess && (rc = cp(out->ess, e->o_ess, TR)) != PF_OK) return rc;
+    if (want_fq && (rc = cp(out->filtered_quantiles, e->o_fq, TR * 3)) != PF_OK) return rc;
     if (LS) {
-      if ((rc = cp(out->sigma2_mean, e->o_sm, T)) || (rc = cp(out->sigma2_sd, e->o_ssd, T)) ||
-          (rc = cp(out->sigma2_quantiles, e->o_sq, T * 5)))
+      if ((rc = cp(out->sigma2_mean, e->o_sm, TR)) || (rc = cp(out->sigma2_sd, e->o_ssd, TR)) ||
+          (rc = cp(out->sigma2_quantiles, e->o_sq, TR * 5)))
         return rc;
     }
     if (LT) {
-      if ((rc = cp(out->tau2_mean, e->o_tm, T)) || (rc = cp(out->tau2_sd, e->o_tsd, T)) ||
-          (rc = cp(out->tau2_quantiles, e->o_tq, T * 5)))
+      if ((rc = cp(out->tau2_mean, e->o_tm, TR)) || (rc = cp(out->tau2_sd, e->o_tsd, TR)) ||
+          (rc = cp(out->tau2_quantiles, e->o_tq, TR * 5)))
         return rc;
     }
   }
   mark(PH_OTHER);
-  int64_t fail_h = 0;
-  CK(cudaMemcpyAsync(&fail_h, e->fail.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  std::vector<int64_t> fails((size_t)R, 0);
+  CK(cudaMemcpyAsync(fails.data(), e->fail.p, R * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CK(cudaEventRecord(e->ev1, st));
   CK(cudaStreamSynchronize(st));
   CK(cudaGetLastError());
+  // status: the first failing replication (batched) or the run's own
+  int64_t fail_h = 0, fail_r = 0;
+  for (int64_t r = 0; r < R && !fail_h; ++r)
+    if (fails[(size_t)r]) { fail_h = fails[(size_t)r]; fail_r = r; }
   for (int k = 0; k < 4; ++k) e->qstats[k] = 0;
   if (ntg) {
     unsigned int h[4];
@@ -1684,7 +1739,9 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   }
   if (fail_h > 0)
     return set_err(PF_ERR_ALL_WEIGHTS_ZERO, "all particle weights are zero (at time step " +
-                                             std::to_string(fail_h) + ")", fail_h);
+                                             std::to_string(fail_h) + ")" +
+                                             (R > 1 ? " in replication " + std::to_string(fail_r) : std::string()),
+                   fail_h);
   if (fail_h < 0) return set_err(PF_ERR_ALL_WEIGHTS_ZERO, "all particle weights are zero", 0);
   if (e->qstats[0] > 0) return quantile_unresolved_error(e->qstats[0]);
   return PF_OK;
@@ -1893,6 +1950,38 @@ int pf_engine_run(pf_engine* e, const double* y, int64_t t_len, const pf_feed* f
   e->y_host.assign(y, y + t_len);
   RunSpec rs{y, t_len, feed, out, false};
   return pick_run(e->mode)(e, rs);
+}
+
+int pf_engine_run_batch(pf_engine* e, const uint64_t* seeds, int32_t reps, const double* y, int64_t t_len,
+                        pf_outputs* out) {
+  if (!e || !seeds || !out) return set_err(PF_ERR_VALUE, "null argument");
+  if (reps < 1) return set_err(PF_ERR_VALUE, "reps must be >= 1");
+  if (t_len < 0) return set_err(PF_ERR_VALUE, "negative series length");
+  for (int64_t i = 0; i < t_len; ++i)
+    if (!std::isfinite(y[i])) return set_err(PF_ERR_NON_FINITE_WEIGHT, "observations contain NaN or infinity");
+  if (out->indices || out->hist_states || out->hist_sigma2 || out->hist_tau2 || out->hist_a_sigma ||
+      out->hist_b_sigma || out->hist_a_tau || out->hist_b_tau || out->final_states || out->final_sigma2 ||
+      out->final_tau2 || out->final_a_sigma || out->final_b_sigma || out->final_a_tau || out->final_b_tau)
+    return set_err(PF_ERR_NOT_IMPLEMENTED, "batched replications return the per-step summaries only");
+  const pf_config& c = e->cfg;
+  if (reps > 1) {
+    if (c.resampler != PF_RESAMPLE_CUTPOINT || e->strata || c.gamma_method != 0 || cdf_plan(e->n).small ||
+        !fuse_top() || c.phase_timing)
+      return set_err(PF_ERR_NOT_IMPLEMENTED,
+                     "batched replications need cut-point resampling, table draws, fused top tree, no phase "
+                     "timing and " + std::to_string(CDF_TILE) + " <= n < 2^" + std::to_string(STRATA_MIN_LOG2N));
+    if ((int64_t)reps > 65535) return set_err(PF_ERR_VALUE, "at most 65535 replications per batch");
+  }
+  CK(cudaSetDevice(c.device));
+  e->y_host.assign(y, y + t_len);
+  const uint64_t seed0 = e->cfg.seed;
+  e->cfg.seed = seeds[0];
+  RunSpec rs{y, t_len, nullptr, out, false};
+  rs.reps = reps;
+  rs.seeds = seeds;
+  const int rc = pick_run(e->mode)(e, rs);
+  e->cfg.seed = seed0;
+  return rc;
 }
 
 int pf_engine_run_resident(pf_engine* e, int64_t t_len) {

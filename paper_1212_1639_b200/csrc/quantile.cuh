@@ -112,7 +112,29 @@ struct QArgs {
   // pbase + block of ptotal (0: this launch alone), particle index offset
   int pbase, ptotal;
   uint32_t gbase;
+  // batched replications (gridDim.z = R, step.cuh RepStride): per-replication
+  // strides of the slot arrays, the partial slots and the [T] output rows
+  int64_t rslots, rpart, rT;
 };
+
+// Replication blockIdx.z's quantile state: targets [R][Q_MAXT], shared pair
+// [R][2] (by parity), candidates [R][ntarget cap], partials, histograms and
+// lists [R][...]; the stats counters are shared (atomic).
+PF_D void q_rep(QArgs& qa) {
+  const int64_t r = blockIdx.z;
+  if (r == 0) return;
+  qa.tg += r * Q_MAXT;
+  qa.sh += 2 * r;
+#pragma unroll
+  for (int q = 0; q < Q_MAXQ; ++q)
+    if (qa.keys[q]) qa.keys[q] += r * qa.rslots;
+  qa.cand += r * (int64_t)qa.ntarget * qa.cap;
+  qa.part += r * qa.rpart;
+  qa.hist += r * (int64_t)Q_MAXT * Q_SUB;
+  qa.fhist += r * (int64_t)Q_MAXT * Q_FB;
+  qa.lidx += r * (int64_t)Q_MAXT * Q_LIST;
+  qa.lw += r * (int64_t)Q_MAXT * Q_LIST;
+}
 
 PF_D int q_pslot(const QArgs& qa) { return qa.pbase + (int)blockIdx.x; }
 PF_D unsigned q_ptotal(const QArgs& qa) { return qa.ptotal ? (unsigned)qa.ptotal : gridDim.x; }
@@ -493,6 +515,11 @@ __global__ void __launch_bounds__(THR, 65536 / (64 * THR))
 cdf_reduce_qr_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ chunk_tot,
                      const int64_t* __restrict__ fail, QArgs qa) {
   static_assert(!TREE || THR == CDF_THREADS, "the fused tree pass uses K2's tiles");
+  if (gridDim.z > 1) {
+    q_rep(qa);
+    src = wsrc_rep(src, qa.rslots);
+    if (fail) fail += blockIdx.z;
+  }
   if (fail && *fail) return;
   constexpr int NR = 2 * Q_PER + 1;
   __shared__ T wt[CDF_THREADS / 32];
@@ -982,6 +1009,12 @@ constexpr int QFB_SMEM_BYTES = QFB_SMEM_T * Q_FB * 8;
 __global__ void __launch_bounds__(256)
 q_fallback_hist_kernel(QArgs qa, const double* __restrict__ lw, int wmode, const double* Mp, int64_t n,
                        int single, int attempt, const int64_t* fail) {
+  if (gridDim.z > 1) {
+    q_rep(qa);
+    lw += blockIdx.z * n;
+    Mp += 2 * blockIdx.z;
+    fail += blockIdx.z;
+  }
   if (*fail || !qa.sh->fb_active[attempt]) return;
   __shared__ uint32_t ilo[Q_MAXT], ihi[Q_MAXT];
   __shared__ int act[Q_MAXT], tq[Q_MAXT], slot[Q_MAXT];
@@ -1095,6 +1128,10 @@ q_fallback_hist_kernel(QArgs qa, const double* __restrict__ lw, int wmode, const
 // bounded guess fell short) the target is marked for attempt 1.
 __global__ void __launch_bounds__(1024) q_fallback_select_kernel(QArgs qa, int attempt, const int64_t* fail,
                                                                   int fuse_prep = 0) {
+  if (gridDim.z > 1) {
+    q_rep(qa);
+    fail += blockIdx.z;
+  }
   if (*fail || !qa.sh->fb_active[attempt]) return;
   const int k = blockIdx.x;
   QTarget& t = qa.tg[k];
@@ -1145,6 +1182,12 @@ __global__ void __launch_bounds__(1024) q_fallback_select_kernel(QArgs qa, int a
 __global__ void __launch_bounds__(256) q_fallback_fill_kernel(QArgs qa, const double* __restrict__ lw, int wmode,
                                                               const double* Mp, int64_t n, int single,
                                                               const int64_t* fail) {
+  if (gridDim.z > 1) {
+    q_rep(qa);
+    lw += blockIdx.z * n;
+    Mp += 2 * blockIdx.z;
+    fail += blockIdx.z;
+  }
   if (*fail || !qa.sh->fb_active[0]) return;
   __shared__ int act[Q_MAXT], tq[Q_MAXT];
   __shared__ uint32_t klo[Q_MAXT], khi[Q_MAXT];
@@ -1303,6 +1346,21 @@ q_select_kernel(QArgs qa, QValueSrc vs, double* __restrict__ scratch, double* ou
 __global__ void __launch_bounds__(1024)
 q_round_kernel(QArgs qa, QValueSrc vs, double* __restrict__ scratch, double* out_x, double* out_s, double* out_t,
                int64_t t_step, const int64_t* fail, int round, unsigned int* unresolved, QAll all) {
+  if (gridDim.z > 1) {
+    const int64_t r = blockIdx.z;
+    q_rep(qa);
+    vs.rec += r * qa.rslots;
+    if (vs.seedp) vs.seedp += r;
+    scratch += r * (int64_t)qa.ntarget * qa.cap;
+    if (out_x) out_x += r * qa.rT * 3;
+    if (out_s) out_s += r * qa.rT * 5;
+    if (out_t) out_t += r * qa.rT * 5;
+    fail += r;
+    for (int q = 0; q < Q_MAXQ; ++q)
+      if (all.keys[0][q]) all.keys[0][q] += r * qa.rslots;
+    all.lw[0] += r * qa.rslots;
+    if (all.M[0]) all.M[0] += 2 * r;
+  }
   if (*fail) return;
   const int k = blockIdx.x;
   if (round && qa.tg[k].status == QS_OK) return;  // resolved in round 0 (uniform over the CTA)
@@ -1324,6 +1382,7 @@ q_round_kernel(QArgs qa, QValueSrc vs, double* __restrict__ scratch, double* out
 // End of step: widen windows that missed, clear the per-step histograms
 // and counters for the next step.
 __global__ void __launch_bounds__(1024) q_step_end_kernel(QArgs qa, int had_miss_possible) {
+  if (gridDim.z > 1) q_rep(qa);
   for (int i = threadIdx.x; i < qa.ntarget * Q_SUB; i += blockDim.x) qa.hist[i] = 0ull;
   __syncthreads();
   const int k = threadIdx.x;

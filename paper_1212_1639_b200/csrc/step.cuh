@@ -142,14 +142,19 @@ struct InitArgs {
   Rec* rec;
   double* s2_init;          // optional: sigma2 draws (T == 0 keep_final)
   int64_t gbase;            // global index of this shard's first slot
+  const uint64_t* seedp;    // batched replications: seedp[r] is replication r's seed
 };
 
 template <int MODE>
 __global__ void __launch_bounds__(256) init_kernel(InitArgs a) {
   constexpr bool LS = MODE & M_LS, LT = MODE & M_LT, SINGLE = MODE & M_SINGLE;
+  // batched replications (gridDim.z = R): replication blockIdx.z's slots
+  const int64_t rz = blockIdx.z;
+  Rec* rec = a.rec + rz * a.n;
+  const uint64_t seed = a.seedp ? a.seedp[rz] : a.seed;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n;
        j += (int64_t)gridDim.x * blockDim.x) {
-    const Philox4 P = philox_block(a.seed, (uint64_t)(a.gbase + j), 0);
+    const Philox4 P = philox_block(seed, (uint64_t)(a.gbase + j), 0);
     const double z = a.feed_z ? a.feed_z[j] : ndtri(unit_open(P.w[0]));
     double x0 = a.x0_mean + a.sqrt_x0_var * z;
     if (SINGLE) x0 = (double)(float)x0;
@@ -161,7 +166,7 @@ __global__ void __launch_bounds__(256) init_kernel(InitArgs a) {
     r.tau2 = t2;
     r.bs = a.bs0;
     r.bt = a.bt0;
-    a.rec[j] = r;
+    rec[j] = r;
     if (a.s2_init) a.s2_init[j] = s2;
   }
 }
@@ -207,6 +212,17 @@ struct DrawArgs {
 
 PF_D uint64_t seed_of(uint64_t seed, const uint64_t* seedp) { return seedp ? *seedp : seed; }
 
+// Batched replications: one launch runs R independent filters of n slots
+// (gridDim.z = R, replication r = blockIdx.z).  Replication r owns slots
+// [r n, (r+1) n) of every per-slot array, row r of the [R][T] outputs and
+// entry r of the per-replication state (seed, scalars, status, max by
+// parity [R][2], moment partials [R][grid.x]).  Offsets are applied once at
+// kernel entry; gridDim.z = 1 is the single run, unchanged.
+struct RepStride {
+  int64_t out;       // output row length (T)
+  int64_t qsh_bytes; // bytes between replications' QShared pairs
+};
+
 template <typename TQ>
 struct StepArgs {
   int64_t n;
@@ -242,6 +258,7 @@ struct StepArgs {
                          // resampling words are formed from them here instead of read from u3
   const double* sp_tot;  // sharded K7: every shard's exponential total of step t-1 (slk.G of them)
   const double* yp;      // non-null: the observation is yp[t-1] (device memory; graph replays)
+  RepStride rp;          // batched replications (gridDim.z > 1)
   int dbg_identity;      // diagnostics only (PF_DEBUG_IDENTITY_ANC): skip the lookup, ancestor = slot
   double ref_slack;      // moment-reference slack (64; 0 = rescale at every new max)
   const Rec* recs[PF_MAX_SHARDS];  // sharded run: every shard's records of step t-1
@@ -432,6 +449,12 @@ PF_D int stage_tables(const GammaSrc& gs, const GammaSrc& gt, const double* ntab
 template <int MODE>
 __global__ void __launch_bounds__(256) draws_kernel(DrawArgs a) {
   constexpr bool LS = MODE & M_LS, LT = MODE & M_LT;
+  {
+    const int64_t r = blockIdx.z, o = r * a.n;
+    a.z += o; a.g_s += o; a.g_t += o; a.u3 += o;
+    a.fail += r;
+    if (a.seedp) a.seedp += r;
+  }
   if (*a.fail) return;
   int slot_s, slot_t, noff = -1;
   stage_tables<LS, LT>(a.gs, a.gt, a.ntab, slot_s, slot_t, noff);
@@ -464,6 +487,17 @@ template <int MODE, typename TQ, bool FD = false>
 __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs<TQ> a) {
   constexpr bool LS = MODE & M_LS, LT = MODE & M_LT, SINGLE = MODE & M_SINGLE;
   constexpr int SB = step_sb<FD>();  // slots per thread per pipeline stage
+  // batched replications (gridDim.z = R): replication blockIdx.z's slice of
+  // every array (locals: the kernel parameters themselves stay read-only)
+  const int64_t rz = blockIdx.z, ro = rz * a.n;
+  // (per-slot arrays are indexed at ro + j below; ro = 0 for a single run)
+  Lookup<TQ> lk_ = a.lk;
+  lk_.q += ro;
+  lk_.cut += ro;
+  Partial* const partials_ = a.partials + rz * gridDim.x;
+  Scalars* const sc_ = a.sc + rz;
+  int64_t* const fail_ = a.fail + rz;
+  const uint64_t* const dseedp_ = a.dr.seedp ? a.dr.seedp + rz : nullptr;
   // the step's tables are constant over the run: stage them while the
   // previous kernel (group build / K4) drains, then wait for its outputs
   int slot_s = -1, slot_t = -1, noff = -1, tab_doubles = 0;
@@ -472,11 +506,11 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
   if (FD) tab_doubles = stage_tables<LS, LT>(a.dr.gs, a.dr.gt, a.dr.ntab, slot_s, slot_t, noff);
   else __syncthreads();
   pdl_wait();
-  if (*a.fail) return;
+  if (*fail_) return;
   const bool feedw = a.feed_w != nullptr;
-  const double cs = a.sc->cs, ct = a.sc->ct, cx = a.sc->cx;
+  const double cs = sc_->cs, ct = sc_->ct, cx = sc_->cx;
   const double yobs = a.yp ? a.yp[a.t - 1] : a.y;
-  const uint64_t dseed = seed_of(a.dr.seed, a.dr.seedp);
+  const uint64_t dseed = seed_of(a.dr.seed, dseedp_);
   // m: reference of this thread's moment sums (moved, with a rescale, only
   // when a log-weight exceeds it by more than ref_slack = 64 -- e <= e^64
   // keeps the fp64 sums far from overflow); mx: the true running max, the
@@ -520,7 +554,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
     } else {
       tot += __ldcg(a.spS + a.n - 1);
     }
-    sp_inv = 1.0 / (tot + spacings_aux_exp(seed_of(a.seed, a.dr.seedp), a.t - 1));
+    sp_inv = 1.0 / (tot + spacings_aux_exp(seed_of(a.seed, dseedp_), a.t - 1));
   }
   // resampling words are loaded one pipeline stage ahead of their lookups
   auto load_w3 = [&](int64_t bi, uint64_t (&w3)[SB]) {
@@ -528,7 +562,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
     for (int b = 0; b < SB; ++b) {
       const int64_t j = bi * batch + b * (int64_t)nth + threadIdx.x;
       const bool live = a.t > 1 && bi < nbatches && j < a.n;
-      w3[b] = !live ? 0ull : a.spS ? spacings_word(sp_off + __ldcs(a.spS + j), sp_inv) : __ldcs(a.u3 + j);
+      w3[b] = !live ? 0ull : a.spS ? spacings_word(sp_off + __ldcs(a.spS + j), sp_inv) : __ldcs(a.u3 + (ro + j));
     }
   };
   auto issue = [&](int64_t bi, int buf, const uint64_t (&w3)[SB]) {
@@ -545,12 +579,12 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
 #pragma unroll
         for (int b = 0; b < SB; ++b)
           if (ok[b]) anc[b] = a.srk.on ? sharded_lookup_rank<TQ>(a.slk, a.srk, w3[b]) : sharded_lookup<TQ>(a.slk, w3[b]);
-      } else if (a.lk.anc) {  // baseline resamplers: ancestors precomputed
+      } else if (lk_.anc) {  // baseline resamplers: ancestors precomputed
 #pragma unroll
         for (int b = 0; b < SB; ++b)
-          if (ok[b]) anc[b] = a.lk.anc[jj[b]];
+          if (ok[b]) anc[b] = lk_.anc[jj[b]];
       } else {
-        ancestors_of<TQ, SB>(a.lk, w3, ok, anc);
+        ancestors_of<TQ, SB>(lk_, w3, ok, anc);
       }
       if (a.idx_out) {
 #pragma unroll
@@ -565,14 +599,14 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
       // ancestors are global indices in a sharded run (identity, local, at t = 1)
       const Rec* rp = (a.slk.G > 0 && a.t > 1)
           ? a.recs[anc[b] >> a.slk.lg] + (anc[b] & (((int64_t)1 << a.slk.lg) - 1))
-          : a.rec_in + anc[b];
+          : a.rec_in + (ro + anc[b]);
       const char* src = reinterpret_cast<const char*>(rp);
       cp_async16(dst, src);
       cp_async16(dst + 16, src + 16);
       // precomputed draws (draws kernel) or the oracle feed
-      if (a.z) cp_async8((uint32_t)__cvta_generic_to_shared(val_at(buf, 0, b)), a.z + jj[b]);
-      if (LS && a.g_s) cp_async8((uint32_t)__cvta_generic_to_shared(val_at(buf, 1, b)), a.g_s + jj[b]);
-      if (LT && a.g_t) cp_async8((uint32_t)__cvta_generic_to_shared(val_at(buf, 2, b)), a.g_t + jj[b]);
+      if (a.z) cp_async8((uint32_t)__cvta_generic_to_shared(val_at(buf, 0, b)), a.z + (ro + jj[b]));
+      if (LS && a.g_s) cp_async8((uint32_t)__cvta_generic_to_shared(val_at(buf, 1, b)), a.g_s + (ro + jj[b]));
+      if (LT && a.g_t) cp_async8((uint32_t)__cvta_generic_to_shared(val_at(buf, 2, b)), a.g_t + (ro + jj[b]));
     }
     asm volatile("cp.async.commit_group;");
   };
@@ -599,7 +633,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
       t2 = o.bt / gtd;
     }
     o.tau2 = t2;
-    a.rec_out[j] = o;
+    a.rec_out[ro + j] = o;
     // ---- log-weight (filtering.py:293)
     double lw;
     if (LS)
@@ -609,9 +643,9 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
     double e;
     if (feedw) {
       e = a.feed_w[j];
-      a.lw[j] = e;
+      a.lw[ro + j] = e;
     } else {
-      a.lw[j] = lw;
+      a.lw[ro + j] = lw;
       if (!(lw == lw) || lw == INFINITY) bad = true;
       if (lw > mx) mx = lw;
       if (lw > m + a.ref_slack) {
@@ -623,9 +657,9 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
         e = lw > -INFINITY ? exp_moment(lw - m, s_exp) : 0.0;
       }
     }
-    if (a.kx) a.kx[j] = key_rd_(xn);
-    if (a.ks) a.ks[j] = key_rd_(s2);
-    if (a.kt) a.kt[j] = key_rd_(t2);
+    if (a.kx) a.kx[ro + j] = key_rd_(xn);
+    if (a.ks) a.ks[ro + j] = key_rd_(s2);
+    if (a.kt) a.kt[ro + j] = key_rd_(t2);
     s0 += e;
     s2w = fma(e, e, s2w);
     sx = fma(e, xn, sx);
@@ -662,7 +696,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
       for (int b = 0; b < SB; ++b) {
         const int64_t j = bi * batch + b * (int64_t)nth + threadIdx.x;
         const Philox4 P = philox_block(dseed, (uint64_t)(a.dr.gbase + j), (uint64_t)a.t);
-        if (j < a.n) a.dr.u3[j] = P.w[3];
+        if (j < a.n) a.dr.u3[ro + j] = P.w[3];
         // tables only (FD runs with gamma_method 0): no call into the
         // accurate solvers, which would cost the kernel a stack frame
         dz[b] = nt_eval_slot(noff, unit_open(P.w[0]));
@@ -722,9 +756,9 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
     p.s2t = acc[6];
     p.s2w = acc[7];
     p.bad = acc[8];
-    a.partials[blockIdx.x] = p;
+    partials_[blockIdx.x] = p;
     __threadfence();
-    const unsigned int ticket = atomicAdd(&a.sc->counter, 1u);
+    const unsigned int ticket = atomicAdd(&sc_->counter, 1u);
     last = (ticket == gridDim.x - 1);
   }
   __syncthreads();
@@ -733,7 +767,7 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
   // ---- last CTA: combine the partials (fixed order -> deterministic)
   __threadfence();
   double M, bsum, S[8];
-  reduce_partials(a.partials, (int)gridDim.x, red, M, bsum, S);
+  reduce_partials(partials_, (int)gridDim.x, red, M, bsum, S);
   if (threadIdx.x != 0) return;
   if (a.xrec) {
     // sharded run: this shard's partial goes to the exchange array; the
@@ -746,10 +780,20 @@ __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs
     p.se = 0.0;
     a.xrec[a.shard] = p;
     __threadfence_system();
-    a.sc->counter = 0;
+    sc_->counter = 0;
     return;
   }
-  finalize_step<LS, LT>(a.t, M, bsum, S, feedw, cs, ct, cx, a.out, a.qmom, a.sc, a.Mout, a.fail);
+  StepOut o = a.out;
+  double* qmom = a.qmom;
+  if (rz) {
+    const int64_t ro_ = rz * a.rp.out;
+    o.fmean += ro_;
+    if (o.s_mean) { o.s_mean += ro_; o.s_sd += ro_; }
+    if (o.t_mean) { o.t_mean += ro_; o.t_sd += ro_; }
+    if (o.ess) o.ess += ro_;
+    if (qmom) qmom = reinterpret_cast<double*>(reinterpret_cast<char*>(qmom) + rz * a.rp.qsh_bytes);
+  }
+  finalize_step<LS, LT>(a.t, M, bsum, S, feedw, cs, ct, cx, o, qmom, sc_, a.Mout + 2 * rz, fail_);
 }
 
 // Sharded run: every shard finalises step t from the G shard partials (the

@@ -71,6 +71,15 @@ class Engine:
                                     None if fd is None else C.byref(fd), C.byref(outputs))
         _lib.check(rc, self.lib)
 
+    def run_batch(self, seeds, y, outputs):
+        """``len(seeds)`` independent replications in one launch sequence
+        (pf_engine_run_batch); outputs hold [R][T] rows."""
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        sd = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+        rc = self.lib.pf_engine_run_batch(self.h, _lib.ptr(sd, C.c_uint64), len(sd), _lib.ptr(y), len(y),
+                                          C.byref(outputs))
+        _lib.check(rc, self.lib)
+
     def run_resident(self, t_len):
         _lib.check(self.lib.pf_engine_run_resident(self.h, int(t_len)), self.lib)
 

@@ -10,7 +10,7 @@ seeds ``seeds[rank::world]`` ("replicas only", SURVEY §8e)."""
 from __future__ import annotations
 
 from .backend import Backend
-from .filtering import run_particle_filter, run_particle_learning
+from .filtering import run_batch, run_particle_filter, run_particle_learning
 from .models import Priors
 
 
@@ -19,9 +19,16 @@ def rank_seeds(seeds, rank, world):
     return list(seeds)[rank::world]
 
 
-def run_replications(spec, y, n, seeds, backend=None, concurrency=1, **kwargs):
+def run_replications(spec, y, n, seeds, backend=None, concurrency=1, batch=1, **kwargs):
     """Run one filter per seed and return the list of FilterOutput (in seed
     order).
+
+    ``batch`` > 1 runs that many replications per kernel launch sequence
+    (filtering.run_batch / pf_engine_run_batch: R filters side by side in
+    every launch, one tree per replication) -- the way to fill the B200 at
+    N ~ 2^20, where one filter's per-step kernels are latency-bound.  Batched
+    runs return the per-step summaries (``precision`` and
+    ``track_quantiles`` are the only other keywords).
 
     ``spec`` is a ``Priors`` (particle learning) or a ``TrendNoiseModel``
     (known parameters); the remaining keywords are those of
@@ -33,6 +40,21 @@ def run_replications(spec, y, n, seeds, backend=None, concurrency=1, **kwargs):
     one at a time."""
     fn = run_particle_learning if isinstance(spec, Priors) else run_particle_filter
     seeds = [int(s) for s in seeds]
+    if batch > 1:
+        extra = set(kwargs) - {"precision", "track_quantiles"}
+        if extra:
+            raise NotImplementedError(f"batched replications do not support {sorted(extra)}")
+        own = backend is None
+        if own:
+            backend = Backend()
+        try:
+            out = []
+            for lo in range(0, len(seeds), batch):
+                out.extend(run_batch(spec, y, n, seeds[lo:lo + batch], backend=backend, **kwargs))
+            return out
+        finally:
+            if own:
+                backend.close()
     if concurrency <= 1 or len(seeds) <= 1:
         own = backend is None
         if own:
