@@ -380,7 +380,8 @@ struct StrataOut {
 int fb_hist_smem() {
   static DevOnce attr;
   if (attr.pending()) {
-    CK(cudaFuncSetAttribute(q_fallback_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, QFB_SMEM_BYTES));
+    CK(cudaFuncSetAttribute(q_fallback_hist_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, QFB_SMEM_BYTES));
+    CK(cudaFuncSetAttribute(q_fallback_hist_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, QFB_SMEM_BYTES));
     attr.mark();
   }
   return PF_OK;
@@ -392,7 +393,7 @@ int fb_hist_grid(int64_t n, int reps = 1) {
   static int occ = 0;
   if (!occ) {
     if (fb_hist_smem() != PF_OK) return 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, q_fallback_hist_kernel, 256, QFB_SMEM_BYTES);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, q_fallback_hist_kernel<0>, 256, QFB_SMEM_BYTES);
     if (occ < 1) occ = 1;
   }
   return grid_for(n, 256, std::max(1, sm_count() * occ / reps));
@@ -1045,6 +1046,11 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
                                     2 * FD_SB * FD_THREADS * (sizeof(Rec) + 3 * sizeof(double)))));
       CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(2 * STEP_SB * 256 * (sizeof(Rec) + 3 * sizeof(double)))));
+      CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)((2 * GT_TABLE_DOUBLES + NT_TABLE_DOUBLES + 4) * sizeof(double) +
+                                    2 * FD_SB * FD_THREADS * (sizeof(Rec) + 3 * sizeof(double)))));
+      CK(cudaFuncSetAttribute(step_kernel<MODE, TQ, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(2 * STEP_SB * 256 * (sizeof(Rec) + 3 * sizeof(double)))));
       attr.mark();
     }
   }
@@ -1257,6 +1263,14 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       if (!a.g_t) a.g_t = e->dgt.p + off;
       if (t > 1) CK(cudaStreamWaitEvent(st, e->ev_draw, 0));
     }
+    auto launch_step = [&](const StepArgs<TQ>& sa) -> cudaError_t {
+      const dim3 g(step_grid, 1, R), b(STEP_THREADS);
+      if (R > 1)
+        return fused ? launch_pdl(PDL_STEP, step_kernel<MODE, TQ, true, true>, g, b, step_smem, st, sa)
+                     : launch_pdl(PDL_STEP, step_kernel<MODE, TQ, false, true>, g, b, step_smem, st, sa);
+      return fused ? launch_pdl(PDL_STEP, step_kernel<MODE, TQ, true>, g, b, step_smem, st, sa)
+                   : launch_pdl(PDL_STEP, step_kernel<MODE, TQ, false>, g, b, step_smem, st, sa);
+    };
     if (rs.resident) {
       cudaEvent_t b0, b1;
       cudaEventCreate(&b0);
@@ -1265,13 +1279,11 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       // timed after every launch of the graph
       const unsigned rf = capture.active ? cudaEventRecordExternal : cudaEventRecordDefault;
       CK(cudaEventRecordWithFlags(b0, st, rf));
-      if (fused) CK(launch_pdl(PDL_STEP, step_kernel<MODE, TQ, true>, dim3(step_grid, 1, R), dim3(STEP_THREADS), step_smem, st, a));
-      else CK(launch_pdl(PDL_STEP, step_kernel<MODE, TQ, false>, dim3(step_grid, 1, R), dim3(STEP_THREADS), step_smem, st, a));
+      CK(launch_step(a));
       CK(cudaEventRecordWithFlags(b1, st, rf));
       step_evs.push_back({b0, b1});
     } else {
-      if (fused) CK(launch_pdl(PDL_STEP, step_kernel<MODE, TQ, true>, dim3(step_grid, 1, R), dim3(STEP_THREADS), step_smem, st, a));
-      else CK(launch_pdl(PDL_STEP, step_kernel<MODE, TQ, false>, dim3(step_grid, 1, R), dim3(STEP_THREADS), step_smem, st, a));
+      CK(launch_step(a));
     }
     LAUNCHED();
     ++step_launches;
@@ -1388,7 +1400,8 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       if (resolve_attr.pending()) {
         CK(cudaFuncSetAttribute(q_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 Q_RESOLVE_SMEM));
-        CK(cudaFuncSetAttribute(q_round_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Q_RESOLVE_SMEM));
+        CK(cudaFuncSetAttribute(q_round_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q_RESOLVE_SMEM));
+        CK(cudaFuncSetAttribute(q_round_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q_RESOLVE_SMEM));
         resolve_attr.mark();
       }
       QAll all;
@@ -1416,7 +1429,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
           // histogram, locate, filter, exact finish; round 0 adds the fallback
           // interval of a target whose window missed, round 1 the exact select
           // of a target still unresolved
-          q_round_kernel<<<dim3(ntg, 1, R), 1024, Q_RESOLVE_SMEM, ss>>>(qa, vs, e->qscratch.p, ox, os, ot, t, e->fail.p, round,
+          (R > 1 ? q_round_kernel<1> : q_round_kernel<0>)<<<dim3(ntg, 1, R), 1024, Q_RESOLVE_SMEM, ss>>>(qa, vs, e->qscratch.p, ox, os, ot, t, e->fail.p, round,
                                                             e->qunres.p, all);
           g_launches.fetch_add(1);
         } else {
@@ -1432,12 +1445,14 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
           for (int attempt = 0; attempt < 2; ++attempt) {
             if (!fused_resolve) q_fallback_prep_kernel<<<1, 32, 0, ss>>>(qa, attempt, e->fail.p);
             if ((rc = fb_hist_smem()) != PF_OK) return rc;
-            q_fallback_hist_kernel<<<dim3(fb_hist_grid(n, (int)R), 1, R), 256, QFB_SMEM_BYTES, ss>>>(qa, lwp, wsrc.mode, wsrc.M, n,
+            (R > 1 ? q_fallback_hist_kernel<1> : q_fallback_hist_kernel<0>)<<<dim3(fb_hist_grid(n, (int)R), 1, R), 256,
+                                                                                QFB_SMEM_BYTES, ss>>>(qa, lwp, wsrc.mode, wsrc.M, n,
                                                                                  SINGLE, attempt, e->fail.p);
-            q_fallback_select_kernel<<<dim3(ntg, 1, R), 1024, 0, ss>>>(qa, attempt, e->fail.p, fused_resolve && attempt == 0);
+            (R > 1 ? q_fallback_select_kernel<1> : q_fallback_select_kernel<0>)<<<dim3(ntg, 1, R), 1024, 0, ss>>>(qa, attempt, e->fail.p, fused_resolve && attempt == 0);
             g_launches.fetch_add(fused_resolve ? 2 : 3);
           }
-          q_fallback_fill_kernel<<<dim3(std::max(1, fb_grid / (int)R), 1, R), 256, 0, ss>>>(qa, lwp, wsrc.mode, wsrc.M, n, SINGLE, e->fail.p);
+          (R > 1 ? q_fallback_fill_kernel<1> : q_fallback_fill_kernel<0>)<<<dim3(std::max(1, fb_grid / (int)R), 1, R),
+                                                                       256, 0, ss>>>(qa, lwp, wsrc.mode, wsrc.M, n, SINGLE, e->fail.p);
           g_launches.fetch_add(1);
         }
       }
@@ -1445,7 +1460,7 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
         q_select_kernel<<<ntg, 1024, 0, ss>>>(qa, vs, e->qscratch.p, ox, os, ot, t, e->fail.p, e->qunres.p, all);
         g_launches.fetch_add(1);
       }
-      q_step_end_kernel<<<dim3(1, 1, R), 1024, 0, ss>>>(qa, 1);
+      (R > 1 ? q_step_end_kernel<1> : q_step_end_kernel<0>)<<<dim3(1, 1, R), 1024, 0, ss>>>(qa, 1);
       g_launches.fetch_add(1);
       CK(cudaEventRecord(e->ev_q[t & 1], ss));
     }

@@ -1006,10 +1006,13 @@ __global__ void q_fallback_prep_kernel(QArgs qa, int attempt, const int64_t* fai
 // 64-bit sum.  Integer sums: the same bins in any order.
 constexpr int QFB_SMEM_T = 2;
 constexpr int QFB_SMEM_BYTES = QFB_SMEM_T * Q_FB * 8;
+// BATCH: launched with gridDim.z = R replications (the offsets modify the
+// parameters, which costs the single-run instantiation a local copy).
+template <int BATCH = 0>
 __global__ void __launch_bounds__(256)
 q_fallback_hist_kernel(QArgs qa, const double* __restrict__ lw, int wmode, const double* Mp, int64_t n,
                        int single, int attempt, const int64_t* fail) {
-  if (gridDim.z > 1) {
+  if (BATCH) {
     q_rep(qa);
     lw += blockIdx.z * n;
     Mp += 2 * blockIdx.z;
@@ -1126,9 +1129,10 @@ q_fallback_hist_kernel(QArgs qa, const double* __restrict__ lw, int wmode, const
 // F2: pick the fallback bin holding the crossing; it becomes the new window
 // (one CTA per target).  If the interval does not hold it (attempt 0's
 // bounded guess fell short) the target is marked for attempt 1.
+template <int BATCH = 0>
 __global__ void __launch_bounds__(1024) q_fallback_select_kernel(QArgs qa, int attempt, const int64_t* fail,
                                                                   int fuse_prep = 0) {
-  if (gridDim.z > 1) {
+  if (BATCH) {
     q_rep(qa);
     fail += blockIdx.z;
   }
@@ -1179,10 +1183,11 @@ __global__ void __launch_bounds__(1024) q_fallback_select_kernel(QArgs qa, int a
 }
 
 // F3: append the candidates of the re-windowed targets.
+template <int BATCH = 0>
 __global__ void __launch_bounds__(256) q_fallback_fill_kernel(QArgs qa, const double* __restrict__ lw, int wmode,
                                                               const double* Mp, int64_t n, int single,
                                                               const int64_t* fail) {
-  if (gridDim.z > 1) {
+  if (BATCH) {
     q_rep(qa);
     lw += blockIdx.z * n;
     Mp += 2 * blockIdx.z;
@@ -1343,10 +1348,11 @@ q_select_kernel(QArgs qa, QValueSrc vs, double* __restrict__ scratch, double* ou
 // (re-windowed targets only) ends with the weighted radix select (S) for a
 // target that is still unresolved.  A target is owned by one CTA from start
 // to end, so the CTA barrier is the only ordering needed.
+template <int BATCH = 0>
 __global__ void __launch_bounds__(1024)
 q_round_kernel(QArgs qa, QValueSrc vs, double* __restrict__ scratch, double* out_x, double* out_s, double* out_t,
                int64_t t_step, const int64_t* fail, int round, unsigned int* unresolved, QAll all) {
-  if (gridDim.z > 1) {
+  if (BATCH) {
     const int64_t r = blockIdx.z;
     q_rep(qa);
     vs.rec += r * qa.rslots;
@@ -1381,8 +1387,9 @@ q_round_kernel(QArgs qa, QValueSrc vs, double* __restrict__ scratch, double* out
 
 // End of step: widen windows that missed, clear the per-step histograms
 // and counters for the next step.
+template <int BATCH = 0>
 __global__ void __launch_bounds__(1024) q_step_end_kernel(QArgs qa, int had_miss_possible) {
-  if (gridDim.z > 1) q_rep(qa);
+  if (BATCH) q_rep(qa);
   for (int i = threadIdx.x; i < qa.ntarget * Q_SUB; i += blockDim.x) qa.hist[i] = 0ull;
   __syncthreads();
   const int k = threadIdx.x;

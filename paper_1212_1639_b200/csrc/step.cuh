@@ -258,10 +258,10 @@ struct StepArgs {
                          // resampling words are formed from them here instead of read from u3
   const double* sp_tot;  // sharded K7: every shard's exponential total of step t-1 (slk.G of them)
   const double* yp;      // non-null: the observation is yp[t-1] (device memory; graph replays)
-  RepStride rp;          // batched replications (gridDim.z > 1)
   int dbg_identity;      // diagnostics only (PF_DEBUG_IDENTITY_ANC): skip the lookup, ancestor = slot
   double ref_slack;      // moment-reference slack (64; 0 = rescale at every new max)
   const Rec* recs[PF_MAX_SHARDS];  // sharded run: every shard's records of step t-1
+  RepStride rp;          // batched replications (gridDim.z > 1)
 };
 
 PF_D double warp_sum(double v) {
@@ -483,21 +483,25 @@ PF_D void cp_async8(uint32_t dst, const void* src) {
 // flight -- the issue slots the latency-bound gather pipeline leaves idle --
 // instead of a separate compute-bound draws kernel and a round trip of the
 // draws through HBM.
-template <int MODE, typename TQ, bool FD = false>
+template <int MODE, typename TQ, bool FD = false, bool BATCH = false>
 __global__ void __launch_bounds__(FD ? FD_THREADS : 256, 1) step_kernel(StepArgs<TQ> a) {
   constexpr bool LS = MODE & M_LS, LT = MODE & M_LT, SINGLE = MODE & M_SINGLE;
   constexpr int SB = step_sb<FD>();  // slots per thread per pipeline stage
   // batched replications (gridDim.z = R): replication blockIdx.z's slice of
   // every array (locals: the kernel parameters themselves stay read-only)
-  const int64_t rz = blockIdx.z, ro = rz * a.n;
+  // (BATCH = false: the single-run instantiation, rz = ro = 0 at compile time)
+  const int64_t rz = BATCH ? (int64_t)blockIdx.z : 0, ro = rz * a.n;
   // (per-slot arrays are indexed at ro + j below; ro = 0 for a single run)
-  Lookup<TQ> lk_ = a.lk;
-  lk_.q += ro;
-  lk_.cut += ro;
+  Lookup<TQ> lk_b = a.lk;
+  if (BATCH) {
+    lk_b.q += ro;
+    lk_b.cut += ro;
+  }
+  const Lookup<TQ>& lk_ = BATCH ? lk_b : a.lk;  // single run: the parameter itself
   Partial* const partials_ = a.partials + rz * gridDim.x;
   Scalars* const sc_ = a.sc + rz;
   int64_t* const fail_ = a.fail + rz;
-  const uint64_t* const dseedp_ = a.dr.seedp ? a.dr.seedp + rz : nullptr;
+  const uint64_t* const dseedp_ = (BATCH && a.dr.seedp) ? a.dr.seedp + rz : a.dr.seedp;
   // the step's tables are constant over the run: stage them while the
   // previous kernel (group build / K4) drains, then wait for its outputs
   int slot_s = -1, slot_t = -1, noff = -1, tab_doubles = 0;
