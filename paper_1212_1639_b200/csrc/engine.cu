@@ -274,6 +274,8 @@ int launch_reduce_qr_m(int grid, WSrc src, int R, TQ* tt, TQ* ct, int64_t* fail,
   }();
   const int64_t tiles = R * (int64_t)(CDF_THREADS / CLS_THR);  // R: K2 tiles
   const int64_t want = env_grid > 0 ? std::min<int64_t>(env_grid, CDF_MAX_CHUNKS) : (int64_t)sm_count() * occ;
+  // batched: the R replications share one grid's worth of CTAs (these
+  // kernels carry a per-CTA fixed cost: shared histograms, partial flushes)
   const int g = (int)std::min<int64_t>(tiles, std::max<int64_t>(1, want / reps));
   kern<<<dim3(g, 1, reps), CLS_THR, smem, st>>>(src, (int)tiles, tt, ct, fail, qa);
   LAUNCHED();
@@ -1064,9 +1066,18 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   if (docc < 1) docc = 1;
   // persistent grids: one wave of resident CTAs
   const int64_t nbatches = (n + STEP_SBX * STEP_THREADS - 1) / (STEP_SBX * STEP_THREADS);
-  // (batched: one wave shared by the R replications)
-  const int step_grid = (int)std::min<int64_t>(nbatches, std::max<int64_t>(1, (int64_t)sms * occ / R));
+  // Batched: PF_BATCH_WAVES=1 (default) gives every replication a full wave
+  // of CTAs, so the block scheduler runs the replications roughly one after
+  // another (z-major order) and only ~one replication's lookup tables and
+  // records are hot in L2 at a time; 0 shares one wave among all R.
+  static const int batch_waves = [] {
+    const char* v = getenv("PF_BATCH_WAVES");
+    return v ? atoi(v) : 1;
+  }();
+  const int64_t wave_div = (R > 1 && !batch_waves) ? R : 1;
+  const int step_grid = (int)std::min<int64_t>(nbatches, std::max<int64_t>(1, (int64_t)sms * occ / wave_div));
   const int draw_grid = (int)std::min<int64_t>((n + 255) / 256, std::max<int64_t>(1, (int64_t)sms * docc / R));
+  if (R > 1) CK(e->partials.ensure((size_t)R * step_grid + 8));  // [R][step_grid] moment partials
   auto launch_draws = [&](int64_t t, cudaStream_t s_) {
     DrawArgs d;
     memset(&d, 0, sizeof(d));

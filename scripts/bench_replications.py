@@ -26,7 +26,7 @@ def main():
     ap.add_argument("--n", type=int, default=1 << 20)
     ap.add_argument("--t", type=int, default=100)
     ap.add_argument("--concurrency", type=int, default=1)
-    ap.add_argument("--batch", type=int, default=16,
+    ap.add_argument("--batch", type=int, default=32,
                     help="replications per launch sequence (pf_engine_run_batch); 1 = one at a time")
     args = ap.parse_args()
     world, rank, local = bench.dist_setup()
@@ -45,11 +45,12 @@ def main():
         from paper_1212_1639_b200.filtering import run_batch
 
         run_batch(P.Priors(), y, args.n, list(range(10 ** 6, 10 ** 6 + min(args.batch, len(seeds)))),
-                  backend=backend)  # warm-up: buffers and the captured loop of this batch shape
+                  backend=backend, track_quantiles=False)  # warm-up: buffers and the captured loop
         bench.barrier(world)
         t0 = time.perf_counter()
         for lo in range(0, len(seeds), args.batch):
-            outs = run_batch(P.Priors(), y, args.n, seeds[lo:lo + args.batch], backend=backend)
+            outs = run_batch(P.Priors(), y, args.n, seeds[lo:lo + args.batch], backend=backend,
+                             track_quantiles=False)
             dev_ms += eng.last_timing()["total_ms"]
             _ = [o.param_posterior["sigma2"].mean[-1] for o in outs]
     elif args.concurrency > 1:

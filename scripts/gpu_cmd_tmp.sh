@@ -1,14 +1,6 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_batch.py -q -x -m gpu 2>&1 | tail -2
-pj() { python -c "
-import json,sys
-for l in sys.stdin:
-    if l.startswith('{'):
-        d=json.loads(l); print('$1', round(d['value']/1e9,3), d.get('roofline',{}).get('step_kernel_ms'))
-"; }
-R=$PWD
-for d in $R $R/_abhead $R $R/_abhead $R $R/_abhead; do
-  echo "== $d"
-  (cd $d && timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $R/gpurun_out/ab24.log 2>&1); pj 2^24 < gpurun_out/ab24.log
-done
+timeout 900 python -m pytest tests/test_gpu_batch.py -q -x -m gpu 2>&1 | tail -4
+compute-sanitizer --tool memcheck timeout 600 python -m pytest tests/test_gpu_batch.py -q -x -m gpu -k "pl_matches and 4096 or known_parameters or engine_reuse" > gpurun_out/memcheck_batch.txt 2>&1; tail -3 gpurun_out/memcheck_batch.txt
+compute-sanitizer --tool racecheck timeout 600 python -m pytest tests/test_gpu_batch.py -q -x -m gpu -k "known_parameters" > gpurun_out/racecheck_batch.txt 2>&1; tail -3 gpurun_out/racecheck_batch.txt
+for r in 32; do timeout 300 python scripts/bench_replications.py --reps 128 --batch $r | tail -1; done

@@ -109,3 +109,32 @@ def test_batched_restrictions(gpu):
     one = run_batch(P.Priors(), y, 1 << 10, [4])          # R = 1 is the ordinary run
     ref = P.run_particle_learning(P.Priors(), y, 1 << 10, seed=4)
     np.testing.assert_array_equal(one[0].filtered_mean, ref.filtered_mean)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_replications_across_ranks(gpu, tmp_path, world):
+    """Replicas only (SURVEY §8e configs[4]): ranks take seeds round robin
+    and batch them; the gathered summaries match one-at-a-time runs."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+    import test_gpu_dist as TD
+
+    out = str(tmp_path / "reps.npz")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(TD._port()),
+           os.path.join(ROOT, "tests", "workers", "replication_worker.py"), "--out", out]
+    env = dict(os.environ, PYTHONPATH=ROOT + os.pathsep + os.environ.get("PYTHONPATH", ""))
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    d = np.load(out)
+    assert list(d["seeds"]) == list(range(7))
+    y = TD._series(10)
+    with P.Backend() as b:
+        for i, s in enumerate(range(7)):
+            one = P.run_particle_learning(P.Priors(), y, 1 << 12, seed=s, backend=b)
+            assert _close(d["fmean"][i], one.filtered_mean) <= 1e-10
+            assert _close(d["smean"][i], one.param_posterior["sigma2"].mean) <= 1e-10
+            assert np.mean(d["tq"][i] == one.param_posterior["tau2"].quantiles) >= 0.99
