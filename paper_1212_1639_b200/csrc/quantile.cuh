@@ -300,6 +300,31 @@ PF_D void q_flush(const QArgs& qa, QAgg& agg) {
 }
 
 // Block-reduce the below-window sums and W, combine CTAs in fixed order.
+// Last-CTA sum of P partial rows of NS slots (row stride `stride`), by the
+// whole CTA: thread t sums slot t % NS over rows t / NS, t / NS + G, ...
+// (G groups, independent L2 loads in flight), then threads
+// < NS add the G group sums in group order.  Deterministic (fixed order for
+// a given P and blockDim); the serial form kept ~600 dependent L2 loads on
+// one thread per slot, tens of microseconds per step.  Returns the slot sum
+// in threads < NS.
+template <int NS, int G>
+PF_D double q_sum_rows(const double* part, unsigned P, int stride, double (*grp)[NS]) {
+  // grp: G x NS shared scratch (the caller's warp-sum array, free again here)
+  const int s = (int)threadIdx.x % NS, g = (int)threadIdx.x / NS;
+  double v = 0.0;
+  __syncthreads();
+  if (g < G) {
+#pragma unroll 4
+    for (unsigned b = g; b < P; b += G) v += __ldcg(&part[(size_t)b * stride + s]);
+    grp[g][s] = v;
+  }
+  __syncthreads();
+  double tot = 0.0;
+  if ((int)threadIdx.x < NS)
+    for (int k = 0; k < G; ++k) tot += grp[k][threadIdx.x];
+  return tot;
+}
+
 PF_D void q_reduce_partials(const QArgs& qa, const QWin& win, double (&acc)[Q_SLOTS], double wsum) {
   __shared__ double red[8][Q_SLOTS + 1];
   __shared__ bool last;
@@ -322,9 +347,8 @@ PF_D void q_reduce_partials(const QArgs& qa, const QWin& win, double (&acc)[Q_SL
   __syncthreads();
   if (!last) return;
   __threadfence();
+  const double s = q_sum_rows<Q_SLOTS + 1, 8>(qa.part, q_ptotal(qa), Q_SLOTS + 1, red);
   if (threadIdx.x <= Q_SLOTS) {
-    double s = 0.0;
-    for (unsigned b = 0; b < q_ptotal(qa); ++b) s += __ldcg(&qa.part[(size_t)b * (Q_SLOTS + 1) + threadIdx.x]);
     if (threadIdx.x == Q_SLOTS) {
       qa.sh->W = s;
     } else {
@@ -1099,7 +1123,7 @@ q_fallback_hist_kernel(QArgs qa, const double* __restrict__ lw, int wmode, const
     }
   }
   // deterministic combine of the below-interval sums
-  __shared__ double red[8][Q_MAXT];
+  __shared__ double red[8][Q_MAXT + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int k = 0; k < Q_MAXT; ++k) {
     double v = acc[k];
@@ -1118,11 +1142,8 @@ q_fallback_hist_kernel(QArgs qa, const double* __restrict__ lw, int wmode, const
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (threadIdx.x < qa.ntarget && act[threadIdx.x]) {
-    double s = 0.0;
-    for (unsigned b = 0; b < q_ptotal(qa); ++b) s += __ldcg(&qa.part[(size_t)b * (Q_MAXT + 1) + threadIdx.x]);
-    qa.tg[threadIdx.x].ibelow = s;
-  }
+  const double s = q_sum_rows<Q_MAXT + 1, 8>(qa.part, q_ptotal(qa), Q_MAXT + 1, red);
+  if (threadIdx.x < qa.ntarget && act[threadIdx.x]) qa.tg[threadIdx.x].ibelow = s;
   if (threadIdx.x == 0) qa.sh->fb_counter = 0;
 }
 
