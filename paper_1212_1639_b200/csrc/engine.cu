@@ -273,7 +273,13 @@ int launch_reduce_qr_m(int grid, WSrc src, int R, TQ* tt, TQ* ct, int64_t* fail,
     return v ? atoi(v) : 0;
   }();
   const int64_t tiles = R * (int64_t)(CDF_THREADS / CLS_THR);  // R: K2 tiles
-  const int64_t want = env_grid > 0 ? std::min<int64_t>(env_grid, CDF_MAX_CHUNKS) : (int64_t)sm_count() * occ;
+  // Each CTA carries a fixed cost (windows, region-sum init, candidate flush,
+  // partial reduction), so small N gets fewer, fuller CTAs: at least 4 tiles
+  // each, down to one per SM (2^20: 148 CTAs, +6 % per step vs 444; 2^22 and up
+  // keep a full wave: one per SM there was 8 % slower).
+  const int64_t want = env_grid > 0 ? std::min<int64_t>(env_grid, CDF_MAX_CHUNKS)
+                                    : std::min<int64_t>((int64_t)sm_count() * occ,
+                                                        std::max<int64_t>(sm_count(), tiles * reps / 4));
   // batched: the R replications share one grid's worth of CTAs (these
   // kernels carry a per-CTA fixed cost: shared histograms, partial flushes)
   const int g = (int)std::min<int64_t>(tiles, std::max<int64_t>(1, want / reps));
