@@ -5,7 +5,9 @@ for l in sys.stdin:
     if l.startswith('{'):
         d=json.loads(l); print('$1', round(d['value']/1e9,3), d.get('roofline',{}).get('step_kernel_ms'))
 "; }
-for n in 1048576 2097152 4194304 16777216; do
+for m in 0 8192 16384 0 8192 16384; do
+  export PF_FB_MIN=$m; echo "== fbmin $m"
+  for n in 1048576 4194304; do
   timeout 300 python bench.py --steps 3 --warmup 3 --n $n --no-cpu-baseline > gpurun_out/ab.log 2>&1; pj $n < gpurun_out/ab.log
+  done
 done
-timeout 300 python scripts/bench_replications.py --reps 128 --batch 32 | tail -1 | cut -c1-120
