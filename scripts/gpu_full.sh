@@ -13,7 +13,8 @@ tail -2 gpurun_out/bench.log
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1; tail -1 gpurun_out/bench_ref.log
 timeout 600 python bench.py --resampler spacings --no-cpu-baseline > gpurun_out/bench_spacings.log 2>&1; tail -1 gpurun_out/bench_spacings.log
 timeout 600 python bench.py --n 1048576 --t 1000 --no-cpu-baseline > gpurun_out/bench_2e20.log 2>&1; tail -1 gpurun_out/bench_2e20.log
-timeout 600 python scripts/bench_replications.py --reps 64 --concurrency 1 > gpurun_out/bench_replications.log 2>&1; tail -1 gpurun_out/bench_replications.log
+timeout 600 python scripts/bench_replications.py --reps 128 > gpurun_out/bench_replications.log 2>&1; tail -1 gpurun_out/bench_replications.log
+timeout 600 python scripts/bench_replications.py --reps 64 --batch 1 > gpurun_out/bench_replications_b1.log 2>&1; tail -1 gpurun_out/bench_replications_b1.log
 timeout 600 python bench.py --process-group --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_pg.log 2>&1; tail -1 gpurun_out/bench_pg.log
 timeout 600 python bench.py --process-group --resampler spacings --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_pg_spacings.log 2>&1; tail -1 gpurun_out/bench_pg_spacings.log
 PF_CHAIN_DEBUG=1 timeout 300 python scripts/prof_run.py 24 300 > gpurun_out/chain.log 2>&1
