@@ -212,9 +212,14 @@ struct TopFuse {
 template <typename T>
 __global__ void __launch_bounds__(CDF_THREADS)
 cdf_reduce_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ chunk_tot,
-                  const int64_t* __restrict__ fail, TopFuse<T> top = TopFuse<T>()) {
+                  const int64_t* __restrict__ fail, TopFuse<T> top = TopFuse<T>(),
+                  double* __restrict__ wout = nullptr) {
+  // wout (optional): the step's weights w = exp(lw - M) as computed here, for
+  // K4 and the quantile classification to read (WSrc mode 1) instead of
+  // recomputing the exp -- the same values, so the same bits
   if (gridDim.z > 1) {  // batched replications: replication blockIdx.z's tree
     const int64_t r = blockIdx.z, G = gridDim.x;
+    if (wout) wout += r * G * R * CDF_TILE;
     src = wsrc_rep(src, G * R * CDF_TILE);
     tile_tot += r * G * R;
     chunk_tot += r * G;
@@ -240,6 +245,11 @@ cdf_reduce_kernel(WSrc src, int R, T* __restrict__ tile_tot, T* __restrict__ chu
     const int64_t tile = chunk * R + r;
     T v[CDF_V], l1[4], l2[2], g;
     load_tile_weights<T>(src, tile * CDF_TILE + threadIdx.x * CDF_V, M, v);
+    if (wout) {
+      double2* wp = reinterpret_cast<double2*>(wout + tile * CDF_TILE + threadIdx.x * CDF_V);
+#pragma unroll
+      for (int k = 0; k < CDF_V / 2; ++k) __stcg(wp + k, make_double2((double)v[2 * k], (double)v[2 * k + 1]));
+    }
     thread_tree8<T>(v, l1, l2, g);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) g = g + __shfl_xor_sync(0xffffffffu, g, o);

@@ -423,9 +423,12 @@ int launch_cdf_tail(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t
 
 // reps > 1: that many independent trees of n leaves in one launch each
 // (batched replications; K3 fused into K2, no strata tables)
+// wout (fp64 only): K2 also writes the weights it forms, K4 reads them
+// (WSrc mode 1) and ev_k2 marks them ready for other streams.
 template <typename T>
 int launch_cdf(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t* fail, int64_t step,
-               cudaStream_t st, StrataOut so = StrataOut(), int reps = 1) {
+               cudaStream_t st, StrataOut so = StrataOut(), int reps = 1, double* wout = nullptr,
+               cudaEvent_t ev_k2 = nullptr) {
   const CdfPlan& p = b.plan;
   T* total = (T*)b.total.p;
   if (reps > 1 && (p.small || so.on || !fuse_top()))
@@ -447,10 +450,16 @@ int launch_cdf(CdfBufs& b, WSrc src, int64_t n, T* q, int32_t* cut, int64_t* fai
     top.step = step;
   }
   CK(launch_pdl(PDL_K2, cdf_reduce_kernel<T>, dim3((int)p.chunks, 1, reps), dim3(CDF_THREADS), 0, st, src, p.R,
-                (T*)b.tile_tot.p, (T*)b.chunk_tot.p, (const int64_t*)fail, top));
+                (T*)b.tile_tot.p, (T*)b.chunk_tot.p, (const int64_t*)fail, top, wout));
   LAUNCHED();
+  if (ev_k2) CK(cudaEventRecord(ev_k2, st));
   chain_mark(st);
-  return launch_cdf_tail<T>(b, src, n, q, cut, fail, step, st, so, fused, reps);
+  WSrc tail = src;
+  if (wout) {
+    tail.src = wout;
+    tail.mode = 1;
+  }
+  return launch_cdf_tail<T>(b, tail, n, q, cut, fail, step, st, so, fused, reps);
 }
 
 // K3 + K4 (after K2, or after the quantile-fused K2).
@@ -503,6 +512,8 @@ struct pf_engine {
   bool single = false;
   DevBuf<Rec> rec[2];
   DevBuf<double> lw;      // log-weights, double-buffered by step parity: [2][n]
+  DevBuf<double> wbuf;    // fp64 weights exp(lw - M) written by K2, by parity: [2][n]
+  cudaEvent_t ev_k2 = nullptr;  // K2 of the step done (wbuf ready for the side stream)
   // draws of step t (draws_kernel), double-buffered by step parity: [2][n]
   DevBuf<double> dz, dgs, dgt;
   DevBuf<uint64_t> du3;
@@ -611,7 +622,7 @@ void drop_graph(pf_engine* e) {
 // Every device buffer a captured loop's kernels point at: a captured graph is
 // only valid while none of them has moved.
 uint64_t graph_buffers_sig(const pf_engine* e) {
-  const void* ps[] = {e->rec[0].p, e->rec[1].p, e->lw.p, e->du3.p, e->dz.p, e->dgs.p, e->dgt.p, e->q.p, e->cut.p,
+  const void* ps[] = {e->rec[0].p, e->rec[1].p, e->lw.p, e->wbuf.p, e->du3.p, e->dz.p, e->dgs.p, e->dgt.p, e->q.p, e->cut.p,
                       e->rank.p, e->f32.p, e->keys.p, e->qtg.p, e->qsh.p, e->qcand.p, e->qpart.p, e->qscratch.p,
                       e->mbuf.p, e->qhist.p, e->qfhist.p, e->qunres.p, e->qlidx.p, e->qlw.p, e->partials.p, e->sc.p,
                       e->fail.p, e->o_fm.p, e->o_sm.p, e->o_ssd.p, e->o_tm.p, e->o_tsd.p, e->o_fq.p, e->o_sq.p,
@@ -1112,6 +1123,18 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   TQ* qv = (TQ*)e->q.p;
   int64_t step_launches = 0;
   const CdfPlan plan = cdf_plan(n);
+  // fp64, N <= 2^22: K2 writes the weights it forms (w = exp(lw - M)) and K4
+  // and the classification read them instead of recomputing the exp (same
+  // bits); the classification then starts after K2.  Measured +1 % at 2^20 /
+  // 2^22 but -0.8 % at 2^24, where the later classification overlaps the
+  // next step kernel instead of K2 / K4.  PF_WBUF=0/1 overrides.
+  static const int wbuf_env = [] {
+    const char* v = getenv("PF_WBUF");
+    return v ? atoi(v) : -1;
+  }();
+  const bool use_w = (wbuf_env >= 0 ? wbuf_env != 0 : ilog2(n) <= 22) && std::is_same<TQ, double>::value &&
+                     uses_cut_tables(c.resampler) && !plan.small && !fw;
+  if (use_w) CK(e->wbuf.ensure(2 * (size_t)NT));  // (before any graph capture: no allocation inside one)
   StrataOut so;
   Lookup<TQ> lk;
   lk.q = qv;
@@ -1338,26 +1361,40 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
     // ---- K2-K4 CDF + cut table (main stream); K5 weighted quantiles on the
     // side stream: window classification of step t, then the exact resolve,
     // overlapping the CDF and the next step's propagation.
+    WSrc wq = wsrc;  // the classification's weight source
+    if (use_w) {
+      wq.src = e->wbuf.p + (size_t)par * NT;
+      wq.mode = 1;
+      if ((rc = launch_cdf<TQ>(e->cdf, wsrc, n, qv, e->cut.p, e->fail.p, t, st, so, (int)R,
+                               e->wbuf.p + (size_t)par * NT, ntg ? e->ev_k2 : nullptr)) != PF_OK)
+        return rc;
+    }
     if (ntg) {
       qa.sh = qshp;
       qa.keys[0] = want_fq ? kbase : nullptr;
       qa.keys[1] = want_sq ? kbase + NT : nullptr;
       qa.keys[2] = want_tq ? kbase + 2 * (size_t)NT : nullptr;
-      CK(cudaEventRecord(e->ev_b, st));  // K1b(t): keys, log-weights, M, moments
       cudaStream_t ss = e->side;
-      CK(cudaStreamWaitEvent(ss, e->ev_b, 0));
+      if (use_w) {
+        CK(cudaStreamWaitEvent(ss, e->ev_k2, 0));  // K2(t): weights (and K1b(t) before it)
+      } else {
+        CK(cudaEventRecord(e->ev_b, st));  // K1b(t): keys, log-weights, M, moments
+        CK(cudaStreamWaitEvent(ss, e->ev_b, 0));
+      }
       if (plan.small || !uses_cut_tables(c.resampler)) {  // any n (bounds-checked pass)
         q_window_kernel<TQ><<<grid_for(n, 256), 256, 0, ss>>>(wsrc, n, e->fail.p, qa);
         LAUNCHED();
       } else {
         const int qm = (want_fq ? 1 : 0) | (want_sq ? 2 : 0) | (want_tq ? 4 : 0);
-        if ((rc = launch_reduce_qr<TQ>(qm, 0, wsrc, (int)plan.tiles, nullptr, nullptr, e->fail.p, qa,
+        if ((rc = launch_reduce_qr<TQ>(qm, 0, wq, (int)plan.tiles, nullptr, nullptr, e->fail.p, qa,
                                        ss, (int)R)) != PF_OK)
           return rc;
       }
     }
     if (uses_cut_tables(c.resampler)) {
-      if ((rc = launch_cdf<TQ>(e->cdf, wsrc, n, qv, e->cut.p, e->fail.p, t, st, so, (int)R)) != PF_OK) return rc;
+      if (!use_w &&
+          (rc = launch_cdf<TQ>(e->cdf, wsrc, n, qv, e->cut.p, e->fail.p, t, st, so, (int)R)) != PF_OK)
+        return rc;
       if (spacings && sp_inline) {
         const uint64_t* w = e->du3.p + (size_t)(t % 3) * n;
         auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0), ExpOfWord{w});
@@ -1886,7 +1923,8 @@ int pf_engine_create(const pf_config* cfg, pf_engine** out) {
   if ((err = cudaEventCreateWithFlags(&e->ev_b, cudaEventDisableTiming)) ||
       (err = cudaEventCreateWithFlags(&e->ev_e, cudaEventDisableTiming)) ||
       (err = cudaEventCreateWithFlags(&e->ev_q[0], cudaEventDisableTiming)) ||
-      (err = cudaEventCreateWithFlags(&e->ev_q[1], cudaEventDisableTiming)) || (err = e->mbuf.ensure(2)))
+      (err = cudaEventCreateWithFlags(&e->ev_q[1], cudaEventDisableTiming)) ||
+      (err = cudaEventCreateWithFlags(&e->ev_k2, cudaEventDisableTiming)) || (err = e->mbuf.ensure(2)))
     return bail(err);
   if ((err = e->rec[0].ensure(n)) || (err = e->rec[1].ensure(n)) || (err = e->lw.ensure(2 * n)) ||
       (err = e->du3.ensure(3 * n)) || (err = e->partials.ensure(sm_count() * 8 + 8)) ||
@@ -2501,7 +2539,7 @@ int pf_engine_destroy(pf_engine* e) {
   cudaSetDevice(e->cfg.device);
   if (e->st) cudaStreamSynchronize(e->st);
   drop_graph(e);
-  DevBuf<double>* bufs[] = {&e->lw, &e->s2init, &e->o_fm, &e->o_sm, &e->o_ssd,
+  DevBuf<double>* bufs[] = {&e->lw, &e->wbuf, &e->s2init, &e->o_fm, &e->o_sm, &e->o_ssd,
                             &e->o_tm, &e->o_tsd, &e->o_fq, &e->o_sq, &e->o_tq, &e->o_ess, &e->probs, &e->m_x, &e->m_s2, &e->m_t2, &e->m_as,
                             &e->m_bs, &e->m_at, &e->m_bt, &e->feed_buf};
   for (auto* b : bufs) b->release();
@@ -2555,6 +2593,7 @@ int pf_engine_destroy(pf_engine* e) {
   if (e->side) cudaStreamSynchronize(e->side);
   if (e->side) cudaStreamDestroy(e->side);
   if (e->ev_b) cudaEventDestroy(e->ev_b);
+  if (e->ev_k2) cudaEventDestroy(e->ev_k2);
   if (e->ev_e) cudaEventDestroy(e->ev_e);
   for (auto ev : e->ev_q)
     if (ev) cudaEventDestroy(ev);
