@@ -1,15 +1,4 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_gpu_engine.py tests/test_gpu_parity_large.py tests/test_gpu_batch.py tests/test_gpu_kernels.py -q -x -m gpu 2>&1 | tail -2
-pj() { python -c "
-import json,sys
-for l in sys.stdin:
-    if l.startswith('{'):
-        d=json.loads(l); print('$1', round(d['value']/1e9,3), d.get('roofline',{}).get('step_kernel_ms'))
-"; }
-for w in 1 0 1 0; do
-  export PF_WBUF=$w; echo "== wbuf $w"
-  for n in 16777216 4194304 1048576; do
-  timeout 300 python bench.py --steps 3 --warmup 3 --n $n --no-cpu-baseline > gpurun_out/ab.log 2>&1; pj $n < gpurun_out/ab.log
-  done
-done
+PF_PROFILE_FROM_STEP=200 timeout 900 ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:"cdf_expand|cdf_reduce_kernel" -c 2 -o gpurun_out/k4_full python scripts/prof_run.py 24 205 > gpurun_out/ncu_k4.log 2>&1
+tail -2 gpurun_out/ncu_k4.log
