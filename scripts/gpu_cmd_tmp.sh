@@ -1,4 +1,5 @@
 #!/bin/bash
 mkdir -p gpurun_out
-PF_PROFILE_FROM_STEP=200 timeout 900 ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:"cdf_expand|cdf_reduce_kernel" -c 2 -o gpurun_out/k4_full python scripts/prof_run.py 24 205 > gpurun_out/ncu_k4.log 2>&1
-tail -2 gpurun_out/ncu_k4.log
+timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+tail -3 gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -1
