@@ -149,6 +149,7 @@ def test_kalman_hand_case():
     assert m[0] == pytest.approx(20 / 11, rel=1e-14) and v[0] == pytest.approx(10 / 11, rel=1e-14)
 
 
+@pytest.mark.filterwarnings("ignore:overflow encountered:RuntimeWarning")  # the degenerate weights themselves
 def test_degenerate_step_raises():
     with pytest.raises(R.Degenerate) as ei:
         R.run_loop(np.array([1e200]), 16, 0, sigma2=1e-300, tau2=0.1)
