@@ -1,5 +1,12 @@
 #!/bin/bash
-mkdir -p gpurun_out
-timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-tail -3 gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -1
+pj() { python -c "
+import json,sys
+for l in sys.stdin:
+    if l.startswith('{'):
+        d=json.loads(l); print('$1', round(d['value']/1e9,3), d.get('roofline',{}).get('step_kernel_ms'))
+"; }
+for w in 2 0 2 0 2 0; do
+  export PF_WBUF=$w; echo "== wbuf $w"
+  timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ab.log 2>&1; pj 2^24 < gpurun_out/ab.log
+done
+PF_WBUF=2 timeout 600 python -m pytest tests/test_gpu_parity_large.py -q -x -m gpu 2>&1 | tail -1
