@@ -138,3 +138,24 @@ def test_replications_across_ranks(gpu, tmp_path, world):
             assert _close(d["fmean"][i], one.filtered_mean) <= 1e-10
             assert _close(d["smean"][i], one.param_posterior["sigma2"].mean) <= 1e-10
             assert np.mean(d["tq"][i] == one.param_posterior["tau2"].quantiles) >= 0.99
+
+
+def test_batched_replications_do_not_interact(gpu):
+    """The same seed in two slots of a batch gives bit-identical summaries
+    (each replication reads and writes only its own slices), whatever sits
+    between them; T = 0 and T = 1 batches are well formed."""
+    y = _series(30, seed=6)
+    with P.Backend() as b:
+        outs = run_batch(P.Priors(), y, 1 << 13, [5, 9, 5, 123, 5], backend=b, track_quantiles=True)
+        for k in (2, 4):
+            np.testing.assert_array_equal(outs[k].filtered_mean, outs[0].filtered_mean)
+            np.testing.assert_array_equal(outs[k].filtered_quantiles, outs[0].filtered_quantiles)
+            for name in ("sigma2", "tau2"):
+                np.testing.assert_array_equal(outs[k].param_posterior[name].quantiles,
+                                              outs[0].param_posterior[name].quantiles)
+        assert not np.array_equal(outs[1].filtered_mean, outs[0].filtered_mean)
+        empty = run_batch(P.Priors(), y[:0], 1 << 13, [1, 2], backend=b)
+        assert len(empty) == 2 and empty[0].filtered_mean.shape == (0,)
+        one = run_batch(P.Priors(), y[:1], 1 << 13, [1, 2], backend=b)
+        ref = P.run_particle_learning(P.Priors(), y[:1], 1 << 13, seed=2, backend=b)
+        _compare(one[1], ref)
