@@ -513,6 +513,10 @@ struct pf_engine {
   DevBuf<Rec> rec[2];
   DevBuf<double> lw;      // log-weights, double-buffered by step parity: [2][n]
   DevBuf<double> wbuf;    // fp64 weights exp(lw - M) written by K2, by parity: [2][n]
+  // store_particles: snapshots are materialised into two halves (by step
+  // parity) and copied out on their own stream, overlapping the next step
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_mat[2] = {nullptr, nullptr}, ev_cp[2] = {nullptr, nullptr};
   cudaEvent_t ev_k2 = nullptr;  // K2 of the step done (wbuf ready for the side stream)
   // draws of step t (draws_kernel), double-buffered by step parity: [2][n]
   DevBuf<double> dz, dgs, dgt;
@@ -804,6 +808,35 @@ int spacings_words(pf_engine* e, int64_t t) {
   return PF_OK;
 }
 
+// PF_HOST_PIN=1: page-lock the run's large host outputs (per-step
+// snapshots, ancestor rows) for the run, so their device-to-host copies are
+// DMA at PCIe rate (56 GB/s vs 21 GB/s pageable and 3.9 GB/s into fresh
+// pages, scripts/micro/d2h_store.py).  Off by default: the API hands over
+// freshly allocated arrays, and registering them faults every page in on one
+// thread first -- measured slower end to end (store at 2^20: 17.5-19.7 vs
+// 13.8-15.1 ms per step).  Memory already page-locked is left as it is;
+// unregistered after the streams drain, error paths included.
+struct HostPins {
+  std::vector<void*> ptrs;
+  cudaStream_t a = nullptr, b = nullptr;
+  void add(void* p, size_t bytes) {
+    static const bool on = [] {
+      const char* v = getenv("PF_HOST_PIN");
+      return v ? atoi(v) != 0 : false;
+    }();
+    if (!on || !p || !bytes) return;
+    if (cudaHostRegister(p, bytes, cudaHostRegisterDefault) == cudaSuccess) ptrs.push_back(p);
+    else cudaGetLastError();
+  }
+  ~HostPins() {
+    if (ptrs.empty()) return;
+    if (a) cudaStreamSynchronize(a);
+    if (b) cudaStreamSynchronize(b);
+    for (void* p : ptrs) cudaHostUnregister(p);
+    cudaGetLastError();
+  }
+};
+
 struct RunSpec {
   const double* y;
   int64_t T;
@@ -839,6 +872,25 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
   const bool timing = out && c.phase_timing;
   int rc;
   if ((rc = build_tables(e, T)) != PF_OK) return rc;
+  HostPins pins;
+  if (store || keep_idx) {
+    if (store && !e->cstream) {
+      CK(cudaStreamCreateWithFlags(&e->cstream, cudaStreamNonBlocking));
+      for (int k = 0; k < 2; ++k) {
+        CK(cudaEventCreateWithFlags(&e->ev_mat[k], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&e->ev_cp[k], cudaEventDisableTiming));
+      }
+    }
+    pins.a = st;
+    pins.b = e->cstream;
+    const size_t rows = (size_t)(T > 0 ? T : 0) * (size_t)n;
+    if (keep_idx) pins.add(out->indices, rows * sizeof(int64_t));
+    if (store) {
+      double* h[7] = {out->hist_states, out->hist_sigma2, out->hist_tau2, out->hist_a_sigma,
+                      out->hist_b_sigma, out->hist_a_tau, out->hist_b_tau};
+      for (double* p : h) pins.add(p, rows * sizeof(double));
+    }
+  }
 
   const size_t TT = (size_t)(T > 0 ? T : 1) * R;  // [R][T] rows
   CK(e->o_fm.ensure(TT));
@@ -1549,22 +1601,35 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
       m.a_t = shape_at(e, false, t);
       m.idx = nullptr;
       size_t off = (size_t)(t - 1) * n;
-      CK(e->m_x.ensure(n)); CK(e->m_s2.ensure(n)); CK(e->m_t2.ensure(n)); CK(e->m_as.ensure(n));
-      CK(e->m_bs.ensure(n)); CK(e->m_at.ensure(n)); CK(e->m_bt.ensure(n));
-      m.x = e->m_x.p; m.s2 = e->m_s2.p; m.t2 = e->m_t2.p; m.as = e->m_as.p; m.bs = e->m_bs.p;
-      m.at = e->m_at.p; m.bt = e->m_bt.p;
+      // snapshot halves by step parity: step t waits only for step t-2's
+      // copies out of its half; the copies run on cstream beside step t+1
+      const int sp = (int)(t & 1);
+      if (t > 2) CK(cudaStreamWaitEvent(st, e->ev_cp[sp], 0));
+      CK(e->m_x.ensure(2 * n)); CK(e->m_s2.ensure(2 * n)); CK(e->m_t2.ensure(2 * n)); CK(e->m_as.ensure(2 * n));
+      CK(e->m_bs.ensure(2 * n)); CK(e->m_at.ensure(2 * n)); CK(e->m_bt.ensure(2 * n));
+      const size_t mo = (size_t)sp * n;
+      m.x = e->m_x.p + mo; m.s2 = e->m_s2.p + mo; m.t2 = e->m_t2.p + mo; m.as = e->m_as.p + mo;
+      m.bs = e->m_bs.p + mo; m.at = e->m_at.p + mo; m.bt = e->m_bt.p + mo;
       m.fail = e->fail.p;
       materialize_kernel<TQ><<<grid_for(n, 256), 256, 0, st>>>(m);
       LAUNCHED();
+      CK(cudaEventRecord(e->ev_mat[sp], st));
+      CK(cudaStreamWaitEvent(e->cstream, e->ev_mat[sp], 0));
       double* dst[7] = {out->hist_states, out->hist_sigma2, out->hist_tau2, out->hist_a_sigma,
                         out->hist_b_sigma, out->hist_a_tau, out->hist_b_tau};
       double* src[7] = {m.x, m.s2, m.t2, m.as, m.bs, m.at, m.bt};
       for (int k = 0; k < 7; ++k)
-        if (dst[k]) CK(cudaMemcpyAsync(dst[k] + off, src[k], n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        if (dst[k])
+          CK(cudaMemcpyAsync(dst[k] + off, src[k], n * sizeof(double), cudaMemcpyDeviceToHost, e->cstream));
+      CK(cudaEventRecord(e->ev_cp[sp], e->cstream));
       mark(PH_STORE);
     }
   }
 
+  if (store) {  // the snapshot copies join the main stream (the final system reuses the halves)
+    CK(cudaStreamWaitEvent(st, e->ev_cp[0], 0));
+    CK(cudaStreamWaitEvent(st, e->ev_cp[1], 0));
+  }
   if (use_graph && !replay) {
     // join every forked stream, then instantiate and run the captured loop
     // (fresh records at each side stream's tail: a stream's last record covers
@@ -2594,6 +2659,14 @@ int pf_engine_destroy(pf_engine* e) {
   if (e->side) cudaStreamDestroy(e->side);
   if (e->ev_b) cudaEventDestroy(e->ev_b);
   if (e->ev_k2) cudaEventDestroy(e->ev_k2);
+  if (e->cstream) {
+    cudaStreamSynchronize(e->cstream);
+    cudaStreamDestroy(e->cstream);
+  }
+  for (int k = 0; k < 2; ++k) {
+    if (e->ev_mat[k]) cudaEventDestroy(e->ev_mat[k]);
+    if (e->ev_cp[k]) cudaEventDestroy(e->ev_cp[k]);
+  }
   if (e->ev_e) cudaEventDestroy(e->ev_e);
   for (auto ev : e->ev_q)
     if (ev) cudaEventDestroy(ev);
