@@ -1,8 +1,13 @@
 #!/bin/bash
-mkdir -p gpurun_out
-timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-tail -3 gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -1
-timeout 900 python bench.py > gpurun_out/bench.log 2>&1; grep '^{' gpurun_out/bench.log | tail -1 | cut -c1-300
-timeout 600 python bench.py --n 1048576 --no-cpu-baseline > gpurun_out/bench_2e20.log 2>&1; grep '^{' gpurun_out/bench_2e20.log | tail -1 | cut -c1-200
-timeout 600 python scripts/bench_replications.py --reps 128 > gpurun_out/bench_replications.log 2>&1; tail -1 gpurun_out/bench_replications.log | cut -c1-200
+pj() { python -c "
+import json,sys
+for l in sys.stdin:
+    if l.startswith('{'):
+        d=json.loads(l); print('$1', round(d['value']/1e9,3), 'e2e', round(d['e2e']['value']/1e9,3), d.get('roofline',{}).get('step_kernel_ms'))
+"; }
+for f in 1 0 1 0; do
+  export PF_FUSED_DRAWS=$f; echo "== fd $f"
+  timeout 300 python bench.py --steps 3 --warmup 3 --n 1048576 --no-cpu-baseline > gpurun_out/ab.log 2>&1; pj 2^20 < gpurun_out/ab.log
+done
+unset PF_FUSED_DRAWS
+for b in 32; do for f in 1 0; do PF_FUSED_DRAWS=$f timeout 300 python scripts/bench_replications.py --reps 128 --batch $b | tail -1 | cut -c1-110; done; done
