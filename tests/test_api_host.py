@@ -175,3 +175,29 @@ def test_spacings_resampler_is_accepted_and_needs_power_of_two():
     from paper_1212_1639_b200.filtering import PERF_RESAMPLERS
 
     assert "spacings" in PERF_RESAMPLERS and _lib.RESAMPLER_CODES["spacings"] == 5
+
+
+def test_cuda_tensor_detection_without_a_device():
+    """The kernel-level wrappers take the device-pointer path only for CUDA
+    tensors; numpy arrays and CPU tensors stay on the host-array path."""
+    import numpy as np
+    import torch
+
+    from paper_1212_1639_b200 import _lib
+
+    assert not _lib.is_cuda_tensor(np.ones(4))
+    assert not _lib.is_cuda_tensor(torch.ones(4))
+    assert not _lib.is_cuda_tensor([1.0, 2.0])
+    assert _lib.device_dtype_code(torch.ones(2, dtype=torch.float32)) == _lib.PF_DTYPE_F32
+    assert _lib.device_dtype_code(torch.ones(2, dtype=torch.float64)) == _lib.PF_DTYPE_F64
+
+
+def test_run_replications_batch_rejects_unsupported_options():
+    import numpy as np
+    import pytest
+
+    import paper_1212_1639_b200 as P
+    from paper_1212_1639_b200.replications import run_replications
+
+    with pytest.raises(NotImplementedError):
+        run_replications(P.Priors(), np.zeros(3), 1 << 12, [1, 2], batch=2, store_particles=True)
