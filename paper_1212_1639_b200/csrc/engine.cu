@@ -1566,8 +1566,10 @@ int run_impl(pf_engine* e, const RunSpec& rs) {
         q_select_kernel<<<ntg, 1024, 0, ss>>>(qa, vs, e->qscratch.p, ox, os, ot, t, e->fail.p, e->qunres.p, all);
         g_launches.fetch_add(1);
       }
-      (R > 1 ? q_step_end_kernel<1> : q_step_end_kernel<0>)<<<dim3(1, 1, R), 1024, 0, ss>>>(qa, 1);
-      g_launches.fetch_add(1);
+      if (!fused_resolve) {  // (the fused rounds end the step themselves)
+        (R > 1 ? q_step_end_kernel<1> : q_step_end_kernel<0>)<<<dim3(1, 1, R), 1024, 0, ss>>>(qa, 1);
+        g_launches.fetch_add(1);
+      }
       CK(cudaEventRecord(e->ev_q[t & 1], ss));
     }
     mark(PH_CDF);

@@ -1390,7 +1390,28 @@ q_round_kernel(QArgs qa, QValueSrc vs, double* __restrict__ scratch, double* out
   }
   if (*fail) return;
   const int k = blockIdx.x;
-  if (round && qa.tg[k].status == QS_OK) return;  // resolved in round 0 (uniform over the CTA)
+  // round 1 ends the step for its target (q_step_end_kernel's reset, one
+  // launch fewer on the side chain): target state, its histogram slice, and
+  // (CTA 0) the shared miss / fallback flags -- nothing later in the step
+  // reads them
+  auto end_step = [&]() {
+    __syncthreads();
+    for (int i = threadIdx.x; i < Q_SUB; i += blockDim.x) qa.hist[(size_t)k * Q_SUB + i] = 0ull;
+    if (threadIdx.x == 0) {
+      QTarget& tg = qa.tg[k];
+      tg.missed = 0;
+      tg.count = 0;
+      tg.status = QS_OK;
+      if (k == 0) {
+        qa.sh->any_miss = 0;
+        qa.sh->fb_active[0] = qa.sh->fb_active[1] = 0;
+      }
+    }
+  };
+  if (round && qa.tg[k].status == QS_OK) {  // resolved in round 0 (uniform over the CTA)
+    end_step();
+    return;
+  }
   q_hist_dev(qa, k, round, threadIdx.x, blockDim.x);
   __syncthreads();
   q_locate_dev(qa, k, round);
@@ -1403,6 +1424,7 @@ q_round_kernel(QArgs qa, QValueSrc vs, double* __restrict__ scratch, double* out
     if (threadIdx.x == 0 && qa.tg[k].status != QS_OK) q_prep_target(qa, 0, k);
   } else {
     q_select_dev(qa, vs, scratch, out_x, out_s, out_t, t_step, unresolved, all, k);
+    end_step();
   }
 }
 
