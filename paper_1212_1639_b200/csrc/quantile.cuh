@@ -39,8 +39,18 @@ constexpr int Q_RESOLVE_SMEM = Q_LIST * (8 + 8 + 4);
 // which is cheaper than classifying a few percent of all particles as
 // candidates every step.
 constexpr double Q_H0 = 0.05;
-constexpr double Q_MASS_MIN = 5e-4;
-constexpr double Q_MASS_MAX = 0.006;
+#ifndef PF_Q_MASS_MIN
+#define PF_Q_MASS_MIN 5e-4
+#endif
+#ifndef PF_Q_MASS_MAX
+#define PF_Q_MASS_MAX 0.012
+#endif
+#ifndef PF_Q_MASS_K
+#define PF_Q_MASS_K 6.0
+#endif
+constexpr double Q_MASS_MIN = PF_Q_MASS_MIN;
+constexpr double Q_MASS_MAX = PF_Q_MASS_MAX;
+constexpr double Q_MASS_K = PF_Q_MASS_K;  // half-width in units of the recent prediction error
 
 enum : uint32_t { QS_OK = 0, QS_MISS_LO = 1, QS_MISS_HI = 2, QS_OVERFLOW = 3, QS_CROWD = 4,
                   QS_REFILL = 5, QS_FB = 6, QS_RETRY = 7, QS_LOCATED = 8 };
@@ -947,7 +957,7 @@ PF_D void q_finish_dev(const QArgs& qa, const QValueSrc& vs, double* out_x, doub
       const double phi = fmax(normal_pdf(z), 1e-4);
       const double em = fabs(z - tg.zprev) * phi;
       tg.ema = 0.7 * tg.ema + 0.3 * em;
-      const double mass = fmin(Q_MASS_MAX, fmax(Q_MASS_MIN, 4.0 * fmax(em, tg.ema)));
+      const double mass = fmin(Q_MASS_MAX, fmax(Q_MASS_MIN, Q_MASS_K * fmax(em, tg.ema)));
       tg.h = fmin(2.0, mass / phi);
       tg.zprev = z;
     }
