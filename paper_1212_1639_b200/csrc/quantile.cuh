@@ -40,7 +40,7 @@ constexpr int Q_RESOLVE_SMEM = Q_LIST * (8 + 8 + 4);
 // candidates every step.
 constexpr double Q_H0 = 0.05;
 #ifndef PF_Q_MASS_MIN
-#define PF_Q_MASS_MIN 2.5e-4
+#define PF_Q_MASS_MIN 1.25e-4
 #endif
 #ifndef PF_Q_MASS_MAX
 #define PF_Q_MASS_MAX 0.012

@@ -6,4 +6,3 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1; grep '^{' gpurun_out/bench.log | tail -1 | cut -c1-150
 timeout 600 python bench.py --n 1048576 --no-cpu-baseline > gpurun_out/bench_2e20.log 2>&1; grep '^{' gpurun_out/bench_2e20.log | tail -1 | cut -c1-150
 timeout 600 python scripts/bench_replications.py --reps 128 > gpurun_out/bench_replications.log 2>&1; tail -1 gpurun_out/bench_replications.log | cut -c1-150
-timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1; tail -1 gpurun_out/bench_ref.log | cut -c1-150
